@@ -1,0 +1,242 @@
+/*
+ * gadi_cuda.h — C ABI of the B200-native GADI-IR solver (sm_100a).
+ *
+ * This is the drop-in boundary for the reference's hot path. Every entry
+ * point replaces one piece of the reference's C++ solver API
+ * (/root/reference/proj/core/include/gadi/ headers); the citation is on each
+ * declaration. Plain pointers and sizes only: no C++ types, no exceptions.
+ *
+ *   reference                                   here
+ *   ------------------------------------------  ------------------------------
+ *   gadi_ir_solve(A,b,split,cfg,x0*)            gadi_cuda_create + gadi_cuda_solve
+ *     solver.hpp:97-98                            (+ gadi_cuda_history)
+ *   class GadiSystem (6 virtuals)               gadi_cuda_residual_uf,
+ *     solver.hpp:74-89                            gadi_cuda_true_residual_norm,
+ *                                                 gadi_cuda_prepare,
+ *                                                 gadi_cuda_set_inner_stop_norm,
+ *                                                 gadi_cuda_solve_H, gadi_cuda_solve_S
+ *   GadiConfig / InnerSolverSpec                gadi_config / gadi_inner_spec
+ *     solver.hpp:17-38, inner_solver.hpp:20-25
+ *   SolveReport / SolveStatus                   gadi_report / gadi_status
+ *     solver.hpp:44-64
+ *   hss_split + regularize                      gadi_cuda_create (split is implied:
+ *     splitting.hpp:22-47                         HSS, built on the device)
+ *   build_convdiff3d  problems.hpp:16-42        GADI_PROBLEM_STENCIL7 (matrix free)
+ *   fit / predict_alpha  gpr.hpp:72-87          gadi_gpr_fit / gadi_gpr_predict
+ *
+ * Error convention (reference: solver.hpp:91-92, errors.hpp:9-45): contract and
+ * parameter violations return a negative gadi_error (the C++ wrapper rethrows
+ * them as ContractViolation / ParameterError); numerical outcomes are never
+ * errors, they come back in gadi_report.status exactly as SolveStatus does.
+ * Handles are not thread safe: one handle per host thread (the reference's
+ * GadiSystem instances are also one-per-solve, solver.cpp:241-245).
+ */
+#ifndef GADI_CUDA_H_
+#define GADI_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GADI_ABI_VERSION 1
+
+/* Precision, precision.hpp:14 (same numeric values). */
+typedef enum { GADI_HALF = 0, GADI_SINGLE = 1, GADI_DOUBLE = 2 } gadi_precision;
+
+/* InnerMethod, inner_solver.hpp:15 (same numeric values). LU_DIRECT is the
+ * reference's CPU band LU; it has no device implementation here and is
+ * rejected with GADI_E_UNSUPPORTED (no CPU fallback). */
+typedef enum { GADI_INNER_LU_DIRECT = 0, GADI_INNER_CG = 1, GADI_INNER_GMRES = 2 } gadi_inner_method;
+
+/* Inner arithmetic (extension). NATIVE = every scalar op rounded once to u_r,
+ * dots pairwise in u_r: the reference's semantics (kernels.cpp:33-54,147-177),
+ * bitwise reproducible against it. FP32 = u_r storage with binary32
+ * arithmetic and binary32 pairwise dot accumulation (the north star's
+ * "FP16 storage / FP32 accumulate"); identical to NATIVE when u_r = single. */
+typedef enum { GADI_ACCUM_NATIVE = 0, GADI_ACCUM_FP32 = 1 } gadi_accum;
+
+/* SolveStatus, solver.hpp:44-51 (same numeric values). */
+typedef enum {
+  GADI_CONVERGED = 0,
+  GADI_MAX_ITERS = 1,
+  GADI_DIVERGED = 2,
+  GADI_OVERFLOW_DETECTED = 3,
+  GADI_SINGULAR_IN_PRECISION = 4,
+  GADI_STALLED = 5
+} gadi_status;
+
+/* InnerStatus, inner_solver.hpp:45. */
+typedef enum { GADI_INNER_CONVERGED = 0, GADI_INNER_STAGNATED = 1, GADI_INNER_OVERFLOW = 2 } gadi_inner_status;
+
+typedef enum {
+  GADI_OK = 0,
+  GADI_E_CONTRACT = -1,    /* ContractViolation: shapes, null pointers      */
+  GADI_E_PARAM = -2,       /* ParameterError: alpha, omega, precision order */
+  GADI_E_UNSUPPORTED = -3, /* LU_DIRECT inner, unsupported layout            */
+  GADI_E_FIT = -4,         /* FitError (gpr.hpp:83)                           */
+  GADI_E_CUDA = -5,
+  GADI_E_NCCL = -6,
+  GADI_E_OOM = -7,
+  GADI_E_STATE = -8        /* call order (e.g. solve_H before prepare)        */
+} gadi_error;
+
+/* InnerSolverSpec, inner_solver.hpp:20-25; defaults from gadi_config_default. */
+typedef struct {
+  int32_t method;          /* gadi_inner_method, default LU_DIRECT */
+  double tol_epsilon;      /* default 1e-2 */
+  int32_t max_inner_iters; /* default 1000 */
+  int32_t restart;         /* default 30 (gmres) */
+} gadi_inner_spec;
+
+/* GadiConfig, solver.hpp:17-38, field for field, plus `accum`. */
+typedef struct {
+  double alpha;            /* 1.0 */
+  double omega;            /* 1.0 */
+  double xi;               /* 0 -> default_xi(u), solver.cpp:12-18 */
+  int32_t u_r, u, u_f;     /* gadi_precision; all DOUBLE by default */
+  gadi_inner_spec inner;
+  int32_t max_outer_iters; /* 20000 */
+  double divergence_factor;/* 1e6 */
+  int32_t stall_window;    /* 0 */
+  int32_t ones_start;      /* 0 */
+  int32_t residual_scaling;/* 1 */
+  int32_t accum;           /* gadi_accum, extension: NATIVE */
+} gadi_config;
+
+/* SolveReport, solver.hpp:54-64. The history lives in the handle
+ * (gadi_cuda_history). RoundingStats collapses to the device overflow count. */
+typedef struct {
+  int32_t status;             /* gadi_status */
+  int32_t outer_iters;
+  double final_rres;
+  int64_t inner_iter_totals;
+  int32_t inner_stagnations;
+  int32_t history_len;        /* == outer_iters + 1 */
+  int64_t h_iters, s_iters;   /* split of inner_iter_totals (extension) */
+  double solve_ms;            /* device time of the solve (CUDA events)   */
+  double h_ms, s_ms, outer_ms;/* per-phase device time                    */
+  double h2d_bytes, d2h_bytes;/* bytes the facade copied for this call    */
+} gadi_report;
+
+typedef enum { GADI_PROBLEM_STENCIL7 = 0, GADI_PROBLEM_CSR = 1 } gadi_problem_kind;
+
+/* Problem description. STENCIL7 is the reference's 3D convection-diffusion
+ * operator (problems.cpp:8-43) applied matrix free: grid n^3, row
+ * i*n^2 + j*n + k (i slowest), coefficient t2 on the i-1, j-1, k-1
+ * neighbours, t1 on the diagonal, t3 on k+1, j+1, i+1; the reference fixes
+ * t1 = 6, t2 = -1-r, t3 = -1+r, r = 1/(2n+2) (problems.hpp:16-22); r =
+ * beta*h/2 generalises it. CSR takes the reference's SparseMatrix layout
+ * (sparse.hpp:17-65): int64 row_ptr/col_idx, binary64 values, column indices
+ * strictly increasing per row; host pointers, copied during create. */
+typedef struct {
+  int32_t kind;            /* gadi_problem_kind */
+  int64_t n;               /* STENCIL7: points per direction (N = n^3) */
+  double t1, t2, t3;       /* STENCIL7 coefficients */
+  int64_t n_rows;          /* CSR */
+  int64_t nnz;
+  const int64_t* row_ptr;
+  const int64_t* col_idx;
+  const double* values;
+} gadi_problem_desc;
+
+typedef struct {
+  int32_t device;          /* CUDA ordinal */
+} gadi_device_opts;
+
+typedef struct gadi_handle gadi_handle;
+
+/* Fills the reference defaults (solver.hpp:17-38, inner_solver.hpp:20-25). */
+void gadi_config_default(gadi_config* cfg);
+/* default_xi, solver.cpp:12-18. */
+double gadi_default_xi(int32_t u);
+const char* gadi_status_name(int32_t status);      /* name(SolveStatus), solver.cpp:20-29 */
+const char* gadi_last_error(void);                 /* thread-local message of the last error */
+int32_t gadi_abi_version(void);
+
+/* Build the device operator: A (binary64, fold order of the reference), the
+ * HSS split M = (A+A^T)/2, N = (A-A^T)/2 (splitting.cpp:12-20, pattern union
+ * with explicit zeros, sparse.cpp:166-178). Replaces CsrGadiSystem's
+ * constructor (solver.cpp:185-186) + hss_split. */
+int gadi_cuda_create(const gadi_problem_desc* desc, const gadi_device_opts* opts, gadi_handle** out);
+int gadi_cuda_destroy(gadi_handle* h);
+int gadi_cuda_dim(const gadi_handle* h, int64_t* n);
+
+/* ---- GadiSystem mirror (solver.hpp:74-89); host vectors of length dim, ----
+ * ---- values carried in binary64 exactly like the reference's Vector.   ---- */
+
+/* residual_uf: b - A x entirely in u_f (kernels.cpp:56-69). b is the vector
+ * most recently given to gadi_cuda_set_rhs. */
+int gadi_cuda_set_rhs(gadi_handle* h, const double* b);
+int gadi_cuda_residual_uf(gadi_handle* h, int32_t u_f, const double* x, double* s_out);
+/* true_residual_norm: binary64 ||b - A x||_2 (solver.cpp:194-197). */
+int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_out);
+/* prepare: H = alpha I + M, S = alpha I + N rounded to u_r (splitting.cpp:37-47,
+ * inner_solver.cpp:41-45). LU_DIRECT -> GADI_E_UNSUPPORTED. */
+int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r,
+                      const gadi_inner_spec* spec, int32_t accum);
+int gadi_cuda_set_inner_stop_norm(gadi_handle* h, double stop_norm);
+/* solve_H: CG on H (inner_solver.cpp:47-83); solve_S: GMRES(restart) on S
+ * (inner_solver.cpp:85-194; a CG request degrades to GMRES, solver.cpp:217-221).
+ * rhs must be u_r-representable (it is rounded on upload, as round_vec does). */
+int gadi_cuda_solve_H(gadi_handle* h, const double* rhs, double* x_out, int32_t* iters,
+                      int32_t* inner_status);
+int gadi_cuda_solve_S(gadi_handle* h, const double* rhs, double* x_out, int32_t* iters,
+                      int32_t* inner_status);
+
+/* ---- facade gadi_ir_solve (solver.hpp:97-98; run_gadi_ir solver.cpp:57-179) ---- */
+
+/* Host buffers: b and x0 (nullable: zeros, or ones if cfg->ones_start) are
+ * uploaded, the whole IR loop runs device resident, x is downloaded. */
+int gadi_cuda_solve(gadi_handle* h, const gadi_config* cfg, const double* b, const double* x0,
+                    double* x_out, gadi_report* rep);
+/* Same loop on device-resident binary64 vectors (no host copies). */
+int gadi_cuda_solve_device(gadi_handle* h, const gadi_config* cfg, const double* d_b,
+                           const double* d_x0, double* d_x, gadi_report* rep);
+/* rel_residual_history of the last solve (history[0] = 1); returns the number
+ * of entries written (min(len, cap)). */
+int gadi_cuda_history(const gadi_handle* h, double* out, int32_t cap);
+
+/* ---- operator-level kernels (parity tests; each is one device pass) ---- */
+
+/* which: 0 = A (binary64 fold, kernels.cpp:41-54), 1 = H, 2 = S (after
+ * prepare; fold in the inner arithmetic). y = Op x, host buffers. */
+int gadi_cuda_apply(gadi_handle* h, int32_t which, const double* x, double* y);
+/* Pairwise dot in precision p (kernels.cpp:33-39,84-90,173-177) and the
+ * max-scaled norm2 in p (kernels.cpp:71-82); device kernels, host buffers. */
+int gadi_cuda_dot(int32_t device, int32_t p, const double* x, const double* y, int64_t n,
+                  double* out);
+int gadi_cuda_norm2(int32_t device, int32_t p, const double* x, int64_t n, double* out);
+
+/* ---- synthetic problem data on the device (bench / large parity runs) ---- */
+
+/* x_true_i = lo + (hi-lo) * u(seed, i), u = splitmix64 counter RNG -> 53-bit
+ * uniform in [0,1); b = A x_true with the reference's binary64 fold. Writes
+ * device buffers of length dim. */
+int gadi_cuda_make_rhs(gadi_handle* h, uint64_t seed, double lo, double hi, double* d_xtrue,
+                       double* d_b);
+
+/* ---- GPR alpha predictor (gpr.hpp:60-87; fit gpr.cpp:109-149,
+ * predict_alpha gpr.cpp:151-169) ---- */
+typedef struct {
+  int32_t fixed_hypers;   /* 1: use sigma_f2/length/sigma_n2 as given (C5); 0: the
+                             reference's 27-point grid search */
+  double sigma_f2, length, sigma_n2;
+  int32_t has_sigma_n2;   /* grid mode: FitOptions::sigma_n2 (gpr.hpp:72-75) */
+  int32_t device;
+} gadi_gpr_opts;
+typedef struct gadi_gpr gadi_gpr;
+/* sizes: system dimensions N_i (inputs are ln N_i, gpr.cpp:114); targets alpha_i. */
+int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gadi_gpr_opts* opts,
+                 gadi_gpr** out);
+int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, double* stddev);
+int gadi_gpr_params(const gadi_gpr* g, double* sigma_f2, double* length, double* sigma_n2,
+                    double* lml, double* target_mean);
+int gadi_gpr_destroy(gadi_gpr* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GADI_CUDA_H_ */

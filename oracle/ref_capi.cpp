@@ -1,0 +1,227 @@
+// extern "C" shim over the REFERENCE library compiled from /root/reference
+// (see oracle/Makefile.ref). TEST INFRASTRUCTURE ONLY: it lets the golden-vector
+// generator (tests/golden/make_golden.py) and the oracle-pinning tests call the
+// reference's own code through ctypes. It is never linked into the product.
+//
+// Each entry point forwards to the reference symbol named in its comment.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "gadi/errors.hpp"
+#include "gadi/gpr.hpp"
+#include "gadi/inner_solver.hpp"
+#include "gadi/kernels.hpp"
+#include "gadi/problems.hpp"
+#include "gadi/solver.hpp"
+#include "gadi/splitting.hpp"
+#include "gadi_cuda.h"
+
+using namespace gadi;
+
+namespace {
+
+SparseMatrix csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
+  std::vector<index_t> r(rp, rp + n + 1), c(ci, ci + rp[n]);
+  std::vector<double> vv(v, v + rp[n]);
+  return SparseMatrix(n, n, std::move(r), std::move(c), std::move(vv));
+}
+
+Vector vec(const double* x, int64_t n) { return Vector(x, x + n); }
+
+void out(const Vector& v, double* o) { std::memcpy(o, v.data(), v.size() * sizeof(double)); }
+
+GadiConfig to_cfg(const gadi_config* c) {
+  GadiConfig g;
+  g.alpha = c->alpha;
+  g.omega = c->omega;
+  g.xi = c->xi;
+  g.u_r = static_cast<Precision>(c->u_r);
+  g.u = static_cast<Precision>(c->u);
+  g.u_f = static_cast<Precision>(c->u_f);
+  g.inner.method = static_cast<InnerMethod>(c->inner.method);
+  g.inner.tol_epsilon = c->inner.tol_epsilon;
+  g.inner.max_inner_iters = c->inner.max_inner_iters;
+  g.inner.restart = c->inner.restart;
+  g.max_outer_iters = c->max_outer_iters;
+  g.divergence_factor = c->divergence_factor;
+  g.stall_window = c->stall_window;
+  g.ones_start = c->ones_start != 0;
+  g.residual_scaling = c->residual_scaling != 0;
+  return g;
+}
+
+}  // namespace
+
+extern "C" {
+
+// build_convdiff3d (problems.cpp:8-43): CSR (N+1, 7n^3-6n^2) and b = A*ones.
+int ref_build_convdiff(int64_t n, int64_t* rp, int64_t* ci, double* v, double* b) {
+  try {
+    auto p = build_convdiff3d({n});
+    std::memcpy(rp, p.A.row_ptr().data(), p.A.row_ptr().size() * 8);
+    std::memcpy(ci, p.A.col_idx().data(), p.A.col_idx().size() * 8);
+    std::memcpy(v, p.A.values().data(), p.A.values().size() * 8);
+    out(p.b, b);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// round_to (precision.hpp:81-87)
+int ref_round(const double* x, int64_t n, int p, double* o) {
+  for (int64_t i = 0; i < n; ++i) o[i] = round_to(x[i], static_cast<Precision>(p));
+  return 0;
+}
+
+// matvec (kernels.cpp:124-133)
+int ref_matvec(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* x,
+               int p, double* y) {
+  try {
+    out(matvec(csr(n, rp, ci, v), vec(x, n), static_cast<Precision>(p)), y);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// residual (kernels.cpp:135-145)
+int ref_residual(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                 const double* x, const double* b, int uf, int ur, double* s) {
+  try {
+    out(residual(csr(n, rp, ci, v), vec(x, n), vec(b, n), static_cast<Precision>(uf),
+                 static_cast<Precision>(ur)),
+        s);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+double ref_dot(const double* x, const double* y, int64_t n, int p) {
+  return dot(vec(x, n), vec(y, n), static_cast<Precision>(p));
+}
+double ref_norm2(const double* x, int64_t n, int p) { return norm2(vec(x, n), static_cast<Precision>(p)); }
+double ref_norm2_64(const double* x, int64_t n) { return norm2_64(vec(x, n)); }
+int ref_axpy(double a, const double* x, const double* y, int64_t n, int p, double* o) {
+  out(axpy(a, vec(x, n), vec(y, n), static_cast<Precision>(p)), o);
+  return 0;
+}
+int ref_scale(double a, const double* x, int64_t n, int p, double* o) {
+  out(scale(a, vec(x, n), static_cast<Precision>(p)), o);
+  return 0;
+}
+
+// hss_split + regularize (splitting.cpp:12-20,37-47). Call once with H/S
+// outputs null to get nnz; then with buffers (rp: n+1, ci/vH/vS: nnz).
+int64_t ref_regularize(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, double alpha,
+                       double omega, int64_t* rpH, int64_t* ciH, double* vH, double* vS) {
+  try {
+    auto reg = regularize(hss_split(csr(n, rp, ci, v)), alpha, omega);
+    if (reg.H.col_idx() != reg.S.col_idx() || reg.H.row_ptr() != reg.S.row_ptr()) return -2;
+    if (rpH) {
+      std::memcpy(rpH, reg.H.row_ptr().data(), (n + 1) * 8);
+      std::memcpy(ciH, reg.H.col_idx().data(), reg.H.nnz() * 8);
+      std::memcpy(vH, reg.H.values().data(), reg.H.nnz() * 8);
+      std::memcpy(vS, reg.S.values().data(), reg.S.nnz() * 8);
+    }
+    return reg.H.nnz();
+  } catch (...) {
+    return -1;
+  }
+}
+
+// krylov_solve (inner_solver.cpp:198-204)
+int ref_krylov(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* rhs,
+               int method, double eps, int max_inner, int restart, int fmt, double stop_norm,
+               double* x, int* iters, int* status) {
+  try {
+    InnerSolverSpec spec;
+    spec.method = static_cast<InnerMethod>(method);
+    spec.tol_epsilon = eps;
+    spec.max_inner_iters = max_inner;
+    spec.restart = restart;
+    auto r = krylov_solve(csr(n, rp, ci, v), vec(rhs, n), spec, static_cast<Precision>(fmt), stop_norm);
+    out(r.x, x);
+    *iters = r.iters;
+    *status = static_cast<int>(r.status);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// hss_split + gadi_ir_solve (solver.cpp:250-258)
+int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
+              const double* x0, const gadi_config* cfg, double* x, double* hist, int cap,
+              gadi_report* rep) {
+  try {
+    SparseMatrix A = csr(n, rp, ci, v);
+    Splitting s = hss_split(A);
+    Vector xs;
+    if (x0) xs = vec(x0, n);
+    auto res = gadi_ir_solve(A, vec(b, n), s, to_cfg(cfg), x0 ? &xs : nullptr);
+    out(res.x, x);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = static_cast<int>(res.report.status);
+    rep->outer_iters = res.report.outer_iters;
+    rep->final_rres = res.report.final_rres;
+    rep->inner_iter_totals = res.report.inner_iter_totals;
+    rep->inner_stagnations = res.report.inner_stagnations;
+    rep->history_len = static_cast<int>(res.report.rel_residual_history.size());
+    for (int i = 0; i < rep->history_len && i < cap; ++i) hist[i] = res.report.rel_residual_history[i];
+    return 0;
+  } catch (const ParameterError&) {
+    return GADI_E_PARAM;
+  } catch (const ContractViolation&) {
+    return GADI_E_CONTRACT;
+  } catch (...) {
+    return -99;
+  }
+}
+
+// gadi_reference_solve (solver.cpp:260-331)
+int ref_reference_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                        const double* b, double alpha, double omega, double tol, int max_iters,
+                        double* x, int* outer, int* status) {
+  try {
+    SparseMatrix A = csr(n, rp, ci, v);
+    auto res = gadi_reference_solve(A, vec(b, n), hss_split(A), alpha, omega, tol, max_iters);
+    out(res.x, x);
+    *outer = res.report.outer_iters;
+    *status = static_cast<int>(res.report.status);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
+// fit + predict_alpha (gpr.cpp:109-169). params: sigma_f2, length, sigma_n2, target_mean.
+int ref_gpr(const int64_t* sizes, const double* alphas, int m, int has_sn2, double sn2,
+            const int64_t* qsizes, int q, double* mean, double* sd, double* params) {
+  try {
+    TrainingSet ts;
+    for (int i = 0; i < m; ++i) ts.pairs.push_back({sizes[i], alphas[i], 1});
+    FitOptions o;
+    if (has_sn2) o.sigma_n2 = sn2;
+    GprModel g = fit(ts, o);
+    for (int i = 0; i < q; ++i) {
+      auto [mu, s] = predict_alpha(g, qsizes[i]);
+      mean[i] = mu;
+      sd[i] = s;
+    }
+    params[0] = g.sigma_f2;
+    params[1] = g.length;
+    params[2] = g.sigma_n2;
+    params[3] = g.target_mean;
+    return 0;
+  } catch (const FitError&) {
+    return GADI_E_FIT;
+  } catch (...) {
+    return -1;
+  }
+}
+
+}  // extern "C"
