@@ -1,0 +1,490 @@
+"""B200-native GADI-IR solver (sm_100a) — Python mirror of the reference API.
+
+The compute path is ``libgadi_cuda.so`` (hand-written CUDA for sm_100a, built
+in-tree from ``csrc/``) behind the C ABI in ``include/gadi_cuda.h``. This
+module is a thin ctypes layer that mirrors the reference's C++ surface
+(/root/reference/proj/core/include/gadi/solver.hpp, inner_solver.hpp,
+problems.hpp, gpr.hpp) so that callers and tests read like the reference's:
+
+    reference (C++)                         here (Python)
+    GadiConfig / InnerSolverSpec            GadiConfig / InnerSolverSpec
+    SolveStatus / SolveReport / GadiResult  SolveStatus / SolveReport / GadiResult
+    build_convdiff3d({n})                   build_convdiff3d(n, r=None)  (matrix free)
+    hss_split(A)                            hss_split(A)
+    gadi_ir_solve(A, b, split, cfg, x0)     gadi_ir_solve(A, b, split, cfg, x0)
+    class GadiSystem (6 virtuals)           CudaGadiSystem
+    fit / predict_alpha                     gpr_fit / GprModel.predict
+
+There is no CPU fallback: every entry point raises if the library or a CUDA
+device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgadi_cuda.so")
+
+__all__ = [
+    "Precision", "InnerMethod", "SolveStatus", "InnerStatus", "Accum", "InnerSolverSpec", "GadiConfig",
+    "SolveReport", "GadiResult", "SparseMatrix", "Stencil7", "Splitting", "build_convdiff3d",
+    "hss_split", "gadi_ir_solve", "CudaGadiSystem", "GadiError", "ContractViolation", "ParameterError",
+    "UnsupportedError", "FitError", "default_xi", "lib", "gpr_fit",
+]
+
+
+class Precision(enum.IntEnum):  # precision.hpp:14
+    Half = 0
+    Single = 1
+    Double = 2
+
+
+class InnerMethod(enum.IntEnum):  # inner_solver.hpp:15
+    LuDirect = 0
+    Cg = 1
+    Gmres = 2
+
+
+class SolveStatus(enum.IntEnum):  # solver.hpp:44-51
+    Converged = 0
+    MaxIters = 1
+    Diverged = 2
+    OverflowDetected = 3
+    SingularInPrecision = 4
+    Stalled = 5
+
+
+class InnerStatus(enum.IntEnum):  # inner_solver.hpp:45
+    Converged = 0
+    Stagnated = 1
+    Overflow = 2
+
+
+class Accum(enum.IntEnum):
+    Native = 0  # every op rounded to u_r (the reference's semantics)
+    Fp32 = 1    # u_r storage, binary32 arithmetic and accumulation
+
+
+# ---------------------------------------------------------------- errors
+class GadiError(RuntimeError):
+    code = -5
+
+
+class ContractViolation(GadiError, ValueError):  # errors.hpp:9-12
+    code = -1
+
+
+class ParameterError(ContractViolation):  # errors.hpp:14-16
+    code = -2
+
+
+class UnsupportedError(GadiError):
+    code = -3
+
+
+class FitError(GadiError):  # errors.hpp:40-42
+    code = -4
+
+
+_ERRS = {-1: ContractViolation, -2: ParameterError, -3: UnsupportedError, -4: FitError}
+
+
+# ---------------------------------------------------------------- ctypes structs
+class _InnerSpec(C.Structure):
+    _fields_ = [("method", C.c_int32), ("tol_epsilon", C.c_double),
+                ("max_inner_iters", C.c_int32), ("restart", C.c_int32)]
+
+
+class _Config(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("omega", C.c_double), ("xi", C.c_double),
+                ("u_r", C.c_int32), ("u", C.c_int32), ("u_f", C.c_int32), ("inner", _InnerSpec),
+                ("max_outer_iters", C.c_int32), ("divergence_factor", C.c_double),
+                ("stall_window", C.c_int32), ("ones_start", C.c_int32),
+                ("residual_scaling", C.c_int32), ("accum", C.c_int32)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("status", C.c_int32), ("outer_iters", C.c_int32), ("final_rres", C.c_double),
+                ("inner_iter_totals", C.c_int64), ("inner_stagnations", C.c_int32),
+                ("history_len", C.c_int32), ("h_iters", C.c_int64), ("s_iters", C.c_int64),
+                ("solve_ms", C.c_double), ("h_ms", C.c_double), ("s_ms", C.c_double),
+                ("outer_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
+
+
+class _Problem(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("t1", C.c_double), ("t2", C.c_double),
+                ("t3", C.c_double), ("n_rows", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.POINTER(C.c_int64)), ("col_idx", C.POINTER(C.c_int64)),
+                ("values", C.POINTER(C.c_double))]
+
+
+class _DevOpts(C.Structure):
+    _fields_ = [("device", C.c_int32)]
+
+
+class _GprOpts(C.Structure):
+    _fields_ = [("fixed_hypers", C.c_int32), ("sigma_f2", C.c_double), ("length", C.c_double),
+                ("sigma_n2", C.c_double), ("has_sigma_n2", C.c_int32), ("device", C.c_int32)]
+
+
+_f64p = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+_lib = None
+
+
+def lib():
+    """Load libgadi_cuda.so (built in-tree). Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                          f"(make -C {os.path.join(HERE, 'csrc')}); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    L.gadi_config_default.argtypes = [C.POINTER(_Config)]
+    L.gadi_config_default.restype = None
+    L.gadi_default_xi.restype = C.c_double
+    L.gadi_default_xi.argtypes = [C.c_int32]
+    L.gadi_status_name.restype = C.c_char_p
+    L.gadi_last_error.restype = C.c_char_p
+    L.gadi_abi_version.restype = C.c_int32
+    L.gadi_cuda_create.argtypes = [C.POINTER(_Problem), C.POINTER(_DevOpts), C.POINTER(C.c_void_p)]
+    L.gadi_cuda_destroy.argtypes = [C.c_void_p]
+    L.gadi_cuda_dim.argtypes = [C.c_void_p, _i64p]
+    L.gadi_cuda_set_rhs.argtypes = [C.c_void_p, _f64p]
+    L.gadi_cuda_residual_uf.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p]
+    L.gadi_cuda_true_residual_norm.argtypes = [C.c_void_p, _f64p, _f64p]
+    L.gadi_cuda_prepare.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int32, C.POINTER(_InnerSpec),
+                                    C.c_int32]
+    L.gadi_cuda_set_inner_stop_norm.argtypes = [C.c_void_p, C.c_double]
+    for f in ("gadi_cuda_solve_H", "gadi_cuda_solve_S"):
+        getattr(L, f).argtypes = [C.c_void_p, _f64p, _f64p, _i32p, _i32p]
+    L.gadi_cuda_solve.argtypes = [C.c_void_p, C.POINTER(_Config), _f64p, _f64p, _f64p, C.POINTER(_Report)]
+    L.gadi_cuda_solve_device.argtypes = [C.c_void_p, C.POINTER(_Config), C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.POINTER(_Report)]
+    L.gadi_cuda_history.argtypes = [C.c_void_p, _f64p, C.c_int32]
+    L.gadi_cuda_apply.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p]
+    L.gadi_cuda_dot.argtypes = [C.c_int32, C.c_int32, _f64p, _f64p, C.c_int64, _f64p]
+    L.gadi_cuda_norm2.argtypes = [C.c_int32, C.c_int32, _f64p, C.c_int64, _f64p]
+    L.gadi_cuda_make_rhs.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_void_p, C.c_void_p]
+    L.gadi_gpr_fit.argtypes = [_f64p, _f64p, C.c_int32, C.POINTER(_GprOpts), C.POINTER(C.c_void_p)]
+    L.gadi_gpr_predict.argtypes = [C.c_void_p, _f64p, C.c_int32, _f64p, _f64p]
+    L.gadi_gpr_params.argtypes = [C.c_void_p, _f64p, _f64p, _f64p, _f64p, _f64p]
+    L.gadi_gpr_destroy.argtypes = [C.c_void_p]
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc < 0:
+        msg = lib().gadi_last_error().decode(errors="replace")
+        raise _ERRS.get(rc, GadiError)(f"gadi error {rc}: {msg}")
+    return rc
+
+
+def _p(a, t=_f64p):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- config / report
+@dataclass
+class InnerSolverSpec:  # inner_solver.hpp:20-25
+    method: InnerMethod = InnerMethod.LuDirect
+    tol_epsilon: float = 1e-2
+    max_inner_iters: int = 1000
+    restart: int = 30
+
+    def _c(self):
+        return _InnerSpec(int(self.method), self.tol_epsilon, self.max_inner_iters, self.restart)
+
+
+@dataclass
+class GadiConfig:  # solver.hpp:17-38
+    alpha: float = 1.0
+    omega: float = 1.0
+    xi: float = 0.0
+    u_r: Precision = Precision.Double
+    u: Precision = Precision.Double
+    u_f: Precision = Precision.Double
+    inner: InnerSolverSpec = field(default_factory=InnerSolverSpec)
+    max_outer_iters: int = 20000
+    divergence_factor: float = 1e6
+    stall_window: int = 0
+    ones_start: bool = False
+    residual_scaling: bool = True
+    accum: Accum = Accum.Native  # extension (include/gadi_cuda.h)
+
+    def _c(self):
+        return _Config(self.alpha, self.omega, self.xi, int(self.u_r), int(self.u), int(self.u_f),
+                       self.inner._c(), self.max_outer_iters, self.divergence_factor, self.stall_window,
+                       int(self.ones_start), int(self.residual_scaling), int(self.accum))
+
+
+def default_xi(u: Precision) -> float:  # solver.cpp:12-18
+    return lib().gadi_default_xi(int(u))
+
+
+@dataclass
+class SolveReport:  # solver.hpp:54-64
+    status: SolveStatus = SolveStatus.MaxIters
+    outer_iters: int = 0
+    rel_residual_history: np.ndarray = field(default_factory=lambda: np.ones(1))
+    final_rres: float = 1.0
+    inner_iter_totals: int = 0
+    inner_stagnations: int = 0
+    h_iters: int = 0
+    s_iters: int = 0
+    solve_ms: float = 0.0
+    h_ms: float = 0.0
+    s_ms: float = 0.0
+    h2d_bytes: float = 0.0
+    d2h_bytes: float = 0.0
+
+
+@dataclass
+class GadiResult:  # solver.hpp:66-69
+    x: np.ndarray
+    report: SolveReport
+
+
+# ---------------------------------------------------------------- problems
+class SparseMatrix:
+    """CSR with the reference's layout (sparse.hpp:17-65): int64 row_ptr /
+    col_idx (strictly increasing per row), binary64 values."""
+
+    def __init__(self, n_rows, n_cols, row_ptr, col_idx, values):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.int64)
+        self.col_idx = np.ascontiguousarray(col_idx, np.int64)
+        self.values = _f64(values)
+
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+    def _desc(self):
+        return _Problem(1, 0, 0.0, 0.0, 0.0, self.n_rows, self.nnz(), _p(self.row_ptr, _i64p),
+                        _p(self.col_idx, _i64p), _p(self.values))
+
+
+@dataclass
+class Stencil7:
+    """The 3D convection-diffusion operator of build_convdiff3d
+    (problems.cpp:8-43), matrix free: n per direction, coefficients t1 (diag),
+    t2 (i-1, j-1, k-1), t3 (k+1, j+1, i+1)."""
+    n: int
+    t1: float
+    t2: float
+    t3: float
+
+    @property
+    def n_rows(self):
+        return self.n ** 3
+
+    def _desc(self):
+        return _Problem(0, self.n, self.t1, self.t2, self.t3, 0, 0, None, None, None)
+
+
+def build_convdiff3d(n: int, r: Optional[float] = None, beta: Optional[float] = None) -> Stencil7:
+    """problems.hpp:16-22: t1 = 6, t2 = -1 - r, t3 = -1 + r with r = 1/(2n+2)
+    (beta = 1). beta (BASELINE configs) gives r = beta * h / 2, h = 1/(n+1)."""
+    if r is None:
+        r = (1.0 if beta is None else beta) / (2.0 * n + 2.0)
+    return Stencil7(n, 6.0, -1.0 - r, -1.0 + r)
+
+
+@dataclass
+class Splitting:  # splitting.hpp:17-22; HSS split built on the device
+    A: object
+    kind: str = "hss"
+
+
+def hss_split(A) -> Splitting:
+    """M = (A+A^T)/2, N = (A-A^T)/2 (splitting.cpp:12-20); the device builds it."""
+    return Splitting(A, "hss")
+
+
+# ---------------------------------------------------------------- GadiSystem mirror
+class CudaGadiSystem:
+    """The reference's GadiSystem plugin (solver.hpp:74-89) on the device.
+
+    Holds one handle: the operator A in device memory, its HSS split, and the
+    inner engines built by prepare(). Vectors cross the boundary as binary64
+    numpy arrays like the reference's Vector.
+    """
+
+    def __init__(self, A, b=None, device: int = 0):
+        L = lib()
+        self._h = C.c_void_p()
+        self._A = A
+        desc = A._desc()
+        _check(L.gadi_cuda_create(C.byref(desc), C.byref(_DevOpts(device)), C.byref(self._h)))
+        n = C.c_int64()
+        L.gadi_cuda_dim(self._h, C.byref(n))
+        self.n = n.value
+        if b is not None:
+            self.set_rhs(b)
+
+    def close(self):
+        if self._h:
+            lib().gadi_cuda_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def dim(self):
+        return self.n
+
+    def set_rhs(self, b):
+        self._b = _f64(b)
+        _check(lib().gadi_cuda_set_rhs(self._h, _p(self._b)))
+
+    def residual_uf(self, x, u_f: Precision = Precision.Double):
+        x = _f64(x)
+        s = np.empty(self.n)
+        _check(lib().gadi_cuda_residual_uf(self._h, int(u_f), _p(x), _p(s)))
+        return s
+
+    def true_residual_norm(self, x) -> float:
+        x = _f64(x)
+        out = C.c_double()
+        _check(lib().gadi_cuda_true_residual_norm(self._h, _p(x), C.byref(out)))
+        return out.value
+
+    def prepare(self, alpha, omega, u_r: Precision, spec: InnerSolverSpec, accum: Accum = Accum.Native):
+        _check(lib().gadi_cuda_prepare(self._h, alpha, omega, int(u_r), C.byref(spec._c()), int(accum)))
+
+    def set_inner_stop_norm(self, s):
+        _check(lib().gadi_cuda_set_inner_stop_norm(self._h, s))
+
+    def _inner(self, f, rhs):
+        rhs = _f64(rhs)
+        x = np.empty(self.n)
+        it, st = C.c_int32(), C.c_int32()
+        _check(f(self._h, _p(rhs), _p(x), C.byref(it), C.byref(st)))
+        return x, it.value, InnerStatus(st.value)
+
+    def solve_H(self, rhat):
+        return self._inner(lib().gadi_cuda_solve_H, rhat)
+
+    def solve_S(self, pz):
+        return self._inner(lib().gadi_cuda_solve_S, pz)
+
+    def apply(self, which: str, x):
+        """y = A x (binary64 fold), H x or S x (inner arithmetic, after prepare)."""
+        x = _f64(x)
+        y = np.empty(self.n)
+        _check(lib().gadi_cuda_apply(self._h, {"A": 0, "H": 1, "S": 2}[which], _p(x), _p(y)))
+        return y
+
+    def solve(self, b, cfg: GadiConfig, x0=None) -> GadiResult:
+        """gadi_ir_solve's body (solver.hpp:97-98): host b/x0 in, host x out."""
+        b = _f64(b)
+        x0a = None if x0 is None else _f64(x0)
+        x = np.empty(self.n)
+        rep = _Report()
+        _check(lib().gadi_cuda_solve(self._h, C.byref(cfg._c()), _p(b), _p(x0a), _p(x), C.byref(rep)))
+        return GadiResult(x, self._report(rep))
+
+    def solve_device(self, d_b: int, d_x: int, cfg: GadiConfig, d_x0: int = 0) -> SolveReport:
+        """Same loop on device pointers (e.g. torch tensors' data_ptr())."""
+        rep = _Report()
+        _check(lib().gadi_cuda_solve_device(self._h, C.byref(cfg._c()), C.c_void_p(d_b),
+                                            C.c_void_p(d_x0 or None), C.c_void_p(d_x), C.byref(rep)))
+        return self._report(rep)
+
+    def make_rhs(self, seed: int, lo: float, hi: float, d_xtrue: int, d_b: int):
+        _check(lib().gadi_cuda_make_rhs(self._h, seed, lo, hi, C.c_void_p(d_xtrue), C.c_void_p(d_b)))
+
+    def _report(self, rep: _Report) -> SolveReport:
+        hist = np.empty(max(rep.history_len, 1))
+        got = lib().gadi_cuda_history(self._h, _p(hist), len(hist))
+        return SolveReport(SolveStatus(rep.status), rep.outer_iters, hist[:got].copy(), rep.final_rres,
+                           rep.inner_iter_totals, rep.inner_stagnations, rep.h_iters, rep.s_iters,
+                           rep.solve_ms, rep.h_ms, rep.s_ms, rep.h2d_bytes, rep.d2h_bytes)
+
+
+def gadi_ir_solve(A, b, split: Splitting, cfg: GadiConfig, x0=None, device: int = 0) -> GadiResult:
+    """gadi_ir_solve (solver.hpp:97-98; solver.cpp:250-258) on the device."""
+    if split.A is not A:
+        raise ContractViolation("gadi_ir_solve: split does not belong to A")
+    if len(b) != A.n_rows:
+        raise ContractViolation("gadi_ir_solve: dimension mismatch")  # solver.cpp:252-253
+    sys_ = CudaGadiSystem(A, device=device)
+    try:
+        return sys_.solve(b, cfg, x0)
+    finally:
+        sys_.close()
+
+
+def device_dot(x, y, p: Precision, device=0) -> float:
+    """dot (kernels.cpp:84-90) on the device: rounded products, pairwise sum in p."""
+    x, y = _f64(x), _f64(y)
+    out = C.c_double()
+    _check(lib().gadi_cuda_dot(device, int(p), _p(x), _p(y), len(x), C.byref(out)))
+    return out.value
+
+
+def device_norm2(x, p: Precision, device=0) -> float:
+    """norm2 (kernels.cpp:71-82) with the pairwise sum on the device."""
+    x = _f64(x)
+    out = C.c_double()
+    _check(lib().gadi_cuda_norm2(device, int(p), _p(x), len(x), C.byref(out)))
+    return out.value
+
+
+# ---------------------------------------------------------------- GPR
+class GprModel:
+    def __init__(self, handle):
+        self._h = handle
+
+    def params(self):
+        v = [C.c_double() for _ in range(5)]
+        _check(lib().gadi_gpr_params(self._h, *[C.byref(t) for t in v]))
+        return dict(zip(("sigma_f2", "length", "sigma_n2", "lml", "target_mean"), [t.value for t in v]))
+
+    def predict(self, sizes):
+        sizes = _f64(sizes)
+        mean = np.empty(len(sizes))
+        sd = np.empty(len(sizes))
+        _check(lib().gadi_gpr_predict(self._h, _p(sizes), len(sizes), _p(mean), _p(sd)))
+        return mean, sd
+
+    def close(self):
+        if self._h:
+            lib().gadi_gpr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gpr_fit(sizes, alphas, fixed=None, sigma_n2=None, device=0) -> GprModel:
+    """fit (gpr.cpp:109-149): grid search, or fixed (sigma_f2, length, sigma_n2)."""
+    sizes, alphas = _f64(sizes), _f64(alphas)
+    o = _GprOpts(0, 0.0, 0.0, 0.0, 0, device)
+    if fixed is not None:
+        o.fixed_hypers = 1
+        o.sigma_f2, o.length, o.sigma_n2 = fixed
+    elif sigma_n2 is not None:
+        o.has_sigma_n2, o.sigma_n2 = 1, sigma_n2
+    h = C.c_void_p()
+    _check(lib().gadi_gpr_fit(_p(sizes), _p(alphas), len(sizes), C.byref(o), C.byref(h)))
+    return GprModel(h)
