@@ -1,0 +1,265 @@
+#!/usr/bin/env python
+"""GADI-IR time-to-1e-10 benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2]
+
+A step is one complete GADI-IR solve of the workload's system to relative
+residual 1e-10 (xi = 1e-20): FP64 outer residual/update, inner CG on H and
+GMRES on S on the device. Workloads (BASELINE.json configs):
+  c3 (default, the north star's target): 3D convection-diffusion n=512
+     (N = 134,217,728), beta=100, FP16 storage / FP32 arithmetic inner, FP64
+     outer, alpha=0.3, omega=1, CG/GMRES(30) with eps=1e-12, max_inner=10.
+  c2: n=256 (N = 16,777,216), beta=10, FP32 inner, alpha=0.05, max_inner=20.
+x_true ~ U[-1,1) from the splitmix64 counter RNG (seed 1), b = A x_true in
+binary64 on the device (the same generator the oracle uses).
+
+value  = device time of one solve with b already in HBM (CUDA events inside
+         the library, max over ranks), seconds; lower is better.
+e2e    = the same solve through the C ABI gadi_cuda_solve with HOST buffers
+         (pinned b in, x out; copies inside the timed region).
+roofline = the inner CG sweep (SpMV + axpys + dots, SURVEY §8(d) B_CG =
+         11 N s_r bytes per iteration) against MEASURED_PEAKS.json hbm_gbs.
+Multi-GPU (torchrun): each rank solves its own full-size replica (weak
+scaling); the z-slab partition is not wired into this driver yet.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c3": dict(n=512, beta=100.0, u_r=0, accum=1, alpha=0.3, eps=1e-12, max_inner=10, restart=30,
+               seed=1, lo=-1.0, hi=1.0, s_r=2, name="convdiff3d n=512 beta=100 fp16-storage/fp32-accum inner"),
+    "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.05, eps=1e-12, max_inner=20, restart=30,
+               seed=1, lo=-1.0, hi=1.0, s_r=4, name="convdiff3d n=256 beta=10 fp32 inner"),
+}
+# outer iterations the device solve needs for each workload (measured on B200,
+# profiles/); used only to project the CPU reference's time-to-solution
+OUTER_ITERS = {"c3": 892, "c2": 366}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = sorted(float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()), default=None)
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_reference_sample(wl, threads_note=True):
+    """Time the reference's own CPU implementation (oracle/_ref, built from the
+    reference sources; else the oracle restatement) on a bounded sample: one
+    GADI-IR outer step (CG on H + GMRES on S + residuals, same inner budget and
+    precision class where the reference can run it) at n=64 with the workload's
+    r = beta*h/2, then project per element and per outer step to the workload
+    size and the device's outer-iteration count."""
+    from oracle import CG, Config, Oracle, Reference
+    o = Oracle()
+    use_ref = Reference.available()
+    R = Reference() if use_ref else o
+    ns = 64
+    r = wl["beta"] / (2.0 * (wl["n"] + 1.0))
+    A = o.convdiff(ns, 6.0, -1.0 - r, -1.0 + r)
+    _, b = o.make_rhs(A, wl["seed"], wl["lo"], wl["hi"])
+    # the reference's FP16 Krylov accumulates dots in binary16 and breaks on
+    # overflow at these sizes (SURVEY §0 finding 1); time its FP32 path
+    ur = 1
+    cfg = Config.make(alpha=wl["alpha"], xi=1e-20, u_r=ur, method=CG, tol_epsilon=wl["eps"],
+                      max_inner_iters=wl["max_inner"], restart=wl["restart"], max_outer_iters=1)
+    t = time.perf_counter()
+    R.solve(A, b, cfg)
+    dt = time.perf_counter() - t
+    N_s, N_t = ns ** 3, wl["n"] ** 3
+    per_outer_t = dt * N_t / N_s
+    proj = per_outer_t * OUTER_ITERS[wl_key(wl)]
+    return {
+        "value": proj, "unit": "s", "cores": 1, "kind": "reference" if use_ref else "port",
+        "sample": (f"1 GADI-IR outer step (fp32 CG/GMRES, max_inner={wl['max_inner']}) at n={ns} "
+                   f"(N={N_s}) with r={r:.5f}: {dt:.2f} s; projected x{N_t // N_s} elements and "
+                   f"x{OUTER_ITERS[wl_key(wl)]} outer steps (projected, single-threaded: the "
+                   f"reference has no intra-solve parallelism)"),
+    }
+
+
+def wl_key(wl):
+    for k, v in WORKLOADS.items():
+        if v is wl:
+            return k
+    return "c3"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=list(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "GADI-IR time-to-1e-10 residual"
+    cfg_json = {"workload": wl["name"], "n": wl["n"], "N": wl["n"] ** 3, "beta": wl["beta"],
+                "alpha": wl["alpha"], "omega": 1.0, "inner": "cg(H)/gmres(S)", "max_inner": wl["max_inner"],
+                "tol_epsilon": wl["eps"], "xi": 1e-20, "l2": "inputs larger than L2 (x, b: 8N bytes each)",
+                "parallelism": f"replicas{world}" if world > 1 else "single"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_reference_sample(wl)
+        print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "higher_is_better": False, "dtype": "f64", "data": "synthetic",
+                          "config": cfg_json, "cpu_baseline": cb,
+                          "e2e": {"value": cb["value"], "unit": "s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return
+
+    import torch
+    import paper_2501_04229_b200 as g
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
+    sysx = g.CudaGadiSystem(S, device=local)
+    N = S.n_rows
+    xt = torch.empty(N, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(xt)
+    sysx.make_rhs(wl["seed"] + rank, wl["lo"], wl["hi"], xt.data_ptr(), b.data_ptr())
+    torch.cuda.synchronize()
+    b_h = b.cpu().pin_memory()
+    x_h = torch.empty(N, dtype=torch.float64).pin_memory()
+    cfg = g.GadiConfig(alpha=wl["alpha"], xi=1e-20, u_r=g.Precision(wl["u_r"]), accum=g.Accum(wl["accum"]),
+                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, wl["eps"], wl["max_inner"], wl["restart"]))
+    b_np = b_h.numpy()
+    x_np = x_h.numpy()
+
+    def step():
+        return sysx.solve_into(b_np, x_np, cfg)
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    reps = []
+    l0 = g.lib().gadi_cuda_launch_count(sysx._h)
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            reps.append(step())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    launches = g.lib().gadi_cuda_launch_count(sysx._h) - l0
+    if dist:
+        dist.barrier()
+    solve_s = sum(r.solve_ms for r in reps) / len(reps) / 1e3
+    e2e_s = sum(r.e2e_ms for r in reps) / len(reps) / 1e3
+    h_ms = sum(r.h_ms for r in reps)
+    h_it = sum(r.h_iters for r in reps)
+    ok = all(r.status == g.SolveStatus.Converged for r in reps)
+    x = torch.from_numpy(x_np).cuda()
+    ferr = (torch.linalg.norm(x - xt) / torch.linalg.norm(xt)).item()
+    if dist:
+        t = torch.tensor([solve_s, e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        solve_s, e2e_s = t.tolist()
+    peak, peak_kind = load_peaks()
+    # inner CG sweep: B_CG = 11 N s_r bytes per iteration
+    bytes_it = 11 * N * wl["s_r"]
+    cg_gbs = bytes_it * h_it / (h_ms / 1e3) / 1e9 if h_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("cg_iteration_dram_bytes")
+    out = {
+        "metric": metric, "value": solve_s, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": solve_s * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 outer / " + ("f16 storage, f32 arithmetic" if wl["u_r"] == 0 else "f32")
+        + " inner", "data": "synthetic (seeded splitmix64 x_true, b = A x_true)", "config": cfg_json,
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(reps[0].h2d_bytes),
+                "d2h_bytes_per_step": int(reps[0].d2h_bytes)},
+        "roofline": {"bound": "hbm", "kernel": "inner CG iteration (spmv+p-update, axpys+dots)",
+                     "achieved": cg_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic,
+                     "algorithmic_bytes_per_iter": bytes_it},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "solve": {"converged": ok, "outer_iters": reps[0].outer_iters, "final_rres": reps[0].final_rres,
+                  "forward_rel_err": ferr, "cg_iters": reps[0].h_iters, "gmres_iters": reps[0].s_iters,
+                  "h_ms": reps[0].h_ms, "s_ms": reps[0].s_ms, "outer_ms": reps[0].outer_ms,
+                  "wall_s_per_step": wall / args.steps},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_reference_sample(wl)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    sysx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -119,6 +119,8 @@ typedef struct {
   double solve_ms;            /* device time of the solve (CUDA events)   */
   double h_ms, s_ms, outer_ms;/* per-phase device time                    */
   double h2d_bytes, d2h_bytes;/* bytes the facade copied for this call    */
+  double e2e_ms;              /* gadi_cuda_solve: host b in -> host x out  */
+  int64_t launches;           /* device kernels launched by this call      */
 } gadi_report;
 
 typedef enum { GADI_PROBLEM_STENCIL7 = 0, GADI_PROBLEM_CSR = 1 } gadi_problem_kind;
@@ -198,6 +200,9 @@ int gadi_cuda_solve_device(gadi_handle* h, const gadi_config* cfg, const double*
 /* rel_residual_history of the last solve (history[0] = 1); returns the number
  * of entries written (min(len, cap)). */
 int gadi_cuda_history(const gadi_handle* h, double* out, int32_t cap);
+
+/* Device kernels this handle has launched so far (bench / driver evidence). */
+int64_t gadi_cuda_launch_count(const gadi_handle* h);
 
 /* ---- operator-level kernels (parity tests; each is one device pass) ---- */
 

@@ -62,7 +62,8 @@ class Report(C.Structure):
                 ("inner_iter_totals", C.c_int64), ("inner_stagnations", C.c_int32),
                 ("history_len", C.c_int32), ("h_iters", C.c_int64), ("s_iters", C.c_int64),
                 ("solve_ms", C.c_double), ("h_ms", C.c_double), ("s_ms", C.c_double),
-                ("outer_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
+                ("outer_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("e2e_ms", C.c_double), ("launches", C.c_int64)]
 
 
 class GprOpts(C.Structure):

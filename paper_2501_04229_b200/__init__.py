@@ -114,7 +114,8 @@ class _Report(C.Structure):
                 ("inner_iter_totals", C.c_int64), ("inner_stagnations", C.c_int32),
                 ("history_len", C.c_int32), ("h_iters", C.c_int64), ("s_iters", C.c_int64),
                 ("solve_ms", C.c_double), ("h_ms", C.c_double), ("s_ms", C.c_double),
-                ("outer_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double)]
+                ("outer_ms", C.c_double), ("h2d_bytes", C.c_double), ("d2h_bytes", C.c_double),
+                ("e2e_ms", C.c_double), ("launches", C.c_int64)]
 
 
 class _Problem(C.Structure):
@@ -178,6 +179,8 @@ def lib():
     L.gadi_gpr_predict.argtypes = [C.c_void_p, _f64p, C.c_int32, _f64p, _f64p]
     L.gadi_gpr_params.argtypes = [C.c_void_p, _f64p, _f64p, _f64p, _f64p, _f64p]
     L.gadi_gpr_destroy.argtypes = [C.c_void_p]
+    L.gadi_cuda_launch_count.argtypes = [C.c_void_p]
+    L.gadi_cuda_launch_count.restype = C.c_int64
     _lib = L
     return L
 
@@ -250,6 +253,9 @@ class SolveReport:  # solver.hpp:54-64
     s_ms: float = 0.0
     h2d_bytes: float = 0.0
     d2h_bytes: float = 0.0
+    outer_ms: float = 0.0
+    e2e_ms: float = 0.0
+    launches: int = 0
 
 
 @dataclass
@@ -400,6 +406,16 @@ class CudaGadiSystem:
         _check(lib().gadi_cuda_solve(self._h, C.byref(cfg._c()), _p(b), _p(x0a), _p(x), C.byref(rep)))
         return GadiResult(x, self._report(rep))
 
+    def solve_into(self, b: np.ndarray, x_out: np.ndarray, cfg: GadiConfig, x0=None) -> SolveReport:
+        """solve() into a caller buffer (e.g. pinned host memory); b, x_out
+        must be contiguous float64 arrays of length dim()."""
+        if b.dtype != np.float64 or x_out.dtype != np.float64 or len(b) != self.n or len(x_out) != self.n:
+            raise ContractViolation("solve_into: b and x_out must be float64 of length dim()")
+        x0a = None if x0 is None else _f64(x0)
+        rep = _Report()
+        _check(lib().gadi_cuda_solve(self._h, C.byref(cfg._c()), _p(b), _p(x0a), _p(x_out), C.byref(rep)))
+        return self._report(rep)
+
     def solve_device(self, d_b: int, d_x: int, cfg: GadiConfig, d_x0: int = 0) -> SolveReport:
         """Same loop on device pointers (e.g. torch tensors' data_ptr())."""
         rep = _Report()
@@ -415,7 +431,8 @@ class CudaGadiSystem:
         got = lib().gadi_cuda_history(self._h, _p(hist), len(hist))
         return SolveReport(SolveStatus(rep.status), rep.outer_iters, hist[:got].copy(), rep.final_rres,
                            rep.inner_iter_totals, rep.inner_stagnations, rep.h_iters, rep.s_iters,
-                           rep.solve_ms, rep.h_ms, rep.s_ms, rep.h2d_bytes, rep.d2h_bytes)
+                           rep.solve_ms, rep.h_ms, rep.s_ms, rep.h2d_bytes, rep.d2h_bytes, rep.outer_ms,
+                           rep.e2e_ms, rep.launches)
 
 
 def gadi_ir_solve(A, b, split: Splitting, cfg: GadiConfig, x0=None, device: int = 0) -> GadiResult:

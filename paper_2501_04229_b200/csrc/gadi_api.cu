@@ -1,0 +1,591 @@
+// gadi_api.cu — run_gadi_ir on the device and the C ABI (include/gadi_cuda.h).
+#include "gadi_host.cuh"
+
+using namespace gadi_host;
+
+namespace {
+
+EngineBase* make_engine(gadi_handle* h, const gadi_inner_spec& sp, double a, double om, int ur, int acc) {
+  const bool st = h->stencil();
+  if (ur == GADI_DOUBLE) return (st ? make_engine_st_d64 : make_engine_csr_d64)(h, sp, a, om, ur, acc);
+  if (ur == GADI_SINGLE) return (st ? make_engine_st_f32 : make_engine_csr_f32)(h, sp, a, om, ur, acc);
+  if (acc == GADI_ACCUM_FP32) return (st ? make_engine_st_h32 : make_engine_csr_h32)(h, sp, a, om, ur, acc);
+  return (st ? make_engine_st_h16 : make_engine_csr_h16)(h, sp, a, om, ur, acc);
+}
+
+// ---------------------------------------------------------------- validation
+void validate(const gadi_config* c) {
+  // solver.cpp:33-40
+  if (!(c->alpha > 0.0)) throw Err(GADI_E_PARAM, "alpha must be positive");
+  if (!(c->omega >= 0.0 && c->omega < 2.0)) throw Err(GADI_E_PARAM, "omega must be in [0, 2)");
+  if (c->xi < 0.0) throw Err(GADI_E_PARAM, "xi must be positive");
+  if (c->max_outer_iters < 1) throw Err(GADI_E_PARAM, "max_outer_iters must be >= 1");
+  for (int p : {c->u_r, c->u, c->u_f})
+    if (p < 0 || p > 2) throw Err(GADI_E_PARAM, "unknown precision");
+  const double uu = unit_roundoff(c->u), uf = unit_roundoff(c->u_f), ur = unit_roundoff(c->u_r);
+  if (!(uu <= uf && uf <= ur)) throw Err(GADI_E_PARAM, "precision triple must satisfy u <= u_f <= u_r");
+  if (c->inner.method == GADI_INNER_LU_DIRECT)
+    throw Err(GADI_E_UNSUPPORTED, "inner method lu_direct has no device implementation (use cg or gmres)");
+  if (c->inner.method != GADI_INNER_CG && c->inner.method != GADI_INNER_GMRES)
+    throw Err(GADI_E_PARAM, "unknown inner method");
+  if (c->accum != GADI_ACCUM_NATIVE && c->accum != GADI_ACCUM_FP32) throw Err(GADI_E_PARAM, "unknown accum");
+}
+
+void prepare(gadi_handle* h, double alpha, double omega, int ur, const gadi_inner_spec& sp, int accum) {
+  if (!(alpha > 0.0)) throw Err(GADI_E_PARAM, "regularize: alpha must be positive");
+  if (!(omega >= 0.0 && omega < 2.0)) throw Err(GADI_E_PARAM, "regularize: omega must be in [0, 2)");
+  if (sp.method == GADI_INNER_LU_DIRECT)
+    throw Err(GADI_E_UNSUPPORTED, "inner method lu_direct has no device implementation (use cg or gmres)");
+  if (accum != GADI_ACCUM_NATIVE && accum != GADI_ACCUM_FP32) throw Err(GADI_E_PARAM, "unknown accum");
+  if (sp.restart > 64) throw Err(GADI_E_UNSUPPORTED, "gmres restart > 64");
+  auto& e = h->eng;
+  const bool same = e && e->u_r == ur && e->accum == accum && std::max(1, e->spec.restart) == std::max(1, sp.restart);
+  if (same && e->alpha == alpha && e->omega == omega) {
+    e->spec = sp;
+    return;
+  }
+  e.reset();
+  CK(cudaStreamSynchronize(h->stream));
+  e.reset(make_engine(h, sp, alpha, omega, ur, accum));
+}
+
+double ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// run_gadi_ir (solver.cpp:57-179) on the device vectors h->d_b and h->d_x
+// (x0, rounded to u below).
+void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
+  validate(cfg);
+  const double xi = cfg->xi > 0.0 ? cfg->xi : gadi_default_xi(cfg->u);
+  const int64_t launches0 = h->launches;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->status = GADI_MAX_ITERS;
+  rep->final_rres = 1.0;
+  h->history.assign(1, 1.0);
+  cudaStream_t s = h->stream;
+  const int64_t N = h->N;
+  CK(cudaEventRecord(h->ev0, s));
+  double h_ms = 0, s_ms = 0;
+
+  // x = round_vec(x0, u) (solver.cpp:65)
+  {
+    auto L = [&](auto pt) {
+      constexpr int P = decltype(pt)::v;
+      k_convert<double, double, P><<<ew_grid(N), 256, 0, s>>>(h->d_x, h->d_x, N);
+      ++h->launches;
+    };
+    if (cfg->u == GADI_HALF) L(VecTag<P_HALF>{});
+    else if (cfg->u == GADI_SINGLE) L(VecTag<P_SINGLE>{});
+    CKL();
+  }
+  // nt0 = true_residual_norm(x) (solver.cpp:67)
+  OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
+  read_state(h);
+  const double nt0 = std::sqrt(h->h_st->res_ss);
+  auto finish = [&]() {
+    CK(cudaEventRecord(h->ev1, s));
+    CK(cudaEventSynchronize(h->ev1));
+    rep->solve_ms = ms_between(h->ev0, h->ev1);
+    rep->h_ms = h_ms;
+    rep->s_ms = s_ms;
+    rep->outer_ms = rep->solve_ms - h_ms - s_ms;
+    rep->history_len = (int)h->history.size();
+    rep->launches = h->launches - launches0;
+  };
+  if (nt0 == 0.0) {
+    rep->status = GADI_CONVERGED;
+    rep->final_rres = 0.0;
+    finish();
+    return;
+  }
+  prepare(h, cfg->alpha, cfg->omega, cfg->u_r, cfg->inner, cfg->accum);
+  EngineBase* e = h->eng.get();
+
+  // rounded_scaled_residual (solver.cpp:86-92); when u_f is binary64 the same
+  // pass also yields true_residual_norm (the reference recomputes it).
+  int ex = 0;
+  double tnorm = 0.0, rhat_ss = 0.0;
+  auto rsr = [&]() {
+    OuterA::resid(h, h->d_x, h->d_s, cfg->u_f, cfg->residual_scaling != 0);
+    e->scale_round(h->d_s);
+    read_state(h);
+    ex = h->h_st->res_e;
+    rhat_ss = h->h_st->rhat_ss;
+    if (cfg->u_f != GADI_DOUBLE) {
+      OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
+      read_state(h);
+      tnorm = std::sqrt(h->h_st->res_ss);
+      // keep the scaling exponent of the u_f residual on the device for k_update
+      h->h_st->res_e = ex;
+      CK(cudaMemcpyAsync(&h->st->res_e, &h->h_st->res_e, sizeof(int), cudaMemcpyHostToDevice, s));
+    } else {
+      tnorm = std::sqrt(h->h_st->res_ss);
+    }
+  };
+  rsr();
+  const double g0 = std::ldexp(std::sqrt(rhat_ss), ex);
+  double stop_norm = std::ldexp(g0, -ex);
+  const double p_rounded = hround((2.0 - cfg->omega) * cfg->alpha, cfg->u_r);
+
+  double best = 1.0;
+  int best_iter = 0;
+  for (int k = 0;; ++k) {
+    const double rres = h->history.back();
+    rep->final_rres = rres;
+    rep->outer_iters = k;
+    const double gn = std::ldexp(std::sqrt(rhat_ss), ex);
+    const bool guard = gn * gn <= g0 * g0 * xi;
+    const bool truem = rres * rres <= xi;
+    if (guard && truem) { rep->status = GADI_CONVERGED; break; }
+    if (guard) { rep->status = GADI_STALLED; break; }
+    if (!std::isfinite(rres)) { rep->status = GADI_OVERFLOW_DETECTED; break; }
+    if (rres > cfg->divergence_factor) { rep->status = GADI_DIVERGED; break; }
+    if (cfg->stall_window > 0) {
+      if (rres < best * (1.0 - 1e-3)) {
+        best = rres;
+        best_iter = k;
+      } else if (k - best_iter >= cfg->stall_window) {
+        rep->status = GADI_STALLED;
+        break;
+      }
+    }
+    if (k >= cfg->max_outer_iters) { rep->status = GADI_MAX_ITERS; break; }
+
+    const double target = cfg->inner.tol_epsilon * stop_norm;
+    CK(cudaEventRecord(h->evA, s));
+    // solve_H uses the spec method (solver.cpp:212-216)
+    InnerOut zo = cfg->inner.method == GADI_INNER_CG ? e->cg(1, e->rhat, e->z, target)
+                                                     : e->gmres(1, e->rhat, e->z, target);
+    CK(cudaEventRecord(h->evB, s));
+    rep->inner_iter_totals += zo.iters;
+    rep->h_iters += zo.iters;
+    if (zo.status == INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
+    if (zo.status == INNER_STAGNATED) ++rep->inner_stagnations;
+    e->scale_pz(p_rounded);
+    // solve_S: a cg request degrades to gmres (solver.cpp:217-221)
+    InnerOut yo = e->gmres(2, e->pz, e->y, target);
+    CK(cudaEventRecord(h->evC, s));
+    rep->inner_iter_totals += yo.iters;
+    rep->s_iters += yo.iters;
+    if (yo.status == INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
+    if (yo.status == INNER_STAGNATED) ++rep->inner_stagnations;
+
+    // x <- x + 2^e y in u (solver.cpp:163-166), non-finite check (:168-174)
+    CK(cudaMemsetAsync(&h->st->xbad, 0, 4, s));
+    e->update(h->d_x, cfg->u);
+    rsr();  // syncs: also closes the H/S timing events
+    h_ms += ms_between(h->evA, h->evB);
+    s_ms += ms_between(h->evB, h->evC);
+    if (h->h_st->xbad) {
+      OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
+      read_state(h);
+      h->history.push_back(std::sqrt(h->h_st->res_ss) / nt0);
+      rep->outer_iters = k + 1;
+      rep->final_rres = h->history.back();
+      rep->status = GADI_OVERFLOW_DETECTED;
+      break;
+    }
+    stop_norm = std::ldexp(g0, -ex);
+    h->history.push_back(tnorm / nt0);
+  }
+  finish();
+}
+
+int fail(const Err& e) {
+  g_last_error = e.what();
+  return e.code;
+}
+
+#define API_BEGIN try {
+#define API_END                                \
+  }                                            \
+  catch (const Err& e) {                       \
+    return fail(e);                            \
+  }                                            \
+  catch (const std::bad_alloc&) {              \
+    g_last_error = "host allocation failed";   \
+    return GADI_E_OOM;                         \
+  }                                            \
+  catch (const std::exception& e) {            \
+    g_last_error = e.what();                   \
+    return GADI_E_CUDA;                        \
+  }                                            \
+  return GADI_OK;
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+void gadi_config_default(gadi_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->alpha = 1.0;
+  c->omega = 1.0;
+  c->xi = 0.0;
+  c->u_r = c->u = c->u_f = GADI_DOUBLE;
+  c->inner.method = GADI_INNER_LU_DIRECT;
+  c->inner.tol_epsilon = 1e-2;
+  c->inner.max_inner_iters = 1000;
+  c->inner.restart = 30;
+  c->max_outer_iters = 20000;
+  c->divergence_factor = 1e6;
+  c->stall_window = 0;
+  c->ones_start = 0;
+  c->residual_scaling = 1;
+  c->accum = GADI_ACCUM_NATIVE;
+}
+
+double gadi_default_xi(int32_t u) {
+  switch (u) {
+    case GADI_DOUBLE: return 1e-26;
+    case GADI_SINGLE: return 1e-8;
+    default: return 1e-4;
+  }
+}
+
+const char* gadi_status_name(int32_t s) {
+  switch (s) {
+    case GADI_CONVERGED: return "Converged";
+    case GADI_MAX_ITERS: return "MaxIters";
+    case GADI_DIVERGED: return "Diverged";
+    case GADI_OVERFLOW_DETECTED: return "OverflowDetected";
+    case GADI_SINGULAR_IN_PRECISION: return "SingularInPrecision";
+    default: return "Stalled";
+  }
+}
+
+const char* gadi_last_error(void) { return g_last_error.c_str(); }
+int32_t gadi_abi_version(void) { return GADI_ABI_VERSION; }
+
+int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_handle** out) {
+  API_BEGIN
+  if (!d || !out) throw Err(GADI_E_CONTRACT, "gadi_cuda_create: null argument");
+  *out = nullptr;
+  std::unique_ptr<gadi_handle> h(new gadi_handle());
+  h->device = opts ? opts->device : 0;
+  CK(cudaSetDevice(h->device));
+  h->kind = d->kind;
+  if (d->kind == GADI_PROBLEM_STENCIL7) {
+    if (d->n < 2) throw Err(GADI_E_CONTRACT, "convdiff3d: n >= 2 required");  // problems.cpp:10
+    h->n = d->n;
+    h->N = d->n * d->n * d->n;
+    h->t1 = d->t1;
+    h->t2 = d->t2;
+    h->t3 = d->t3;
+  } else if (d->kind == GADI_PROBLEM_CSR) {
+    const int64_t n = d->n_rows;
+    if (n < 1 || !d->row_ptr || !d->col_idx || !d->values) throw Err(GADI_E_CONTRACT, "csr: bad arguments");
+    if (n >= (int64_t(1) << 31)) throw Err(GADI_E_UNSUPPORTED, "csr: n_rows must be < 2^31");
+    const int64_t* rp = d->row_ptr;
+    if (rp[0] != 0 || rp[n] != d->nnz) throw Err(GADI_E_CONTRACT, "row_ptr must start at 0 and end at nnz");
+    for (int64_t i = 0; i < n; ++i) {  // sparse.cpp:19-34
+      if (rp[i] > rp[i + 1]) throw Err(GADI_E_CONTRACT, "row_ptr must be non-decreasing");
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+        if (d->col_idx[k] < 0 || d->col_idx[k] >= n) throw Err(GADI_E_CONTRACT, "column index out of range");
+        if (k > rp[i] && d->col_idx[k] <= d->col_idx[k - 1])
+          throw Err(GADI_E_CONTRACT, "column indices must be strictly increasing within a row");
+      }
+    }
+    h->N = n;
+    h->nnzA = d->nnz;
+    std::vector<int32_t> ci32(d->col_idx, d->col_idx + d->nnz);
+    h->d_rpA = dalloc<int64_t>(n + 1);
+    h->d_ciA = dalloc<int32_t>(d->nnz);
+    h->d_vA = dalloc<double>(d->nnz);
+    CK(cudaMemcpy(h->d_rpA, rp, (n + 1) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_ciA, ci32.data(), d->nnz * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_vA, d->values, d->nnz * 8, cudaMemcpyHostToDevice));
+    HostCsr P;
+    hss_split_host(n, rp, d->col_idx, d->values, P, h->Mv, h->Nv, h->diag_in);
+    h->nnzHS = P.rp[n];
+    h->diag_pos.resize(n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k)
+        if (P.ci[k] == i) h->diag_pos[i] = k;
+    std::vector<int32_t> hci(P.ci.begin(), P.ci.end());
+    h->d_rpHS = dalloc<int64_t>(n + 1);
+    h->d_ciHS = dalloc<int32_t>(h->nnzHS);
+    CK(cudaMemcpy(h->d_rpHS, P.rp.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_ciHS, hci.data(), h->nnzHS * 4, cudaMemcpyHostToDevice));
+  } else {
+    throw Err(GADI_E_CONTRACT, "unknown problem kind");
+  }
+  CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  const int64_t N = h->N;
+  h->d_x = dalloc<double>(N);
+  h->d_b = dalloc<double>(N);
+  h->d_s = dalloc<double>(N);
+  h->d_t64 = dalloc<double>(N);
+  CK(cudaMemset(h->d_b, 0, N * 8));
+  h->st = dalloc<DevState>(1);
+  CK(cudaMemset(h->st, 0, sizeof(DevState)));
+  CK(cudaHostAlloc(&h->h_st, sizeof(DevState), cudaHostAllocDefault));
+  std::memset(h->h_st, 0, sizeof(DevState));
+  const int64_t maxblk = std::max<int64_t>(N / 64, 1) + 8;
+  h->d_part0 = dalloc<double>(maxblk);
+  h->d_part1 = dalloc<double>(maxblk);
+  h->d_ticket = dalloc<unsigned>(1);
+  CK(cudaMemset(h->d_ticket, 0, sizeof(unsigned)));
+  CK(cudaHostAlloc(&h->h_done, sizeof(int), cudaHostAllocMapped));
+  *h->h_done = 0;
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->d_h_done), h->h_done, 0));
+  CK(cudaMemcpy(&h->st->hdone, &h->d_h_done, sizeof(int*), cudaMemcpyHostToDevice));
+  for (cudaEvent_t* ev : {&h->ev0, &h->ev1, &h->evA, &h->evB, &h->evC}) CK(cudaEventCreate(ev));
+  h->ring.resize(4);
+  for (auto& ev : h->ring) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  *out = h.release();
+  API_END
+}
+
+int gadi_cuda_destroy(gadi_handle* h) {
+  if (!h) return GADI_OK;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  h->eng.reset();
+  for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_rpHS, (void*)h->d_ciHS,
+                  (void*)h->d_x, (void*)h->d_b, (void*)h->d_s, (void*)h->d_t64, (void*)h->st,
+                  (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_ticket})
+    if (p) cudaFree(p);
+  if (h->h_st) cudaFreeHost(h->h_st);
+  if (h->h_done) cudaFreeHost(h->h_done);
+  for (cudaEvent_t ev : {h->ev0, h->ev1, h->evA, h->evB, h->evC})
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : h->ring) cudaEventDestroy(ev);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return GADI_OK;
+}
+
+int gadi_cuda_dim(const gadi_handle* h, int64_t* n) {
+  if (!h || !n) return GADI_E_CONTRACT;
+  *n = h->N;
+  return GADI_OK;
+}
+
+int gadi_cuda_set_rhs(gadi_handle* h, const double* b) {
+  API_BEGIN
+  if (!h || !b) throw Err(GADI_E_CONTRACT, "set_rhs: null argument");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(h->d_b, b, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int gadi_cuda_residual_uf(gadi_handle* h, int32_t u_f, const double* x, double* s_out) {
+  API_BEGIN
+  if (!h || !x || !s_out) throw Err(GADI_E_CONTRACT, "residual_uf: null argument");
+  if (u_f < 0 || u_f > 2) throw Err(GADI_E_PARAM, "unknown precision");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
+  OuterA::resid(h, h->d_t64, h->d_s, u_f, false);
+  CK(cudaMemcpyAsync(s_out, h->d_s, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_out) {
+  API_BEGIN
+  if (!h || !x || !norm_out) throw Err(GADI_E_CONTRACT, "true_residual_norm: null argument");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
+  OuterA::resid(h, h->d_t64, nullptr, GADI_DOUBLE, false);
+  read_state(h);
+  *norm_out = std::sqrt(h->h_st->res_ss);
+  API_END
+}
+
+int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r, const gadi_inner_spec* spec,
+                      int32_t accum) {
+  API_BEGIN
+  if (!h || !spec) throw Err(GADI_E_CONTRACT, "prepare: null argument");
+  if (u_r < 0 || u_r > 2) throw Err(GADI_E_PARAM, "unknown precision");
+  CK(cudaSetDevice(h->device));
+  prepare(h, alpha, omega, u_r, *spec, accum);
+  API_END
+}
+
+int gadi_cuda_set_inner_stop_norm(gadi_handle* h, double stop_norm) {
+  if (!h) return GADI_E_CONTRACT;
+  h->stop_norm = stop_norm;
+  return GADI_OK;
+}
+
+static int inner_call(gadi_handle* h, int which, const double* rhs, double* x_out, int32_t* iters,
+                      int32_t* status) {
+  API_BEGIN
+  if (!h || !rhs || !x_out) throw Err(GADI_E_CONTRACT, "solve: null argument");
+  if (!h->eng) throw Err(GADI_E_STATE, "solve_H/solve_S before prepare");
+  CK(cudaSetDevice(h->device));
+  EngineBase* e = h->eng.get();
+  CK(cudaMemcpyAsync(h->d_t64, rhs, h->N * 8, cudaMemcpyHostToDevice, h->stream));
+  e->to_inner(h->d_t64, e->rhat);
+  const double target = e->spec.tol_epsilon * h->stop_norm;
+  InnerOut o;
+  if (which == 1 && e->spec.method == GADI_INNER_CG) o = e->cg(1, e->rhat, e->z, target);
+  else o = e->gmres(which, e->rhat, e->z, target);
+  e->to_double(e->z, h->d_t64);
+  CK(cudaMemcpyAsync(x_out, h->d_t64, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (iters) *iters = o.iters;
+  if (status) *status = o.status;
+  API_END
+}
+
+int gadi_cuda_solve_H(gadi_handle* h, const double* rhs, double* x_out, int32_t* iters, int32_t* status) {
+  return inner_call(h, 1, rhs, x_out, iters, status);
+}
+int gadi_cuda_solve_S(gadi_handle* h, const double* rhs, double* x_out, int32_t* iters, int32_t* status) {
+  return inner_call(h, 2, rhs, x_out, iters, status);
+}
+
+int gadi_cuda_solve(gadi_handle* h, const gadi_config* cfg, const double* b, const double* x0, double* x_out,
+                    gadi_report* rep) {
+  API_BEGIN
+  if (!h || !cfg || !b || !x_out || !rep) throw Err(GADI_E_CONTRACT, "solve: null argument");
+  CK(cudaSetDevice(h->device));
+  validate(cfg);
+  // e2e: timed from the host copy of b to the host copy of x
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, h->stream));
+  CK(cudaMemcpyAsync(h->d_b, b, h->N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  double h2d = (double)h->N * 8;
+  if (x0) {
+    CK(cudaMemcpyAsync(h->d_x, x0, h->N * 8, cudaMemcpyHostToDevice, h->stream));
+    h2d += (double)h->N * 8;
+  } else {
+    k_fill<<<ew_grid(h->N), 256, 0, h->stream>>>(h->d_x, cfg->ones_start ? 1.0 : 0.0, h->N);
+    CKL();
+    ++h->launches;
+  }
+  const int64_t l0 = h->launches;
+  run(h, cfg, rep);
+  CK(cudaMemcpyAsync(x_out, h->d_x, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaEventRecord(e1, h->stream));
+  CK(cudaEventSynchronize(e1));
+  rep->e2e_ms = ms_between(e0, e1);
+  rep->h2d_bytes = h2d;
+  rep->d2h_bytes = (double)h->N * 8;
+  rep->launches = h->launches - l0 + (x0 ? 0 : 1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  API_END
+}
+
+int gadi_cuda_solve_device(gadi_handle* h, const gadi_config* cfg, const double* d_b, const double* d_x0,
+                           double* d_x, gadi_report* rep) {
+  API_BEGIN
+  if (!h || !cfg || !d_b || !d_x || !rep) throw Err(GADI_E_CONTRACT, "solve_device: null argument");
+  CK(cudaSetDevice(h->device));
+  validate(cfg);
+  CK(cudaMemcpyAsync(h->d_b, d_b, h->N * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  if (d_x0) {
+    CK(cudaMemcpyAsync(h->d_x, d_x0, h->N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    k_fill<<<ew_grid(h->N), 256, 0, h->stream>>>(h->d_x, cfg->ones_start ? 1.0 : 0.0, h->N);
+    CKL();
+    ++h->launches;
+  }
+  run(h, cfg, rep);
+  CK(cudaMemcpyAsync(d_x, h->d_x, h->N * 8, cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int gadi_cuda_history(const gadi_handle* h, double* out, int32_t cap) {
+  if (!h || (!out && cap > 0)) return GADI_E_CONTRACT;
+  const int n = (int)std::min<size_t>(h->history.size(), (size_t)std::max(cap, 0));
+  for (int i = 0; i < n; ++i) out[i] = h->history[i];
+  return n;
+}
+
+int gadi_cuda_apply(gadi_handle* h, int32_t which, const double* x, double* y) {
+  API_BEGIN
+  if (!h || !x || !y) throw Err(GADI_E_CONTRACT, "apply: null argument");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
+  if (which == 0) {
+    OuterA::apply(h, h->d_t64, h->d_s);
+    CK(cudaMemcpyAsync(y, h->d_s, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    if (!h->eng) throw Err(GADI_E_STATE, "apply H/S before prepare");
+    EngineBase* e = h->eng.get();
+    e->to_inner(h->d_t64, e->rhat);
+    e->apply(which, e->rhat, e->z);
+    e->to_double(e->z, h->d_s);
+    CK(cudaMemcpyAsync(y, h->d_s, h->N * 8, cudaMemcpyDeviceToHost, h->stream));
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int64_t gadi_cuda_launch_count(const gadi_handle* h) { return h ? h->launches : 0; }
+
+static int reduce_test(int32_t device, int32_t p, const double* x, const double* y, int64_t n, double* out,
+                       bool norm) {
+  API_BEGIN
+  if (!x || !out || n < 0) throw Err(GADI_E_CONTRACT, "dot: bad argument");
+  if (p < 0 || p > 2) throw Err(GADI_E_PARAM, "unknown precision");
+  CK(cudaSetDevice(device));
+  if (n == 0) {
+    *out = 0.0;
+    return GADI_OK;
+  }
+  std::vector<double> xs(x, x + n), ys;
+  double m = 0.0;
+  if (norm) {  // norm2 = m * sqrt(pairwise(round(round(x/m)^2))) (kernels.cpp:71-82)
+    for (double v : xs)
+      if (m < std::fabs(v)) m = std::fabs(v);
+    if (m == 0.0 || !std::isfinite(m)) {
+      *out = m;
+      return GADI_OK;
+    }
+    for (double& v : xs) v = hround(v / m, p);
+    ys = xs;
+  } else {
+    ys.assign(y, y + n);
+  }
+  double *dx = dalloc<double>(n), *dy = dalloc<double>(n), *dout = dalloc<double>(1);
+  const Geo g = make_geo(n, 1);
+  double *p0 = dalloc<double>(g.nblk + 1), *p1 = dalloc<double>(g.nblk + 1);
+  unsigned* tk = dalloc<unsigned>(1);
+  CK(cudaMemset(tk, 0, 4));
+  CK(cudaMemcpy(dx, xs.data(), n * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dy, ys.data(), n * 8, cudaMemcpyHostToDevice));
+  Red rd{p0, p1, tk};
+  if (p == GADI_HALF) k_dot_d<__half><<<g.nblk, g.threads()>>>(dx, dy, g, rd, dout);
+  else if (p == GADI_SINGLE) k_dot_d<float><<<g.nblk, g.threads()>>>(dx, dy, g, rd, dout);
+  else k_dot_d<double><<<g.nblk, g.threads()>>>(dx, dy, g, rd, dout);
+  CKL();
+  double r = 0;
+  CK(cudaMemcpy(&r, dout, 8, cudaMemcpyDeviceToHost));
+  for (void* q : {(void*)dx, (void*)dy, (void*)dout, (void*)p0, (void*)p1, (void*)tk}) cudaFree(q);
+  *out = norm ? hround(m * hround(std::sqrt(r), p), p) : r;
+  API_END
+}
+
+int gadi_cuda_dot(int32_t device, int32_t p, const double* x, const double* y, int64_t n, double* out) {
+  if (!y) return GADI_E_CONTRACT;
+  return reduce_test(device, p, x, y, n, out, false);
+}
+int gadi_cuda_norm2(int32_t device, int32_t p, const double* x, int64_t n, double* out) {
+  return reduce_test(device, p, x, nullptr, n, out, true);
+}
+
+int gadi_cuda_make_rhs(gadi_handle* h, uint64_t seed, double lo, double hi, double* d_xtrue, double* d_b) {
+  API_BEGIN
+  if (!h || !d_xtrue || !d_b) throw Err(GADI_E_CONTRACT, "make_rhs: null argument");
+  CK(cudaSetDevice(h->device));
+  k_uniform<<<ew_grid(h->N), 256, 0, h->stream>>>(d_xtrue, seed, lo, hi, h->N);
+  CKL();
+  ++h->launches;
+  OuterA::apply(h, d_xtrue, d_b);
+  CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,8 @@
+// Instantiates the Stencil7 engine with storage double, arithmetic double.
+#include "gadi_host.cuh"
+
+namespace gadi_host {
+GADI_ENGINE_FACTORY(make_engine_st_d64) {
+  return new Engine<Stencil7<double>, double, double>(h, sp, a, om, ur, acc);
+}
+}  // namespace gadi_host

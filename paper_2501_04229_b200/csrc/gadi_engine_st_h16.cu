@@ -1,0 +1,8 @@
+// Instantiates the Stencil7 engine with storage __half, arithmetic __half.
+#include "gadi_host.cuh"
+
+namespace gadi_host {
+GADI_ENGINE_FACTORY(make_engine_st_h16) {
+  return new Engine<Stencil7<__half>, __half, __half>(h, sp, a, om, ur, acc);
+}
+}  // namespace gadi_host

@@ -1,0 +1,676 @@
+// gadi_host.cuh — host-side engine of the B200 GADI-IR solver (shared by the
+// per-format translation units gadi_engine_*.cu and the C ABI in gadi_api.cu).
+//
+// run_gadi_ir (solver.cpp:57-179) is restated over device-resident vectors:
+// x, b, s in binary64, the inner vectors in u_r storage. Per outer step the
+// host issues CG on H, the p-scaling, GMRES on S, the update and the new
+// residual. Inside CG the host only keeps the launch queue a few iterations
+// ahead of the device (the recurrences and stop tests run on the device,
+// gadi_kernels.cuh); GMRES reads one small Hessenberg column per Arnoldi step
+// (the Givens rotations run on the host in the inner format's rounding).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gadi_cuda.h"
+#include "gadi_kernels.cuh"
+
+using namespace gadi;
+
+namespace gadi_host {
+
+inline thread_local std::string g_last_error;
+
+struct Err : std::runtime_error {
+  int code;
+  Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(x)                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess)                                                                        \
+      throw Err(e_ == cudaErrorMemoryAllocation ? GADI_E_OOM : GADI_E_CUDA,                       \
+                std::string(#x) + ": " + cudaGetErrorString(e_));                                 \
+  } while (0)
+
+#define CKL() CK(cudaGetLastError())
+
+// ---------------------------------------------------------------- host rounding
+// round_to (precision.hpp:54-87): one RNE rounding of a binary64 to binary16 /
+// binary32, used for the Givens/back-solve scalars that run on the host.
+inline double hround(double x, int p) {
+  if (p == GADI_SINGLE) return (double)(float)x;
+  if (p != GADI_HALF) return x;
+  if (std::isnan(x) || std::isinf(x) || x == 0.0) return x;
+  const double ax = std::fabs(x);
+  if (ax >= 65520.0) return std::copysign(INFINITY, x);
+  const int e = std::ilogb(ax);
+  const int q = e < -14 ? -24 : e - 10;
+  return std::copysign(std::ldexp(std::nearbyint(std::ldexp(ax, -q)), q), x);
+}
+
+inline double unit_roundoff(int p) {
+  return p == GADI_HALF ? std::ldexp(1.0, -11) : p == GADI_SINGLE ? std::ldexp(1.0, -24) : std::ldexp(1.0, -53);
+}
+
+inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+inline int ilog2(int64_t v) {
+  int d = 0;
+  while ((int64_t(1) << (d + 1)) <= v) ++d;
+  return d;
+}
+
+// 2^D segments -> lanes x warps x segments-per-lane x blocks (gadi_kernels.cuh).
+// Up to RMAX segments per lane while that still leaves >= 4 blocks per SM.
+inline Geo make_geo(int64_t N, int vec) {
+  Geo g;
+  g.N = N;
+  int64_t nseg;
+  if (vec > 1) {
+    nseg = N / vec;
+    g.D = ilog2(nseg);
+  } else {
+    g.D = N < 4 ? 0 : ilog2(N) - 1;
+    nseg = int64_t(1) << g.D;
+  }
+  g.L = (int)std::min<int64_t>(32, nseg);
+  g.W = (int)std::min<int64_t>(8, nseg / g.L);
+  g.R = RMAX;
+  while (g.R > 1 && nseg / ((int64_t)g.L * g.W * g.R) < 592) g.R /= 2;
+  g.nblk = (int)(nseg / ((int64_t)g.L * g.W * g.R));
+  return g;
+}
+
+inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
+  return (N % vec == 0) && is_pow2(N / vec) && (!stencil || n % vec == 0);
+}
+
+template <int V>
+struct VecTag {
+  static constexpr int v = V;
+};
+
+inline dim3 ew_grid(int64_t n) { return dim3((unsigned)((n + 255) / 256)); }
+
+template <class T>
+constexpr int prec_of() {
+  return std::is_same<T, __half>::value ? GADI_HALF : std::is_same<T, float>::value ? GADI_SINGLE : GADI_DOUBLE;
+}
+
+// ---------------------------------------------------------------- the problem
+struct HostCsr {
+  std::vector<int64_t> rp, ci;
+};
+
+// hss_split (splitting.cpp:12-20) on the host for the CSR path: union pattern
+// of A and A^T, M = (A + A^T)/2, N = (A - A^T)/2 with explicit zeros (the
+// duplicate summation of from_triplets, sparse.cpp:36-58,166-178), plus the
+// diagonal in the pattern (shift_diagonal, sparse.cpp:180-183). diag_in
+// records whether the diagonal was already in M's own pattern.
+inline void hss_split_host(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, HostCsr& P,
+                    std::vector<double>& Mv, std::vector<double>& Nv, std::vector<uint8_t>& diag_in) {
+  const int64_t nnz = rp[n];
+  std::vector<int64_t> trp(n + 1, 0), tci(nnz), next(n);
+  std::vector<double> tv(nnz);
+  for (int64_t k = 0; k < nnz; ++k) ++trp[ci[k] + 1];
+  for (int64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
+  for (int64_t j = 0; j < n; ++j) next[j] = trp[j];
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int64_t q = next[ci[k]]++;
+      tci[q] = i;
+      tv[q] = v[k];
+    }
+  P.rp.assign(n + 1, 0);
+  P.ci.clear();
+  Mv.clear();
+  Nv.clear();
+  diag_in.clear();
+  P.ci.reserve(nnz + n);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t a = rp[i], ae = rp[i + 1], t = trp[i], te = trp[i + 1];
+    bool diag_done = false;
+    while (a < ae || t < te || !diag_done) {
+      const int64_t ca = a < ae ? ci[a] : INT64_MAX, ct = t < te ? tci[t] : INT64_MAX;
+      int64_t col = std::min(ca, ct);
+      if (!diag_done && i <= col) col = i;
+      const bool hA = ca == col, hT = ct == col;
+      double m = 0.0, nv = 0.0;
+      if (hA && hT) {
+        m = 0.5 * v[a] + 0.5 * tv[t];
+        nv = 0.5 * v[a] + -0.5 * tv[t];
+      } else if (hA) {
+        m = 0.5 * v[a];
+        nv = 0.5 * v[a];
+      } else if (hT) {
+        m = 0.5 * tv[t];
+        nv = -0.5 * tv[t];
+      }
+      if (col == i) {
+        diag_done = true;
+        diag_in.push_back(hA || hT);
+      }
+      P.ci.push_back(col);
+      Mv.push_back(m);
+      Nv.push_back(nv);
+      if (hA) ++a;
+      if (hT) ++t;
+    }
+    P.rp[i + 1] = (int64_t)P.ci.size();
+  }
+}
+
+}  // namespace gadi_host
+
+// ==================================================================== handle
+struct EngineBase;
+
+struct gadi_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int kind = GADI_PROBLEM_STENCIL7;
+  int64_t N = 0, n = 0;
+  double t1 = 0, t2 = 0, t3 = 0;
+  // CSR A (device) and the HSS pattern (device) + fp64 M/N values (host)
+  int64_t* d_rpA = nullptr;
+  int32_t* d_ciA = nullptr;
+  double* d_vA = nullptr;
+  int64_t nnzA = 0, nnzHS = 0;
+  int64_t* d_rpHS = nullptr;
+  int32_t* d_ciHS = nullptr;
+  std::vector<double> Mv, Nv;
+  std::vector<int64_t> diag_pos;  // position of (i,i) in the HS pattern
+  std::vector<uint8_t> diag_in;
+  // outer vectors (binary64)
+  double *d_x = nullptr, *d_b = nullptr, *d_s = nullptr, *d_t64 = nullptr;
+  // reductions / state
+  DevState* st = nullptr;
+  DevState* h_st = nullptr;  // pinned mirror
+  double *d_part0 = nullptr, *d_part1 = nullptr;
+  unsigned* d_ticket = nullptr;
+  int* h_done = nullptr;  // mapped pinned flag (CG done)
+  int* d_h_done = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr, evC = nullptr;
+  std::vector<cudaEvent_t> ring;
+  int64_t launches = 0;
+  // prepared inner engine
+  std::unique_ptr<EngineBase> eng;
+  double stop_norm = 1.0;
+  std::vector<double> history;
+
+  bool stencil() const { return kind == GADI_PROBLEM_STENCIL7; }
+};
+
+namespace gadi_host {
+
+template <class T>
+T* dalloc(int64_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<int64_t>(n, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+inline void read_state(gadi_handle* h) {
+  CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+inline Red red_of(gadi_handle* h) { return Red{h->d_part0, h->d_part1, h->d_ticket}; }
+
+// ------------------------------------------------------------ outer kernels on A
+struct OuterA {
+  // s = b - A x in u_f; s == nullptr computes the norm only.
+  static void resid(gadi_handle* h, const double* x, double* s, int uf, bool scaling) {
+    CK(cudaMemsetAsync(&h->st->maxbits, 0, sizeof(unsigned long long), h->stream));
+    const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
+    const Geo g = make_geo(h->N, al ? 2 : 1);
+    auto go = [&](auto op) {
+      auto L = [&](auto pt, auto vt) {
+        constexpr int PF = decltype(pt)::v, V = decltype(vt)::v;
+        k_resid_A<decltype(op), PF, V><<<g.nblk, g.threads(), 0, h->stream>>>(op, x, h->d_b, s,
+                                                                               scaling ? 1 : 0, g, red_of(h), h->st);
+      };
+      auto LV = [&](auto pt) {
+        if (al) L(pt, VecTag<2>{});
+        else L(pt, VecTag<1>{});
+      };
+      if (uf == GADI_HALF) LV(VecTag<P_HALF>{});
+      else if (uf == GADI_SINGLE) LV(VecTag<P_SINGLE>{});
+      else LV(VecTag<P_DOUBLE>{});
+    };
+    if (h->stencil()) {
+      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}};
+      go(op);
+    } else {
+      Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
+      go(op);
+    }
+    CKL();
+    ++h->launches;
+  }
+  static void apply(gadi_handle* h, const double* x, double* y) {
+    auto go = [&](auto op) {
+      k_apply<decltype(op), double, double, double><<<ew_grid(h->N), 256, 0, h->stream>>>(op, x, y, h->N,
+                                                                                          MatvecAF());
+    };
+    if (h->stencil()) {
+      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}};
+      go(op);
+    } else {
+      Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
+      go(op);
+    }
+    CKL();
+    ++h->launches;
+  }
+};
+
+}  // namespace gadi_host
+
+// ================================================================== engines
+struct InnerOut {
+  int iters = 0;
+  int status = INNER_CONVERGED;
+};
+
+// The inner solvers for one (operator, storage, arithmetic) choice.
+struct EngineBase {
+  virtual ~EngineBase() = default;
+  int u_r = GADI_DOUBLE, accum = 0, cprec = GADI_DOUBLE;
+  size_t tsize = 8;
+  gadi_inner_spec spec{};
+  double alpha = 1, omega = 1;
+  // inner-format device vectors (type-erased)
+  void *rhat = nullptr, *z = nullptr, *pz = nullptr, *y = nullptr;
+  // H/S solves on inner-format device vectors; CG consumes rhs (r in place)
+  virtual InnerOut cg(int which, void* rhs, void* x, double target) = 0;
+  virtual InnerOut gmres(int which, const void* rhs, void* x, double target) = 0;
+  virtual void scale_round(const double* s) = 0;            // rhat = round(s 2^-e)
+  virtual void scale_pz(double phat) = 0;                   // pz = round(phat z)
+  virtual void update(double* x, int pu) = 0;               // x += 2^e y
+  virtual void to_inner(const double* src, void* dst) = 0;  // round_vec to u_r
+  virtual void to_double(const void* src, double* dst) = 0;
+  virtual void apply(int which, const void* x, void* yv) = 0;
+};
+
+namespace gadi_host {
+
+template <class Op, class T, class C>
+struct Engine final : EngineBase {
+  gadi_handle* h;
+  Op opH, opS;
+  bool aligned;
+  Geo geo;
+  static constexpr int VA = 16 / sizeof(T);
+  // CG / GMRES work vectors
+  T *pA = nullptr, *pB = nullptr, *q = nullptr, *wA = nullptr, *wB = nullptr, *gr = nullptr, *V = nullptr;
+  C* dH = nullptr;  // CSR values (device)
+  C* dS = nullptr;
+  int m_restart = 30;
+  std::vector<T*> owned;
+
+  T* vec() {
+    T* v = dalloc<T>(h->N);
+    owned.push_back(v);
+    return v;
+  }
+
+  Engine(gadi_handle* hh, const gadi_inner_spec& sp, double a, double om, int ur, int acc) : h(hh) {
+    u_r = ur;
+    accum = acc;
+    cprec = std::is_same<C, __half>::value ? GADI_HALF : std::is_same<C, float>::value ? GADI_SINGLE : GADI_DOUBLE;
+    tsize = sizeof(T);
+    spec = sp;
+    alpha = a;
+    omega = om;
+    const int64_t N = h->N;
+    aligned = aligned_for(N, h->n, h->stencil(), VA);
+    geo = make_geo(N, aligned ? VA : 1);
+    m_restart = std::max(1, spec.restart);
+    rhat = vec();
+    z = vec();
+    pz = vec();
+    y = vec();
+    pA = vec();
+    pB = vec();
+    q = vec();
+    wA = vec();
+    wB = vec();
+    gr = vec();
+    V = dalloc<T>((int64_t)(m_restart + 1) * N);
+    owned.push_back(V);
+    build_ops();
+  }
+
+  ~Engine() override {
+    for (T* v : owned) cudaFree(v);
+    if (dH) cudaFree(dH);
+    if (dS) cudaFree(dS);
+  }
+
+  static C cval(double v, int ur) {
+    // matrix values are rounded to u_r (rounded_copy, inner_solver.cpp:41-45)
+    const double r = hround(v, ur);
+    if constexpr (std::is_same<C, __half>::value) return __double2half(r);
+    else return (C)r;
+  }
+
+  void build_ops() {
+    // regularize (splitting.cpp:37-47): H = shift_diagonal(M, alpha), S = shift_diagonal(N, alpha),
+    // the shift being 1.0*M_ii + alpha (sparse.cpp:166-183).
+    if constexpr (std::is_same<Op, Stencil7<C>>::value) {
+      const double t1 = h->t1, t2 = h->t2, t3 = h->t3;
+      const double ml = 0.5 * t2 + 0.5 * t3, mc = 0.5 * t1 + 0.5 * t1, mu = 0.5 * t3 + 0.5 * t2;
+      const double nl = 0.5 * t2 + -0.5 * t3, nc = 0.5 * t1 + -0.5 * t1, nu = 0.5 * t3 + -0.5 * t2;
+      const double hc = 1.0 * mc + alpha, sc = 1.0 * nc + alpha;
+      const double Hc[7] = {ml, ml, ml, hc, mu, mu, mu};
+      const double Sc[7] = {nl, nl, nl, sc, nu, nu, nu};
+      opH.n = opS.n = h->n;
+      opH.nn = opS.nn = h->n * h->n;
+      opH.N = opS.N = h->N;
+      for (int k = 0; k < 7; ++k) {
+        opH.c[k] = cval(Hc[k], u_r);
+        opS.c[k] = cval(Sc[k], u_r);
+      }
+    } else {
+      const int64_t nnz = h->nnzHS;
+      std::vector<C> hv(nnz), sv(nnz);
+      for (int64_t k = 0; k < nnz; ++k) {
+        hv[k] = cval(h->Mv[k], u_r);
+        sv[k] = cval(h->Nv[k], u_r);
+      }
+      for (int64_t i = 0; i < h->N; ++i) {
+        const int64_t k = h->diag_pos[i];
+        hv[k] = cval(h->diag_in[i] ? 1.0 * h->Mv[k] + alpha : alpha, u_r);
+        sv[k] = cval(h->diag_in[i] ? 1.0 * h->Nv[k] + alpha : alpha, u_r);
+      }
+      dH = dalloc<C>(nnz);
+      dS = dalloc<C>(nnz);
+      CK(cudaMemcpy(dH, hv.data(), nnz * sizeof(C), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dS, sv.data(), nnz * sizeof(C), cudaMemcpyHostToDevice));
+      opH = Op{h->N, h->d_rpHS, h->d_ciHS, dH};
+      opS = Op{h->N, h->d_rpHS, h->d_ciHS, dS};
+    }
+  }
+
+  template <class F>
+  void V2(F&& f) {
+    if (aligned) f(VecTag<VA>{});
+    else f(VecTag<1>{});
+  }
+
+  const Op& op(int which) const { return which == 1 ? opH : opS; }
+
+  // ------------------------------------------------------------------ CG
+  // inner_solver.cpp:47-83 on the device: per iteration one fused
+  // (p-update + SpMV + p.q) pass and one fused (two axpys + r.r + ||r||)
+  // pass. The host keeps at most ring.size() iterations queued ahead and stops
+  // queueing once the device raises the mapped done flag.
+  InnerOut cg(int which, void* rhs_v, void* x_v, double target) override {
+    T* r = static_cast<T*>(rhs_v);
+    T* x = static_cast<T*>(x_v);
+    cudaStream_t s = h->stream;
+    const Red rd = red_of(h);
+    const Op& o = op(which);
+    const int nt = geo.threads();
+    *(volatile int*)h->h_done = 0;
+    V2([&](auto vt) {
+      constexpr int V_ = decltype(vt)::v;
+      k_cg_init<T, C, V_><<<geo.nblk, nt, 0, s>>>(r, spec.max_inner_iters, target, geo, rd, h->st);
+    });
+    CKL();
+    ++h->launches;
+    const int kAhead = (int)h->ring.size();
+    for (int it = 0; it < spec.max_inner_iters; ++it) {
+      if (it >= kAhead) {
+        CK(cudaEventSynchronize(h->ring[it % kAhead]));
+        if (*(volatile int*)h->h_done) break;
+      }
+      T* p_in = (it & 1) ? pA : pB;
+      T* p_out = (it & 1) ? pB : pA;
+      const int first = it == 0;
+      V2([&](auto vt) {
+        constexpr int V_ = decltype(vt)::v;
+        k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
+        k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st);
+      });
+      CKL();
+      h->launches += 2;
+      CK(cudaEventRecord(h->ring[it % kAhead], s));
+    }
+    read_state(h);
+    if (!h->h_st->cg_xvalid) CK(cudaMemsetAsync(x, 0, h->N * sizeof(T), s));  // x = 0 (:51)
+    InnerOut out;
+    out.iters = h->h_st->cg_iters;
+    out.status = h->h_st->cg_status;
+    return out;
+  }
+
+  // --------------------------------------------------------------- GMRES
+  // inner_solver.cpp:85-194: vector work on the device (the basis scaling
+  // fused into the next matvec, MGS fused with the next Arnoldi dot), the
+  // (m+1) x m Hessenberg / Givens / back-solve on the host in the inner
+  // format's rounding, exactly as the reference orders them.
+  InnerOut gmres(int which, const void* rhs_v, void* x_v, double target) override {
+    const T* rhs = static_cast<const T*>(rhs_v);
+    T* x = static_cast<T*>(x_v);
+    cudaStream_t s = h->stream;
+    const Red rd = red_of(h);
+    const Op& o = op(which);
+    const int64_t N = h->N;
+    const int m = m_restart, fmt = cprec, nt = geo.threads();
+    auto Rf = [&](double v) { return hround(v, fmt); };
+    std::vector<double> Hc((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), yv(m + 1);
+    auto HC = [&](int i, int j) -> double& { return Hc[(size_t)i * m + j]; };
+    int total = 0, status = -1;
+    bool x_zero = true;  // x = 0 until the first update (inner_solver.cpp:92)
+    auto resid = [&]() {  // r = rhs - S x ; flags, max, ||r||_2 (binary64), norm2 in fmt
+      CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
+      CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
+      V2([&](auto vt) {
+        constexpr int V_ = decltype(vt)::v;
+        k_gm_resid<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st);
+        k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
+      });
+      CKL();
+      h->launches += 2;
+      read_state(h);
+    };
+    while (total < spec.max_inner_iters) {
+      resid();
+      if (h->h_st->flags & 1) {
+        status = INNER_OVERFLOW;
+        break;
+      }
+      const double beta = h->h_st->red_c;
+      if (std::sqrt(h->h_st->red_d) <= target) {
+        status = INNER_CONVERGED;
+        break;
+      }
+      if (beta == 0.0) break;
+      std::fill(Hc.begin(), Hc.end(), 0.0);
+      std::fill(cs.begin(), cs.end(), 0.0);
+      std::fill(sn.begin(), sn.end(), 0.0);
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      int j = 0;
+      bool happy = false;
+      double inv = 1.0 / beta;  // v_0 = r / beta (scale with a binary64 factor)
+      const T* wprev = gr;
+      for (; j < m && total < spec.max_inner_iters; ++j, ++total) {
+        T* vj = V + (int64_t)j * N;
+        T* w = (j & 1) ? wB : wA;
+        V2([&](auto vt) {
+          constexpr int V_ = decltype(vt)::v;
+          k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
+          for (int i = 0; i <= j; ++i) {
+            T* vi = V + (int64_t)i * N;
+            if (i < j) {
+              k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + N, i, geo, rd, h->st);
+            } else {
+              CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
+              k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
+            }
+          }
+          k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
+        });
+        CKL();
+        h->launches += j + 3;
+        read_state(h);
+        for (int i = 0; i <= j + 1; ++i) HC(i, j) = h->h_st->hcol[i];
+        const double h1 = HC(j + 1, j);
+        if (!std::isfinite(h1)) {
+          status = INNER_OVERFLOW;
+          goto done;
+        }
+        // v_{j+1} = w / h1 happens inside the next matvec (skipped if h1 == 0:
+        // the loop then ends at this step, below).
+        inv = h1 != 0.0 ? 1.0 / h1 : 0.0;
+        wprev = w;
+        for (int i = 0; i < j; ++i) {
+          const double t1 = Rf(Rf(cs[i] * HC(i, j)) + Rf(sn[i] * HC(i + 1, j)));
+          const double t2 = Rf(Rf(cs[i] * HC(i + 1, j)) - Rf(sn[i] * HC(i, j)));
+          HC(i, j) = t1;
+          HC(i + 1, j) = t2;
+        }
+        {
+          const double a = HC(j, j), b = HC(j + 1, j);
+          const double denom = Rf(std::hypot(a, b));
+          if (denom == 0.0) {
+            happy = true;
+            ++j;
+            ++total;
+            break;
+          }
+          cs[j] = Rf(a / denom);
+          sn[j] = Rf(b / denom);
+          HC(j, j) = denom;
+          HC(j + 1, j) = 0.0;
+          const double gj = g[j];
+          g[j] = Rf(cs[j] * gj);
+          g[j + 1] = Rf(-sn[j] * gj);
+          if (std::fabs(g[j + 1]) <= target || h1 == 0.0) {
+            happy = true;
+            ++j;
+            ++total;
+            break;
+          }
+        }
+      }
+      for (int i = j - 1; i >= 0; --i) {
+        double acc = g[i];
+        for (int k = i + 1; k < j; ++k) acc = Rf(acc - Rf(HC(i, k) * yv[k]));
+        yv[i] = Rf(acc / HC(i, i));
+      }
+      if (j > 0) {
+        for (int i = 0; i < j; ++i) h->h_st->ycoef[i] = yv[i];
+        CK(cudaMemcpyAsync(h->st->ycoef, h->h_st->ycoef, j * sizeof(double), cudaMemcpyHostToDevice, s));
+      }
+      CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
+      V2([&](auto vt) {
+        constexpr int V_ = decltype(vt)::v;
+        k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, x_zero ? 1 : 0, V, N, j, geo, h->st);
+      });
+      CKL();
+      ++h->launches;
+      x_zero = false;
+      read_state(h);
+      if (h->h_st->flags & 1) {
+        status = INNER_OVERFLOW;
+        break;
+      }
+      if (happy) {
+        resid();
+        if (std::sqrt(h->h_st->red_d) <= target) {
+          status = INNER_CONVERGED;
+          break;
+        }
+      }
+    }
+  done:
+    if (x_zero) CK(cudaMemsetAsync(x, 0, N * sizeof(T), s));
+    // all_finite(x) (inner_solver.cpp:192): every update of x was checked above
+    if (status < 0) status = INNER_STAGNATED;
+    InnerOut out;
+    out.iters = total;
+    out.status = status;
+    return out;
+  }
+
+  // ----------------------------------------------------------- outer pieces
+  void scale_round(const double* sv) override {
+    const Red rd = red_of(h);
+    const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
+    const Geo g = make_geo(h->N, al ? 2 : 1);
+    if (al) k_scale_round<T, 2><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
+    else k_scale_round<T, 1><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
+    CKL();
+    ++h->launches;
+  }
+  void scale_pz(double phat) override {
+    V2([&](auto vt) {
+      constexpr int V_ = decltype(vt)::v;
+      k_scale<T, V_><<<geo.nblk, geo.threads(), 0, h->stream>>>(static_cast<T*>(z), static_cast<T*>(pz), phat, geo);
+    });
+    CKL();
+    ++h->launches;
+  }
+  void update(double* x, int pu) override {
+    const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
+    const Geo g = make_geo(h->N, al ? 2 : 1);
+    auto L = [&](auto pt, auto vt) {
+      constexpr int PU = decltype(pt)::v, V_ = decltype(vt)::v;
+      k_update<T, PU, V_><<<g.nblk, g.threads(), 0, h->stream>>>(x, static_cast<const T*>(y), g, h->st);
+    };
+    auto LV = [&](auto pt) {
+      if (al) L(pt, VecTag<2>{});
+      else L(pt, VecTag<1>{});
+    };
+    if (pu == GADI_HALF) LV(VecTag<P_HALF>{});
+    else if (pu == GADI_SINGLE) LV(VecTag<P_SINGLE>{});
+    else LV(VecTag<P_DOUBLE>{});
+    CKL();
+    ++h->launches;
+  }
+  void to_inner(const double* src, void* dst) override {
+    constexpr int PT = prec_of<T>();
+    k_convert<double, T, PT><<<ew_grid(h->N), 256, 0, h->stream>>>(src, static_cast<T*>(dst), h->N);
+    CKL();
+    ++h->launches;
+  }
+  void to_double(const void* src, double* dst) override {
+    k_convert<T, double, P_DOUBLE><<<ew_grid(h->N), 256, 0, h->stream>>>(static_cast<const T*>(src), dst, h->N);
+    CKL();
+    ++h->launches;
+  }
+  void apply(int which, const void* xv, void* yv_) override {
+    k_apply<Op, T, C, T><<<ew_grid(h->N), 256, 0, h->stream>>>(op(which), static_cast<const T*>(xv),
+                                                               static_cast<T*>(yv_), h->N, MatvecF<C, T>());
+    CKL();
+    ++h->launches;
+  }
+};
+
+// One translation unit per (operator, storage, arithmetic) instantiates each
+// engine (gadi_engine_*.cu) so the build compiles them in parallel.
+#define GADI_ENGINE_FACTORY(name) \
+  EngineBase* name(gadi_handle* h, const gadi_inner_spec& sp, double a, double om, int ur, int acc)
+GADI_ENGINE_FACTORY(make_engine_st_d64);
+GADI_ENGINE_FACTORY(make_engine_st_f32);
+GADI_ENGINE_FACTORY(make_engine_st_h16);
+GADI_ENGINE_FACTORY(make_engine_st_h32);
+GADI_ENGINE_FACTORY(make_engine_csr_d64);
+GADI_ENGINE_FACTORY(make_engine_csr_f32);
+GADI_ENGINE_FACTORY(make_engine_csr_h16);
+GADI_ENGINE_FACTORY(make_engine_csr_h32);
+
+}  // namespace gadi_host

@@ -1,15 +1,23 @@
 // gadi_kernels.cuh — the device kernels of the GADI-IR hot path.
 //
-// One thread owns one reduction segment (see gadi_common.cuh); every kernel
-// that produces a dot product or norm folds it into the same pass that writes
-// the vector (SpMV + p.Ap; the two CG axpys + r.r + ||r||_2; GMRES MGS axpy +
-// the next Arnoldi dot), and the last block to finish evaluates the top of
-// the pairwise tree and the scalar recurrences (alpha, beta, stop tests) on
-// the device, so the host never waits inside an inner iteration.
+// Work decomposition. The N vector entries are cut into 2^D reduction
+// segments (gadi_common.cuh). A lane owns R segments that are 32 apart, so a
+// warp's loads at each step are one contiguous 512-byte run (VEC*sizeof(T)
+// == 16 bytes per lane); the warp folds its R x 32 contiguous segments into
+// one pairwise partial (butterfly per step, then a tree over the R steps), a
+// block folds its W warps, and the last block to finish folds the block
+// partials. Every level is a perfect binary tree over contiguous ranges, so
+// the result is the reference's pairwise sum (kernels.cpp:33-39) bit for bit.
+//
+// Every kernel that produces a dot product or norm folds it into the pass
+// that writes the vector (SpMV + p.Ap with p = r + beta p formed on the fly;
+// both CG axpys + r.r + ||r||_2; GMRES MGS axpy + the next Arnoldi dot), and
+// the last block evaluates the scalar recurrences (alpha, beta, stop tests)
+// on the device: the host never waits inside a CG solve.
 //
 // Template parameters: Op (Stencil7 / Csr), T (storage: __half, float,
 // double), C (arithmetic: T, or float for binary16 storage with binary32
-// accumulation), VEC (elements per thread on the aligned path; 1 = general).
+// accumulation), VEC (elements per segment on the aligned path; 1 = general).
 #pragma once
 
 #include "gadi_common.cuh"
@@ -17,11 +25,16 @@
 
 namespace gadi {
 
+constexpr int RMAX = 8;  // segments per lane (unrolled)
+
 struct Geo {
   int64_t N;
-  int D;     // tree depth of the segments
-  int bdim;  // threads per block (power of 2)
-  int nblk;  // blocks (power of 2); nblk * bdim = 2^D segments
+  int D;     // 2^D segments
+  int L;     // lanes per warp chunk (32, or 2^D when smaller)
+  int W;     // warps per block
+  int R;     // segments per lane
+  int nblk;  // blocks; nblk * W * R * L == 2^D
+  __host__ __device__ int threads() const { return L * W; }
 };
 
 struct Red {
@@ -38,7 +51,7 @@ struct DevState {
   // generic reduction outputs
   double red_c, red_d;
   int flags;
-  int pad0;
+  int cg_xvalid;
   unsigned long long maxbits;
   // GMRES Arnoldi column, h(0..j+1, j)
   double hcol[72];
@@ -61,22 +74,80 @@ __device__ __forceinline__ void cg_finish(DevState* st, int status, int iters) {
   }
 }
 
-// ------------------------------------------------------------ reductions
-// Reduce v0 (pairwise in C) and v1 (pairwise in binary64) over the grid.
-// Returns true in exactly one thread (thread 0 of the last block), which
-// then holds the totals. Every thread of every block must call it.
+// ------------------------------------------------------------ segment loop
+// Runs body(seg, c, d) on this lane's R segments and returns the warp's
+// pairwise totals of c (in C0) and d (in binary64), valid in every lane.
+template <int VEC, bool R0, bool R1, class C0, class Body>
+__device__ __forceinline__ void seg_run(const Geo& g, Body&& body, C0& w0, double& w1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  C0 a0[RMAX];
+  double a1[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r < g.R) {
+      const int64_t t = (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane;
+      const Seg s = seg_of<VEC>(t, g.N, g.D);
+      C0 c = Ar<C0>::zero();
+      double d = 0.0;
+      body(s, c, d);
+      if (R0) a0[r] = warp_tree(c, g.L);
+      if (R1) a1[r] = warp_tree(d, g.L);
+    }
+  }
+#pragma unroll
+  for (int st = 1; st < RMAX; st <<= 1)
+#pragma unroll
+    for (int r = 0; r + st < RMAX; r += 2 * st)
+      if (r + st < g.R) {
+        if (R0) a0[r] = Ar<C0>::add(a0[r], a0[r + st]);
+        if (R1) a1[r] = __dadd_rn(a1[r], a1[r + st]);
+      }
+  w0 = R0 ? a0[0] : Ar<C0>::zero();
+  w1 = R1 ? a1[0] : 0.0;
+}
+
+// Elementwise loop over this lane's segments (no reduction).
+template <int VEC, class Body>
+__device__ __forceinline__ void seg_each(const Geo& g, Body&& body) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r)
+    if (r < g.R) {
+      const int64_t t = (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane;
+      body(seg_of<VEC>(t, g.N, g.D));
+    }
+}
+
+// Fold the warp totals over the block and the grid. Returns true in exactly
+// one thread (thread 0 of the last block), which then holds the grid totals.
+// Every thread of every block must call it.
 template <class C0>
-__device__ __forceinline__ bool grid_finish(C0 v0, double v1, const Geo& g, const Red& r, C0& t0,
-                                            double& t1) {
+__device__ __forceinline__ bool grid_finish(C0 w0, double w1, const Geo& g, const Red& r, C0& t0, double& t1) {
   __shared__ __align__(8) unsigned char smb0[32 * sizeof(double)];
   __shared__ double sm1[32];
   __shared__ int last;
   C0* sm0 = reinterpret_cast<C0*>(smb0);
-  C0 b0 = block_tree(v0, g.bdim, sm0);
-  double b1 = block_tree(v1, g.bdim, sm1);
-  if (threadIdx.x == 0) {
-    r.part0[blockIdx.x] = to_dbl(b0);
-    r.part1[blockIdx.x] = b1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (g.W > 1) {
+    if (lane == 0) {
+      sm0[warp] = w0;
+      sm1[warp] = w1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      C0 v0 = lane < g.W ? sm0[lane] : Ar<C0>::zero();
+      double v1 = lane < g.W ? sm1[lane] : 0.0;
+      if (lane < g.W) {
+        v0 = warp_tree(v0, g.W);
+        v1 = warp_tree(v1, g.W);
+      }
+      w0 = v0;
+      w1 = v1;
+    }
+  }
+  if (tid == 0) {
+    r.part0[blockIdx.x] = to_dbl(w0);
+    r.part1[blockIdx.x] = w1;
     __threadfence();
     const unsigned t = atomicAdd(r.ticket, 1u);
     last = (t == (unsigned)g.nblk - 1u);
@@ -84,7 +155,7 @@ __device__ __forceinline__ bool grid_finish(C0 v0, double v1, const Geo& g, cons
   __syncthreads();
   if (!last) return false;
   __threadfence();
-  const int P = g.nblk, B = blockDim.x, tid = threadIdx.x;
+  const int P = g.nblk, B = blockDim.x;
   C0 a0;
   double a1;
   int cnt;
@@ -93,11 +164,11 @@ __device__ __forceinline__ bool grid_finish(C0 v0, double v1, const Geo& g, cons
     a1 = tid < P ? __ldcg(r.part1 + tid) : 0.0;
     cnt = P;
   } else {
-    const int64_t L = P / B;
-    const double* p0 = r.part0 + (int64_t)tid * L;
-    const double* p1 = r.part1 + (int64_t)tid * L;
-    a0 = run_pairwise<C0>(L, [&](int64_t j) { return from_dbl<C0>(__ldcg(p0 + j)); });
-    a1 = run_pairwise<double>(L, [&](int64_t j) { return __ldcg(p1 + j); });
+    const int64_t Lr = P / B;
+    const double* p0 = r.part0 + (int64_t)tid * Lr;
+    const double* p1 = r.part1 + (int64_t)tid * Lr;
+    a0 = run_pairwise<C0>(Lr, [&](int64_t j) { return from_dbl<C0>(__ldcg(p0 + j)); });
+    a1 = run_pairwise<double>(Lr, [&](int64_t j) { return __ldcg(p1 + j); });
     cnt = B;
   }
   a0 = block_tree(a0, cnt, sm0);
@@ -150,28 +221,27 @@ __device__ __forceinline__ void store_seg(T* __restrict__ p, const Seg& s, const
   }
 }
 // Operator fold over a segment: aligned = one VEC-wide row fold, general =
-// element by element.
-template <int VEC, int G, class Op, class X, class Acc, class F>
-__device__ __forceinline__ void fold_seg(const Op& op, const X* __restrict__ x, const Seg& s,
-                                         Acc (&acc)[G], F f) {
+// element by element. `cc` returns the operand at the segment's points.
+template <int VEC, int G, class Op, class Src, class X, class Acc, class F>
+__device__ __forceinline__ void fold_seg(const Op& op, const Src& x, const Seg& s, Acc (&acc)[G], F f,
+                                         X (&cc)[G]) {
   if constexpr (VEC > 1) {
-    op.template fold<VEC>(x, s.lo, acc, f);
+    op.template fold<VEC>(x, s.lo, acc, f, cc);
   } else {
 #pragma unroll
-    for (int i = 0; i < G; ++i)
+    for (int i = 0; i < G; ++i) {
       if (i < s.len) {
         Acc a1[1] = {acc[i]};
-        op.template fold<1>(x, s.lo + i, a1, f);
+        X c1[1];
+        op.template fold<1>(x, s.lo + i, a1, f, c1);
         acc[i] = a1[0];
+        cc[i] = c1[0];
+      } else {
+        cc[i] = from_dbl<X>(0.0);
       }
+    }
   }
 }
-
-#define GADI_SEG()                                                     \
-  constexpr int G = VEC > 1 ? VEC : 4;                                 \
-  const int64_t tix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  \
-  const Seg s = seg_of<VEC>(tix, g.N, g.D);                            \
-  (void)G
 
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
@@ -197,71 +267,79 @@ struct MatvecAF {  // b = A x in binary64 (problems.cpp:44)
   }
 };
 
+#define GADI_G constexpr int G = VEC > 1 ? VEC : 4
+#define GADI_LIVE(i) (VEC > 1 || (i) < s.len)
+
 // ================================================================== CG
-// r = p = rhs, x = 0, rs = dot(r, r) (inner_solver.cpp:51-55); initial stop test.
+// r = rhs (in place), rs = dot(r, r) and the initial stop test
+// (inner_solver.cpp:51-57). x and p are produced by the first iteration.
 template <class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ rhs, T* __restrict__ r,
-                                                 T* __restrict__ p, T* __restrict__ x, int max_inner,
-                                                 double target, Geo g, Red rd, DevState* st) {
-  GADI_SEG();
-  T v[G], z[G];
-  load_seg<T, VEC, G>(rhs, s, v);
+__global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int max_inner, double target, Geo g,
+                                                 Red rd, DevState* st) {
+  GADI_G;
+  C w0;
+  double w1;
+  seg_run<VEC, true, true>(g, [&](const Seg& s, C& c, double& d) {
+    T v[G];
+    load_seg<T, VEC, G>(r, s, v);
+    C tc[G];
+    double td[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) z[i] = from_dbl<T>(0.0);
-  store_seg<T, VEC, G>(r, s, v);
-  store_seg<T, VEC, G>(p, s, v);
-  store_seg<T, VEC, G>(x, s, z);
-  C tc[G];
-  double td[G];
-#pragma unroll
-  for (int i = 0; i < G; ++i) {
-    const C c = ld_c<T, C>(v[i]);
-    tc[i] = Ar<C>::mul(c, c);
-    const double d = to_dbl(v[i]);
-    td[i] = d * d;
-  }
-  C sc = seg_sum<C, G>(tc, s.len);
-  double sd = seg_sum<double, G>(td, s.len);
+    for (int i = 0; i < G; ++i) {
+      const C cv = ld_c<T, C>(v[i]);
+      tc[i] = Ar<C>::mul(cv, cv);
+      const double dv = to_dbl(v[i]);
+      td[i] = __dmul_rn(dv, dv);
+    }
+    c = seg_sum<C, G>(tc, s.len);
+    d = seg_sum<double, G>(td, s.len);
+  }, w0, w1);
   C rs;
   double ss;
-  if (grid_finish(sc, sd, g, rd, rs, ss)) {
+  if (grid_finish(w0, w1, g, rd, rs, ss)) {
     st->cg_rs = to_dbl(rs);
     st->cg_it = 0;
     st->cg_flags = 0;
+    st->cg_xvalid = 0;
     st->cg_max = max_inner;
     st->cg_target = target;
-    if (max_inner <= 0) {
-      cg_finish(st, INNER_STAGNATED, 0);
-    } else if (sqrt(ss) <= target) {
-      cg_finish(st, INNER_CONVERGED, 0);
-    } else {
-      st->cg_done = 0;
-    }
+    st->cg_done = 0;
+    if (max_inner <= 0) cg_finish(st, INNER_STAGNATED, 0);
+    else if (sqrt(ss) <= target) cg_finish(st, INNER_CONVERGED, 0);
   }
 }
 
-// q = H p, pap = dot(p, q); alpha = rs / pap or break (inner_solver.cpp:62-65).
+// p_out = r + beta p_in (or r on the first iteration; inner_solver.cpp:53,76),
+// q = H p_out, pap = dot(p_out, q); then alpha = rs / pap or `break`
+// (inner_solver.cpp:62-65).
 template <class Op, class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_cg_spmv(Op op, const T* __restrict__ p, T* __restrict__ q,
-                                                 Geo g, Red rd, DevState* st) {
+__global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r, const T* __restrict__ p_in,
+                                                  T* __restrict__ p_out, T* __restrict__ q, int first, Geo g,
+                                                  Red rd, DevState* st) {
   if (*(volatile int*)&st->cg_done) return;
-  GADI_SEG();
-  C acc[G];
+  GADI_G;
+  const PUpdSrc<T, C> src{r, p_in, from_dbl<C>(st->cg_beta), first};
+  C w0;
+  double w1;
+  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+    C acc[G];
+    T pv[G], qv[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) acc[i] = Ar<C>::zero();
-  fold_seg<VEC, G>(op, p, s, acc, MatvecF<C, T>());
-  T qv[G], pv[G];
+    for (int i = 0; i < G; ++i) acc[i] = Ar<C>::zero();
+    fold_seg<VEC, G>(op, src, s, acc, MatvecF<C, T>(), pv);
+    C tc[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) qv[i] = st_t<T, C>(acc[i]);
-  store_seg<T, VEC, G>(q, s, qv);
-  load_seg<T, VEC, G>(p, s, pv);
-  C tc[G];
-#pragma unroll
-  for (int i = 0; i < G; ++i) tc[i] = Ar<C>::mul(ld_c<T, C>(pv[i]), ld_c<T, C>(qv[i]));
-  C sc = seg_sum<C, G>(tc, s.len);
+    for (int i = 0; i < G; ++i) {
+      qv[i] = st_t<T, C>(acc[i]);
+      tc[i] = Ar<C>::mul(ld_c<T, C>(pv[i]), ld_c<T, C>(qv[i]));
+    }
+    store_seg<T, VEC, G>(q, s, qv);
+    store_seg<T, VEC, G>(p_out, s, pv);
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
   C pap;
   double dummy;
-  if (grid_finish(sc, 0.0, g, rd, pap, dummy)) {
+  if (grid_finish(w0, w1, g, rd, pap, dummy)) {
     const double pd = to_dbl(pap);
     st->cg_pap = pd;
     if (pd == 0.0 || !isfinite(pd)) {
@@ -273,130 +351,131 @@ __global__ void __launch_bounds__(256) k_cg_spmv(Op op, const T* __restrict__ p,
   }
 }
 
-// x += a p; r -= a q; rs' = dot(r, r); ||r||_2 (binary64) for the next stop
-// test; overflow checks (inner_solver.cpp:66-77).
+// x += a p (x = 0 + a p on the first iteration); r -= a q; rs' = dot(r, r);
+// ||r||_2 in binary64 for the next stop test; overflow checks
+// (inner_solver.cpp:66-77).
 template <class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_cg_update(T* __restrict__ x, T* __restrict__ r,
-                                                   const T* __restrict__ p, const T* __restrict__ q, Geo g,
-                                                   Red rd, DevState* st) {
+__global__ void __launch_bounds__(256) k_cg_update(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                                                   const T* __restrict__ q, int first, Geo g, Red rd,
+                                                   DevState* st) {
   if (*(volatile int*)&st->cg_done) return;
-  GADI_SEG();
+  GADI_G;
   const C a = from_dbl<C>(st->cg_a);
   const C na = Ar<C>::neg(a);
-  T xv[G], rv[G], pv[G], qv[G];
-  load_seg<T, VEC, G>(x, s, xv);
-  load_seg<T, VEC, G>(r, s, rv);
-  load_seg<T, VEC, G>(p, s, pv);
-  load_seg<T, VEC, G>(q, s, qv);
-  C tc[G];
-  double td[G];
   int bad = 0;
+  C w0;
+  double w1;
+  seg_run<VEC, true, true>(g, [&](const Seg& s, C& c, double& d) {
+    T xv[G], rv[G], pv[G], qv[G];
+    if (!first) load_seg<T, VEC, G>(x, s, xv);
+    load_seg<T, VEC, G>(r, s, rv);
+    load_seg<T, VEC, G>(p, s, pv);
+    load_seg<T, VEC, G>(q, s, qv);
+    C tc[G];
+    double td[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    xv[i] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(xv[i]), Ar<C>::mul(a, ld_c<T, C>(pv[i]))));
-    rv[i] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[i]), Ar<C>::mul(na, ld_c<T, C>(qv[i]))));
-    const C rc = ld_c<T, C>(rv[i]);
-    tc[i] = Ar<C>::mul(rc, rc);
-    const double d = to_dbl(rv[i]);
-    td[i] = d * d;
-    if (VEC > 1 || i < s.len) bad |= (finite_t(rv[i]) ? 0 : 1) | (finite_t(xv[i]) ? 0 : 2);
-  }
-  store_seg<T, VEC, G>(x, s, xv);
-  store_seg<T, VEC, G>(r, s, rv);
+    for (int i = 0; i < G; ++i) {
+      const C x0 = first ? Ar<C>::zero() : ld_c<T, C>(xv[i]);
+      xv[i] = st_t<T, C>(Ar<C>::add(x0, Ar<C>::mul(a, ld_c<T, C>(pv[i]))));
+      rv[i] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[i]), Ar<C>::mul(na, ld_c<T, C>(qv[i]))));
+      const C rc = ld_c<T, C>(rv[i]);
+      tc[i] = Ar<C>::mul(rc, rc);
+      const double dv = to_dbl(rv[i]);
+      td[i] = __dmul_rn(dv, dv);
+      if (GADI_LIVE(i)) bad |= (finite_t(rv[i]) ? 0 : 1) | (finite_t(xv[i]) ? 0 : 2);
+    }
+    store_seg<T, VEC, G>(x, s, xv);
+    store_seg<T, VEC, G>(r, s, rv);
+    c = seg_sum<C, G>(tc, s.len);
+    d = seg_sum<double, G>(td, s.len);
+  }, w0, w1);
   or_flags(&st->cg_flags, bad);
-  C sc = seg_sum<C, G>(tc, s.len);
-  double sd = seg_sum<double, G>(td, s.len);
   C rsn;
   double ss;
-  if (grid_finish(sc, sd, g, rd, rsn, ss)) {
+  if (grid_finish(w0, w1, g, rd, rsn, ss)) {
     const int it = st->cg_it;
     const double rn = to_dbl(rsn);
     const int flags = *(volatile int*)&st->cg_flags;
+    st->cg_xvalid = 1;
     if (!isfinite(rn) || (flags & 1)) {
       cg_finish(st, INNER_OVERFLOW, it + 1);
     } else {
       st->cg_beta = to_dbl(div_c<C>(rsn, from_dbl<C>(st->cg_rs)));
       st->cg_rs = rn;
       st->cg_it = it + 1;
-      if (it + 1 >= st->cg_max) {
-        cg_finish(st, (flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
-      } else if (sqrt(ss) <= st->cg_target) {
-        cg_finish(st, INNER_CONVERGED, it + 1);
-      }
+      if (it + 1 >= st->cg_max) cg_finish(st, (flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
+      else if (sqrt(ss) <= st->cg_target) cg_finish(st, INNER_CONVERGED, it + 1);
     }
   }
-}
-
-// p = r + beta p (inner_solver.cpp:76).
-template <class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_cg_pupd(const T* __restrict__ r, T* __restrict__ p, Geo g,
-                                                 DevState* st) {
-  if (*(volatile int*)&st->cg_done) return;
-  GADI_SEG();
-  const C b = from_dbl<C>(st->cg_beta);
-  T rv[G], pv[G];
-  load_seg<T, VEC, G>(r, s, rv);
-  load_seg<T, VEC, G>(p, s, pv);
-#pragma unroll
-  for (int i = 0; i < G; ++i) pv[i] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[i]), Ar<C>::mul(b, ld_c<T, C>(pv[i]))));
-  store_seg<T, VEC, G>(p, s, pv);
 }
 
 // ================================================================ GMRES
 // r = rhs - S x in the inner arithmetic (inner_solver.cpp:97 / :182, the
-// two-stage residual kernels.cpp:56-69), max|r|, ||r||_2, finiteness.
+// two-stage residual kernels.cpp:56-69; x_zero: the restart from x = 0,
+// folded over +0 without reading x), max|r| (for norm2), ||r||_2 (binary64),
+// finiteness.
 template <class Op, class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x, const T* __restrict__ rhs,
-                                                  T* __restrict__ r, Geo g, Red rd, DevState* st) {
-  GADI_SEG();
-  T bv[G];
-  load_seg<T, VEC, G>(rhs, s, bv);
-  C acc[G];
-#pragma unroll
-  for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
-  fold_seg<VEC, G>(op, x, s, acc, ResidF<C, T>());
-  T rv[G];
-  double td[G], m = 0.0;
+__global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x, int x_zero,
+                                                  const T* __restrict__ rhs, T* __restrict__ r, Geo g, Red rd,
+                                                  DevState* st) {
+  GADI_G;
   int bad = 0;
+  double m = 0.0;
+  C w0;
+  double w1;
+  seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) {
+    T bv[G], xc[G], rv[G];
+    load_seg<T, VEC, G>(rhs, s, bv);
+    C acc[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    rv[i] = st_t<T, C>(acc[i]);
-    const double d = to_dbl(rv[i]);
-    td[i] = d * d;
-    if (VEC > 1 || i < s.len) {
-      bad |= finite_t(rv[i]) ? 0 : 1;
-      m = fmax(m, fabs(d));
+    for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
+    if (x_zero) fold_seg<VEC, G>(op, ZeroSrc<T>{}, s, acc, ResidF<C, T>(), xc);
+    else fold_seg<VEC, G>(op, PlainSrc<T>{x}, s, acc, ResidF<C, T>(), xc);
+    double td[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      rv[i] = st_t<T, C>(acc[i]);
+      const double dv = to_dbl(rv[i]);
+      td[i] = __dmul_rn(dv, dv);
+      if (GADI_LIVE(i)) {
+        bad |= finite_t(rv[i]) ? 0 : 1;
+        m = (dv == dv) ? fmax(m, fabs(dv)) : m;
+      }
     }
-  }
-  store_seg<T, VEC, G>(r, s, rv);
+    store_seg<T, VEC, G>(r, s, rv);
+    d = seg_sum<double, G>(td, s.len);
+  }, w0, w1);
   block_max_abs(&st->maxbits, m);
   or_flags(&st->flags, bad);
-  double sd = seg_sum<double, G>(td, s.len);
   C dc;
   double ss;
-  if (grid_finish(Ar<C>::zero(), sd, g, rd, dc, ss)) st->red_d = ss;
+  if (grid_finish(w0, w1, g, rd, dc, ss)) st->red_d = ss;
 }
 
 // norm2 in the inner format (kernels.cpp:71-82): m = max|w| (from maxbits),
-// q = w/m, sum of q*q pairwise, m * sqrt(sum); written to *dst.
+// q = w/m, pairwise sum of q*q, m * sqrt(sum); written to *dst.
 template <class T, class C, int VEC>
 __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* dst, Geo g, Red rd,
                                                DevState* st) {
-  GADI_SEG();
+  GADI_G;
   const double m = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
   const C mc = from_dbl<C>(m);
-  T wv[G];
-  load_seg<T, VEC, G>(w, s, wv);
-  C tc[G];
+  C w0;
+  double w1;
+  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+    T wv[G];
+    load_seg<T, VEC, G>(w, s, wv);
+    C tc[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    const C q = div_c<C>(ld_c<T, C>(wv[i]), mc);
-    tc[i] = Ar<C>::mul(q, q);
-  }
-  C sc = seg_sum<C, G>(tc, s.len);
+    for (int i = 0; i < G; ++i) {
+      const C qv = div_c<C>(ld_c<T, C>(wv[i]), mc);
+      tc[i] = Ar<C>::mul(qv, qv);
+    }
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
   C sum;
   double dummy;
-  if (grid_finish(sc, 0.0, g, rd, sum, dummy)) {
+  if (grid_finish(w0, w1, g, rd, sum, dummy)) {
     if (m == 0.0 || !isfinite(m)) {
       *dst = m;
     } else {
@@ -409,35 +488,54 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
 // dst = round(a * src) with a in binary64 (scale, kernels.cpp:166-171).
 template <class T, int VEC>
 __global__ void __launch_bounds__(256) k_scale(const T* __restrict__ src, T* __restrict__ dst, double a, Geo g) {
-  GADI_SEG();
-  T v[G];
-  load_seg<T, VEC, G>(src, s, v);
+  GADI_G;
+  seg_each<VEC>(g, [&](const Seg& s) {
+    T v[G];
+    load_seg<T, VEC, G>(src, s, v);
 #pragma unroll
-  for (int i = 0; i < G; ++i) v[i] = from_dbl<T>(__dmul_rn(a, to_dbl(v[i])));
-  store_seg<T, VEC, G>(dst, s, v);
+    for (int i = 0; i < G; ++i) v[i] = from_dbl<T>(__dmul_rn(a, to_dbl(v[i])));
+    store_seg<T, VEC, G>(dst, s, v);
+  });
 }
 
-// w = S v_j and h_0j = dot(w, v_0) (inner_solver.cpp:120-122).
-template <class Op, class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ vj, const T* __restrict__ v0,
+// Arnoldi step j (inner_solver.cpp:120-122, 133-134): v_j = w_prev / h (the
+// previous step's scale, fused here; SCALED == false: v_j as stored), then
+// w = S v_j and h_0j = dot(w, v_0). wprev and w must be different buffers.
+template <class Op, class T, class C, int VEC, bool SCALED>
+__global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ wprev, double inv,
+                                                   T* __restrict__ vj, const T* __restrict__ v0,
                                                    T* __restrict__ w, Geo g, Red rd, DevState* st) {
-  GADI_SEG();
-  C acc[G];
+  GADI_G;
+  C w0;
+  double w1;
+  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+    C acc[G];
+    T vv[G], wv[G], v0v[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) acc[i] = Ar<C>::zero();
-  fold_seg<VEC, G>(op, vj, s, acc, MatvecF<C, T>());
-  T wv[G], v0v[G];
+    for (int i = 0; i < G; ++i) acc[i] = Ar<C>::zero();
+    if constexpr (SCALED) {
+      fold_seg<VEC, G>(op, ScaleSrc<T>{wprev, inv}, s, acc, MatvecF<C, T>(), vv);
+      store_seg<T, VEC, G>(vj, s, vv);
+    } else {
+      fold_seg<VEC, G>(op, PlainSrc<T>{vj}, s, acc, MatvecF<C, T>(), vv);
+    }
 #pragma unroll
-  for (int i = 0; i < G; ++i) wv[i] = st_t<T, C>(acc[i]);
-  store_seg<T, VEC, G>(w, s, wv);
-  load_seg<T, VEC, G>(v0, s, v0v);
-  C tc[G];
+    for (int i = 0; i < G; ++i) wv[i] = st_t<T, C>(acc[i]);
+    store_seg<T, VEC, G>(w, s, wv);
+    if (!SCALED && vj == v0) {
 #pragma unroll
-  for (int i = 0; i < G; ++i) tc[i] = Ar<C>::mul(ld_c<T, C>(wv[i]), ld_c<T, C>(v0v[i]));
-  C sc = seg_sum<C, G>(tc, s.len);
+      for (int i = 0; i < G; ++i) v0v[i] = vv[i];
+    } else {
+      load_seg<T, VEC, G>(v0, s, v0v);
+    }
+    C tc[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) tc[i] = Ar<C>::mul(ld_c<T, C>(wv[i]), ld_c<T, C>(v0v[i]));
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
   C h;
   double dummy;
-  if (grid_finish(sc, 0.0, g, rd, h, dummy)) st->hcol[0] = to_dbl(h);
+  if (grid_finish(w0, w1, g, rd, h, dummy)) st->hcol[0] = to_dbl(h);
 }
 
 // Modified Gram-Schmidt step i (inner_solver.cpp:121-125): w -= h_i v_i, then
@@ -446,56 +544,68 @@ template <class T, class C, int VEC, bool LAST>
 __global__ void __launch_bounds__(256) k_gm_mgs(T* __restrict__ w, const T* __restrict__ vi,
                                                 const T* __restrict__ vnext, int i, Geo g, Red rd,
                                                 DevState* st) {
-  GADI_SEG();
+  GADI_G;
   const C nh = Ar<C>::neg(from_dbl<C>(st->hcol[i]));
-  T wv[G], vv[G];
-  load_seg<T, VEC, G>(w, s, wv);
-  load_seg<T, VEC, G>(vi, s, vv);
+  double m = 0.0;
+  C w0;
+  double w1;
+  seg_run<VEC, !LAST, false>(g, [&](const Seg& s, C& c, double&) {
+    T wv[G], vv[G];
+    load_seg<T, VEC, G>(w, s, wv);
+    load_seg<T, VEC, G>(vi, s, vv);
 #pragma unroll
-  for (int k = 0; k < G; ++k) wv[k] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(wv[k]), Ar<C>::mul(nh, ld_c<T, C>(vv[k]))));
-  store_seg<T, VEC, G>(w, s, wv);
+    for (int k = 0; k < G; ++k) wv[k] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(wv[k]), Ar<C>::mul(nh, ld_c<T, C>(vv[k]))));
+    store_seg<T, VEC, G>(w, s, wv);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        if (GADI_LIVE(k)) {
+          const double dv = to_dbl(wv[k]);
+          m = (dv == dv) ? fmax(m, fabs(dv)) : m;
+        }
+    } else {
+      load_seg<T, VEC, G>(vnext, s, vv);
+      C tc[G];
+#pragma unroll
+      for (int k = 0; k < G; ++k) tc[k] = Ar<C>::mul(ld_c<T, C>(wv[k]), ld_c<T, C>(vv[k]));
+      c = seg_sum<C, G>(tc, s.len);
+    }
+  }, w0, w1);
   if constexpr (LAST) {
-    double m = 0.0;
-#pragma unroll
-    for (int k = 0; k < G; ++k)
-      if (VEC > 1 || k < s.len) m = fmax(m, fabs(to_dbl(wv[k])));
     block_max_abs(&st->maxbits, m);
   } else {
-    load_seg<T, VEC, G>(vnext, s, vv);
-    C tc[G];
-#pragma unroll
-    for (int k = 0; k < G; ++k) tc[k] = Ar<C>::mul(ld_c<T, C>(wv[k]), ld_c<T, C>(vv[k]));
-    C sc = seg_sum<C, G>(tc, s.len);
     C h;
     double dummy;
-    if (grid_finish(sc, 0.0, g, rd, h, dummy)) st->hcol[i + 1] = to_dbl(h);
+    if (grid_finish(w0, w1, g, rd, h, dummy)) st->hcol[i + 1] = to_dbl(h);
   }
 }
 
 // x += y_0 v_0; x += y_1 v_1; ... (inner_solver.cpp:174), one pass, the
-// sequence of rounded axpys kept per element.
+// sequence of rounded axpys kept per element; x_zero: x starts at 0.
 template <class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, const T* __restrict__ V, int64_t ldv,
-                                                   int j, Geo g, DevState* st) {
-  GADI_SEG();
-  T xv[G], vv[G];
-  load_seg<T, VEC, G>(x, s, xv);
-  C xc[G];
-#pragma unroll
-  for (int k = 0; k < G; ++k) xc[k] = ld_c<T, C>(xv[k]);
-  for (int i = 0; i < j; ++i) {
-    const C y = from_dbl<C>(st->ycoef[i]);
-    load_seg<T, VEC, G>(V + (int64_t)i * ldv, s, vv);
-#pragma unroll
-    for (int k = 0; k < G; ++k) xc[k] = ld_c<T, C>(st_t<T, C>(Ar<C>::add(xc[k], Ar<C>::mul(y, ld_c<T, C>(vv[k])))));
-  }
+__global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero, const T* __restrict__ V,
+                                                   int64_t ldv, int j, Geo g, DevState* st) {
+  GADI_G;
   int bad = 0;
+  seg_each<VEC>(g, [&](const Seg& s) {
+    T xv[G], vv[G];
+    C xc[G];
+    if (!x_zero) load_seg<T, VEC, G>(x, s, xv);
 #pragma unroll
-  for (int k = 0; k < G; ++k) {
-    xv[k] = st_t<T, C>(xc[k]);
-    if (VEC > 1 || k < s.len) bad |= finite_t(xv[k]) ? 0 : 1;
-  }
-  store_seg<T, VEC, G>(x, s, xv);
+    for (int k = 0; k < G; ++k) xc[k] = x_zero ? Ar<C>::zero() : ld_c<T, C>(xv[k]);
+    for (int i = 0; i < j; ++i) {
+      const C y = from_dbl<C>(st->ycoef[i]);
+      load_seg<T, VEC, G>(V + (int64_t)i * ldv, s, vv);
+#pragma unroll
+      for (int k = 0; k < G; ++k) xc[k] = ld_c<T, C>(st_t<T, C>(Ar<C>::add(xc[k], Ar<C>::mul(y, ld_c<T, C>(vv[k])))));
+    }
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      xv[k] = st_t<T, C>(xc[k]);
+      if (GADI_LIVE(k)) bad |= finite_t(xv[k]) ? 0 : 1;
+    }
+    store_seg<T, VEC, G>(x, s, xv);
+  });
   or_flags(&st->flags, bad);
 }
 
@@ -507,21 +617,24 @@ template <class Op, int PF, int VEC>
 __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict__ x, const double* __restrict__ b,
                                                  double* __restrict__ sv, int scaling, Geo g, Red rd,
                                                  DevState* st) {
-  GADI_SEG();
-  double acc[G];
-  load_seg<double, VEC, G>(b, s, acc);
-  fold_seg<VEC, G>(op, x, s, acc, ResidAF<PF>());
-  double td[G], m = 0.0;
+  GADI_G;
+  double m = 0.0, w0, w1;
+  seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) {
+    double acc[G], xc[G];
+    load_seg<double, VEC, G>(b, s, acc);
+    fold_seg<VEC, G>(op, PlainSrc<double>{x}, s, acc, ResidAF<PF>(), xc);
+    double td[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    td[i] = acc[i] * acc[i];
-    if (VEC > 1 || i < s.len) m = (acc[i] == acc[i]) ? fmax(m, fabs(acc[i])) : m;
-  }
-  if (sv) store_seg<double, VEC, G>(sv, s, acc);
+    for (int i = 0; i < G; ++i) {
+      td[i] = __dmul_rn(acc[i], acc[i]);
+      if (GADI_LIVE(i)) m = (acc[i] == acc[i]) ? fmax(m, fabs(acc[i])) : m;
+    }
+    if (sv) store_seg<double, VEC, G>(sv, s, acc);
+    d = seg_sum<double, G>(td, s.len);
+  }, w0, w1);
   block_max_abs(&st->maxbits, m);
-  double sd = seg_sum<double, G>(td, s.len);
   double dummy, ss;
-  if (grid_finish(0.0, sd, g, rd, dummy, ss)) {
+  if (grid_finish(w0, w1, g, rd, dummy, ss)) {
     __threadfence();
     const double mx = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
     st->res_ss = ss;
@@ -534,42 +647,47 @@ __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict
 template <class T, int VEC>
 __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ sv, T* __restrict__ rhat, Geo g,
                                                      Red rd, DevState* st) {
-  GADI_SEG();
+  GADI_G;
   const int e = st->res_e;
-  double v[G], td[G];
-  load_seg<double, VEC, G>(sv, s, v);
-  T o[G];
+  double w0, w1;
+  seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) {
+    double v[G], td[G];
+    load_seg<double, VEC, G>(sv, s, v);
+    T o[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    o[i] = from_dbl<T>(e != 0 ? scalbn(v[i], -e) : v[i]);
-    const double d = to_dbl(o[i]);
-    td[i] = d * d;
-  }
-  store_seg<T, VEC, G>(rhat, s, o);
-  double sd = seg_sum<double, G>(td, s.len);
+    for (int i = 0; i < G; ++i) {
+      o[i] = from_dbl<T>(e != 0 ? scalbn(v[i], -e) : v[i]);
+      const double dv = to_dbl(o[i]);
+      td[i] = __dmul_rn(dv, dv);
+    }
+    store_seg<T, VEC, G>(rhat, s, o);
+    d = seg_sum<double, G>(td, s.len);
+  }, w0, w1);
   double dummy, ss;
-  if (grid_finish(0.0, sd, g, rd, dummy, ss)) st->rhat_ss = ss;
+  if (grid_finish(w0, w1, g, rd, dummy, ss)) st->rhat_ss = ss;
 }
 
 // x = round_u(x + round_u(2^e y)) (solver.cpp:163-166 with axpy kernels.cpp:147-164).
 template <class T, int PU, int VEC>
 __global__ void __launch_bounds__(256) k_update(double* __restrict__ x, const T* __restrict__ y, Geo g,
                                                 DevState* st) {
-  GADI_SEG();
+  GADI_G;
   const int e = st->res_e;
-  double xv[G];
-  T yv[G];
-  load_seg<double, VEC, G>(x, s, xv);
-  load_seg<T, VEC, G>(y, s, yv);
   int bad = 0;
+  seg_each<VEC>(g, [&](const Seg& s) {
+    double xv[G];
+    T yv[G];
+    load_seg<double, VEC, G>(x, s, xv);
+    load_seg<T, VEC, G>(y, s, yv);
 #pragma unroll
-  for (int i = 0; i < G; ++i) {
-    double yd = to_dbl(yv[i]);
-    if (e != 0) yd = scalbn(yd, e);
-    xv[i] = round_p<PU>(__dadd_rn(xv[i], round_p<PU>(__dmul_rn(1.0, yd))));
-    if (VEC > 1 || i < s.len) bad |= isfinite(xv[i]) ? 0 : 1;
-  }
-  store_seg<double, VEC, G>(x, s, xv);
+    for (int i = 0; i < G; ++i) {
+      double yd = to_dbl(yv[i]);
+      if (e != 0) yd = scalbn(yd, e);
+      xv[i] = round_p<PU>(__dadd_rn(xv[i], round_p<PU>(__dmul_rn(1.0, yd))));
+      if (GADI_LIVE(i)) bad |= isfinite(xv[i]) ? 0 : 1;
+    }
+    store_seg<double, VEC, G>(x, s, xv);
+  });
   or_flags(&st->xbad, bad);
 }
 
@@ -580,7 +698,7 @@ __global__ void k_convert(const TI* __restrict__ in, TO* __restrict__ out, int64
   if (i < n) out[i] = from_dbl<TO>(round_p<PR>(to_dbl(in[i])));
 }
 
-__global__ void k_fill(double* __restrict__ x, double v, int64_t n) {
+static __global__ void k_fill(double* __restrict__ x, double v, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = v;
 }
@@ -595,7 +713,7 @@ __device__ __forceinline__ double uniform01(uint64_t seed, uint64_t i, double lo
   const double u = __dmul_rn((double)(splitmix64(seed, i) >> 11), 0x1p-53);
   return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
 }
-__global__ void k_uniform(double* __restrict__ x, uint64_t seed, double lo, double hi, int64_t n) {
+static __global__ void k_uniform(double* __restrict__ x, uint64_t seed, double lo, double hi, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = uniform01(seed, (uint64_t)i, lo, hi);
 }
@@ -606,25 +724,30 @@ __global__ void k_apply(Op op, const X* __restrict__ x, Y* __restrict__ y, int64
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   Acc a[1];
+  X cc[1];
   a[0] = Ar<Acc>::zero();
-  op.template fold<1>(x, e, a, f);
+  op.template fold<1>(PlainSrc<X>{x}, e, a, f, cc);
   y[e] = st_t<Y, Acc>(a[0]);
 }
 
-// dot / norm2 over binary64-carried values in precision C (test entry points).
+// dot over binary64-carried values in precision C (test entry points).
 template <class C>
 __global__ void __launch_bounds__(256) k_dot_d(const double* __restrict__ x, const double* __restrict__ y, Geo g,
                                                Red rd, double* out) {
   constexpr int VEC = 1;
-  GADI_SEG();
-  C tc[G];
+  GADI_G;
+  C w0;
+  double w1;
+  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+    C tc[G];
 #pragma unroll
-  for (int i = 0; i < G; ++i)
-    tc[i] = i < s.len ? Ar<C>::mul(Ar<C>::from_d(x[s.lo + i]), Ar<C>::from_d(y[s.lo + i])) : Ar<C>::zero();
-  C sc = seg_sum<C, G>(tc, s.len);
+    for (int i = 0; i < G; ++i)
+      tc[i] = i < s.len ? Ar<C>::mul(Ar<C>::from_d(x[s.lo + i]), Ar<C>::from_d(y[s.lo + i])) : Ar<C>::zero();
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
   C t;
   double dummy;
-  if (grid_finish(sc, 0.0, g, rd, t, dummy)) *out = to_dbl(t);
+  if (grid_finish(w0, w1, g, rd, t, dummy)) *out = to_dbl(t);
 }
 
 }  // namespace gadi

@@ -4,11 +4,72 @@
 // the reference's per-row loops (kernels.cpp:41-54 matvec, :56-69 residual)
 // visit the CSR it builds; the caller's functor f(acc, coef, x) supplies the
 // per-entry rounding (matvec: acc + coef*x; residual: acc - coef*x).
+//
+// The operand is read through a "source" so that an elementwise producer can
+// be fused into the operator pass: PlainSrc reads a vector; PUpdSrc forms
+// p = r + beta p on the fly (CG, inner_solver.cpp:76, fused into the next
+// SpMV); ScaleSrc forms v = w / h (GMRES basis, inner_solver.cpp:134, fused
+// into the next Arnoldi matvec); ZeroSrc is the x = 0 start vector.
 #pragma once
 
 #include "gadi_common.cuh"
 
 namespace gadi {
+
+template <class T>
+struct PlainSrc {
+  const T* __restrict__ p;
+  template <int VEC>
+  __device__ __forceinline__ void vec(int64_t e0, T (&v)[VEC]) const {
+    ld_vec<T, VEC>(p, e0, v);
+  }
+  __device__ __forceinline__ T at(int64_t e) const { return p[e]; }
+};
+
+template <class T>
+struct ZeroSrc {  // the x = 0 start vector (+0 everywhere), no memory traffic
+  template <int VEC>
+  __device__ __forceinline__ void vec(int64_t, T (&v)[VEC]) const {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = from_dbl<T>(0.0);
+  }
+  __device__ __forceinline__ T at(int64_t) const { return from_dbl<T>(0.0); }
+};
+
+template <class T, class C>
+struct PUpdSrc {  // p_new = first ? r : round(r + beta * p)
+  const T* __restrict__ r;
+  const T* __restrict__ p;
+  C beta;
+  int first;
+  __device__ __forceinline__ T f(T rv, T pv) const {
+    if (first) return rv;
+    return st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv), Ar<C>::mul(beta, ld_c<T, C>(pv))));
+  }
+  template <int VEC>
+  __device__ __forceinline__ void vec(int64_t e0, T (&v)[VEC]) const {
+    T rv[VEC], pv[VEC];
+    ld_vec<T, VEC>(r, e0, rv);
+    if (!first) ld_vec<T, VEC>(p, e0, pv);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = first ? rv[i] : f(rv[i], pv[i]);
+  }
+  __device__ __forceinline__ T at(int64_t e) const { return first ? r[e] : f(r[e], p[e]); }
+};
+
+template <class T>
+struct ScaleSrc {  // v = round(inv * w), inv in binary64 (scale, kernels.cpp:166-171)
+  const T* __restrict__ w;
+  double inv;
+  __device__ __forceinline__ T f(T x) const { return from_dbl<T>(__dmul_rn(inv, to_dbl(x))); }
+  template <int VEC>
+  __device__ __forceinline__ void vec(int64_t e0, T (&v)[VEC]) const {
+    ld_vec<T, VEC>(w, e0, v);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = f(v[i]);
+  }
+  __device__ __forceinline__ T at(int64_t e) const { return f(w[e]); }
+};
 
 // 3D convection-diffusion 7-point operator, matrix free (problems.cpp:8-43):
 // row i*n^2 + j*n + k; c[] = {i-1, j-1, k-1, centre, k+1, j+1, i+1}, the
@@ -21,27 +82,28 @@ struct Stencil7 {
 
   // Fold for the VEC consecutive elements e0..e0+VEC-1 of one grid row
   // (aligned path: e0 % VEC == 0 and n % VEC == 0; VEC == 1 is any element).
-  template <int VEC, class X, class Acc, class F>
-  __device__ __forceinline__ void fold(const X* __restrict__ x, int64_t e0, Acc (&acc)[VEC], F f) const {
+  // `cc` returns the operand at the VEC centre points.
+  template <int VEC, class Src, class X, class Acc, class F>
+  __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {
     const int64_t k0 = e0 % n;
     const int64_t r = e0 / n;
     const int64_t j = r % n;
     const int64_t i = r / n;
-    X cc[VEC], nb[VEC];
-    ld_vec<X, VEC>(x, e0, cc);
+    X nb[VEC];
+    x.template vec<VEC>(e0, cc);
     if (i > 0) {
-      ld_vec<X, VEC>(x, e0 - nn, nb);
+      x.template vec<VEC>(e0 - nn, nb);
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[0], nb[v]);
     }
     if (j > 0) {
-      ld_vec<X, VEC>(x, e0 - n, nb);
+      x.template vec<VEC>(e0 - n, nb);
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[1], nb[v]);
     }
     {
       const bool has0 = k0 > 0;
-      X km0 = has0 ? x[e0 - 1] : cc[0];
+      X km0 = has0 ? x.at(e0 - 1) : cc[0];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         if (v > 0) acc[v] = f(acc[v], c[2], cc[v - 1]);
@@ -52,7 +114,7 @@ struct Stencil7 {
     for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[3], cc[v]);
     {
       const bool hasL = k0 + VEC < n;
-      X kpL = hasL ? x[e0 + VEC] : cc[0];
+      X kpL = hasL ? x.at(e0 + VEC) : cc[0];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         if (v < VEC - 1) acc[v] = f(acc[v], c[4], cc[v + 1]);
@@ -60,12 +122,12 @@ struct Stencil7 {
       }
     }
     if (j + 1 < n) {
-      ld_vec<X, VEC>(x, e0 + n, nb);
+      x.template vec<VEC>(e0 + n, nb);
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[5], nb[v]);
     }
     if (i + 1 < n) {
-      ld_vec<X, VEC>(x, e0 + nn, nb);
+      x.template vec<VEC>(e0 + nn, nb);
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[6], nb[v]);
     }
@@ -83,14 +145,15 @@ struct Csr {
   const int32_t* __restrict__ ci;
   const V* __restrict__ val;
 
-  template <int VEC, class X, class Acc, class F>
-  __device__ __forceinline__ void fold(const X* __restrict__ x, int64_t e0, Acc (&acc)[VEC], F f) const {
+  template <int VEC, class Src, class X, class Acc, class F>
+  __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {
+    x.template vec<VEC>(e0, cc);
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       const int64_t row = e0 + v;
       const int64_t b = rp[row], e = rp[row + 1];
       Acc a = acc[v];
-      for (int64_t k = b; k < e; ++k) a = f(a, val[k], x[ci[k]]);
+      for (int64_t k = b; k < e; ++k) a = f(a, val[k], x.at(ci[k]));
       acc[v] = a;
     }
   }
