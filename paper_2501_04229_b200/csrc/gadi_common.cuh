@@ -78,9 +78,21 @@ __device__ __forceinline__ double round_p(double x) {
 
 // Correctly rounded division / sqrt in C: computed in binary64, rounded once
 // (rounded_binop, precision.cpp:91-97; 53 >= 2p+2 makes it exact).
+// For binary32 the native correctly rounded division is the same value; for
+// binary16 a binary32 quotient rounded once to binary16 is too (24 >= 2*11+2).
 template <class C>
 __device__ __forceinline__ C div_c(C a, C b) {
-  return Ar<C>::from_d(__ddiv_rn(Ar<C>::to_d(a), Ar<C>::to_d(b)));
+  if constexpr (std::is_same<C, float>::value) return __fdiv_rn(a, b);
+  else if constexpr (std::is_same<C, __half>::value)
+    return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b)));
+  else return __ddiv_rn(a, b);
+}
+
+// x * 2^e exactly as ldexp/scalbn (solver.cpp:89,165): a multiply by the exact
+// power of two is the same correctly rounded value while 2^e is a normal double.
+__device__ __forceinline__ double pow2d(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+__device__ __forceinline__ double ldexp_fast(double x, int e, double p2) {
+  return (e >= -1000 && e <= 1000) ? __dmul_rn(x, p2) : scalbn(x, e);
 }
 
 // Storage <-> compute conversions (exact widening; one RN narrowing).

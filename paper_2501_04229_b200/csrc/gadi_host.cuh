@@ -68,6 +68,7 @@ inline int ilog2(int64_t v) {
   while ((int64_t(1) << (d + 1)) <= v) ++d;
   return d;
 }
+inline int lg_of(int64_t n) { return is_pow2(n) ? ilog2(n) : -1; }
 
 // 2^D segments -> lanes x warps x segments-per-lane x blocks (gadi_kernels.cuh).
 // Up to RMAX segments per lane while that still leaves >= 4 blocks per SM.
@@ -248,7 +249,7 @@ struct OuterA {
       else LV(VecTag<P_DOUBLE>{});
     };
     if (h->stencil()) {
-      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}};
+      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
       go(op);
     } else {
       Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
@@ -263,7 +264,7 @@ struct OuterA {
                                                                                           MatvecAF());
     };
     if (h->stencil()) {
-      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}};
+      Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
       go(op);
     } else {
       Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
@@ -377,6 +378,7 @@ struct Engine final : EngineBase {
       opH.n = opS.n = h->n;
       opH.nn = opS.nn = h->n * h->n;
       opH.N = opS.N = h->N;
+      opH.lg = opS.lg = lg_of(h->n);
       for (int k = 0; k < 7; ++k) {
         opH.c[k] = cval(Hc[k], u_r);
         opS.c[k] = cval(Sc[k], u_r);

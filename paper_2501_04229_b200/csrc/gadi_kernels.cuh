@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) k_scale(const T* __restrict__ src, T* __r
 // w = S v_j and h_0j = dot(w, v_0). wprev and w must be different buffers.
 template <class Op, class T, class C, int VEC, bool SCALED>
 __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ wprev, double inv,
-                                                   T* __restrict__ vj, const T* __restrict__ v0,
+                                                   T* vj, const T* v0,
                                                    T* __restrict__ w, Geo g, Red rd, DevState* st) {
   GADI_G;
   C w0;
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ 
 #pragma unroll
     for (int i = 0; i < G; ++i) wv[i] = st_t<T, C>(acc[i]);
     store_seg<T, VEC, G>(w, s, wv);
-    if (!SCALED && vj == v0) {
+    if (vj == v0) {  // step 0: v_0 is the operand just formed (never re-read)
 #pragma unroll
       for (int i = 0; i < G; ++i) v0v[i] = vv[i];
     } else {
@@ -649,6 +649,7 @@ __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ 
                                                      Red rd, DevState* st) {
   GADI_G;
   const int e = st->res_e;
+  const double p2 = (e >= -1000 && e <= 1000) ? pow2d(-e) : 1.0;
   double w0, w1;
   seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) {
     double v[G], td[G];
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ 
     T o[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-      o[i] = from_dbl<T>(e != 0 ? scalbn(v[i], -e) : v[i]);
+      o[i] = from_dbl<T>(e != 0 ? ldexp_fast(v[i], -e, p2) : v[i]);
       const double dv = to_dbl(o[i]);
       td[i] = __dmul_rn(dv, dv);
     }
@@ -673,6 +674,7 @@ __global__ void __launch_bounds__(256) k_update(double* __restrict__ x, const T*
                                                 DevState* st) {
   GADI_G;
   const int e = st->res_e;
+  const double p2 = (e >= -1000 && e <= 1000) ? pow2d(e) : 1.0;
   int bad = 0;
   seg_each<VEC>(g, [&](const Seg& s) {
     double xv[G];
@@ -682,7 +684,7 @@ __global__ void __launch_bounds__(256) k_update(double* __restrict__ x, const T*
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       double yd = to_dbl(yv[i]);
-      if (e != 0) yd = scalbn(yd, e);
+      if (e != 0) yd = ldexp_fast(yd, e, p2);
       xv[i] = round_p<PU>(__dadd_rn(xv[i], round_p<PU>(__dmul_rn(1.0, yd))));
       if (GADI_LIVE(i)) bad |= isfinite(xv[i]) ? 0 : 1;
     }

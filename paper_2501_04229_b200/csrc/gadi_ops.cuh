@@ -79,16 +79,24 @@ template <class V>
 struct Stencil7 {
   int64_t n, nn, N;
   V c[7];
+  int lg;  // log2(n) when n is a power of two (always on the aligned path), else -1
 
   // Fold for the VEC consecutive elements e0..e0+VEC-1 of one grid row
   // (aligned path: e0 % VEC == 0 and n % VEC == 0; VEC == 1 is any element).
   // `cc` returns the operand at the VEC centre points.
   template <int VEC, class Src, class X, class Acc, class F>
   __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {
-    const int64_t k0 = e0 % n;
-    const int64_t r = e0 / n;
-    const int64_t j = r % n;
-    const int64_t i = r / n;
+    int64_t k0, j, i;
+    if (lg >= 0) {  // shifts, not 64-bit division, on the hot path
+      k0 = e0 & (n - 1);
+      j = (e0 >> lg) & (n - 1);
+      i = e0 >> (2 * lg);
+    } else {
+      k0 = e0 % n;
+      const int64_t r = e0 / n;
+      j = r % n;
+      i = r / n;
+    }
     X nb[VEC];
     x.template vec<VEC>(e0, cc);
     if (i > 0) {
