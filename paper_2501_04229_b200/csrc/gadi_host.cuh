@@ -22,6 +22,7 @@
 
 #include "../../include/gadi_cuda.h"
 #include "gadi_kernels.cuh"
+#include "gadi_st25.cuh"
 
 using namespace gadi;
 
@@ -93,6 +94,50 @@ inline Geo make_geo(int64_t N, int vec) {
 
 inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
   return (N % vec == 0) && is_pow2(N / vec) && (!stencil || n % vec == 0);
+}
+
+// Geometry of the 2.5D plane-marching stencil kernels (gadi_st25.cuh) for a
+// grid of n^3 points stored as `tsize`-byte values with `nin` staged inputs.
+// ok = false when the shape does not fit (then the generic kernels run).
+inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g) {
+  const int vec = 16 / tsize;
+  if (!is_pow2(n) || n % vec != 0 || n < 8) return false;
+  const int64_t TR = n / vec;
+  if (TR > 1024) return false;
+  g.n = (int)n;
+  g.lg = ilog2(n);
+  g.nn = n * n;
+  g.TR = (int)TR;
+  g.lgTR = ilog2(TR);
+  int64_t TJ = std::max<int64_t>(1, 512 / TR);
+  TJ = std::min<int64_t>(TJ, n);
+  const int64_t chunks = TJ * TR;
+  g.threads = (int)std::min<int64_t>(256, chunks);
+  g.CPT = (int)(chunks / g.threads);
+  if (g.CPT > ST25_CPT_MAX || g.threads < 32) return false;
+  g.TJ = (int)TJ;
+  g.lgTJ = ilog2(TJ);
+  g.njt = (int)(n / TJ);
+  int64_t IL = 32;
+  while (IL > 4 && g.njt * (n / IL) < 2048) IL /= 2;
+  IL = std::min<int64_t>(IL, n);
+  g.IL = (int)IL;
+  g.nblk = (int)(g.njt * (n / IL));
+  g.stages = 3;
+  const int64_t pe = (TJ + 2) * n;
+  g.smem = 128 + (size_t)(g.stages * nin + 3) * pe * tsize;
+  if (g.smem > 200 * 1024) return false;
+  return true;
+}
+
+template <class P>
+inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  static bool attr = false;  // one attribute call per instantiation
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_st25<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  k_st25<P><<<g.nblk, g.threads, g.smem, s>>>(pol, g, rd, st);
 }
 
 template <int V>
@@ -248,7 +293,17 @@ struct OuterA {
       else if (uf == GADI_SINGLE) LV(VecTag<P_SINGLE>{});
       else LV(VecTag<P_DOUBLE>{});
     };
-    if (h->stencil()) {
+    St25Geo g25;
+    if (h->stencil() && make_st25(h->n, 8, 1, g25)) {
+      auto L = [&](auto pt) {
+        constexpr int PF = decltype(pt)::v;
+        PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x, h->d_b, s, scaling ? 1 : 0};
+        launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      };
+      if (uf == GADI_HALF) L(VecTag<P_HALF>{});
+      else if (uf == GADI_SINGLE) L(VecTag<P_SINGLE>{});
+      else L(VecTag<P_DOUBLE>{});
+    } else if (h->stencil()) {
       Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
       go(op);
     } else {
@@ -318,6 +373,8 @@ struct Engine final : EngineBase {
   C* dS = nullptr;
   int m_restart = 30;
   std::vector<T*> owned;
+  bool st25 = false;  // 2.5D TMA stencil kernels (gadi_st25.cuh) for the operator passes
+  St25Geo g25;        // sized for two staged inputs; one-input policies reuse it
 
   T* vec() {
     T* v = dalloc<T>(h->N);
@@ -336,6 +393,11 @@ struct Engine final : EngineBase {
     const int64_t N = h->N;
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
+    if constexpr (std::is_same<Op, Stencil7<C>>::value) {
+      st25 = make_st25(h->n, sizeof(T), 2, g25);
+      St25Geo g1;
+      st25 = st25 && make_st25(h->n, sizeof(T), 1, g1);
+    }
     m_restart = std::max(1, spec.restart);
     rhat = vec();
     z = vec();
@@ -412,6 +474,44 @@ struct Engine final : EngineBase {
 
   const Op& op(int which) const { return which == 1 ? opH : opS; }
 
+  // The 2.5D TMA stencil versions of the operator passes (gadi_st25.cuh);
+  // each returns false when it does not apply (CSR, or a grid shape the
+  // plane marcher does not cover) and the generic kernel runs instead.
+  bool spmvp25(const Op& o, const T* r, const T* p_in, T* p_out, int first) {
+    if constexpr (std::is_same<Op, Stencil7<C>>::value) {
+      if (!st25) return false;
+      PolSpmvp<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]},
+                         r, p_in, p_out, q, Ar_beta(), first};
+      launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      return true;
+    } else {
+      return false;
+    }
+  }
+  bool gmmatvec25(const Op& o, const T* wprev, double inv, T* vj, T* w) {
+    if constexpr (std::is_same<Op, Stencil7<C>>::value) {
+      if (!st25) return false;
+      PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev, inv, vj, V, w};
+      launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      return true;
+    } else {
+      return false;
+    }
+  }
+  bool gmresid25(const Op& o, const T* x, const T* rhs) {
+    if constexpr (std::is_same<Op, Stencil7<C>>::value) {
+      if (!st25) return false;
+      PolGmResid<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, x, rhs, gr};
+      launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      return true;
+    } else {
+      return false;
+    }
+  }
+  // beta for the fused p-update is read by the kernel from the device state;
+  // the policy carries a placeholder the kernel overwrites (see PolSpmvp::beta).
+  static C Ar_beta() { return C(); }
+
   // ------------------------------------------------------------------ CG
   // inner_solver.cpp:47-83 on the device: per iteration one fused
   // (p-update + SpMV + p.q) pass and one fused (two axpys + r.r + ||r||)
@@ -442,7 +542,8 @@ struct Engine final : EngineBase {
       const int first = it == 0;
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
+        if (!spmvp25(o, r, p_in, p_out, first))
+          k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
         k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st);
       });
       CKL();
@@ -480,7 +581,8 @@ struct Engine final : EngineBase {
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        k_gm_resid<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st);
+        if (x_zero || !gmresid25(o, x, rhs))
+          k_gm_resid<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st);
         k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
       });
       CKL();
@@ -513,7 +615,8 @@ struct Engine final : EngineBase {
         T* w = (j & 1) ? wB : wA;
         V2([&](auto vt) {
           constexpr int V_ = decltype(vt)::v;
-          k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
+          if (!gmmatvec25(o, wprev, inv, vj, w))
+            k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
           for (int i = 0; i <= j; ++i) {
             T* vi = V + (int64_t)i * N;
             if (i < j) {

@@ -1,0 +1,497 @@
+// gadi_st25.cuh — 2.5D plane-marching 7-point stencil kernels with TMA staging.
+//
+// One CTA owns a tile of TJ grid rows (j0 .. j0+TJ-1, all n points of each
+// row) over IL consecutive planes i (ib .. ib+IL-1) and marches along i, the
+// slowest index (row = i*n^2 + j*n + k, problems.cpp:14). The raw inputs of
+// each plane (TJ+2 rows including the j-halo: one contiguous range of
+// global memory) arrive by one 1-D bulk TMA copy per input
+// (cp.async.bulk ... mbarrier::complete_tx) into an S-stage shared-memory
+// ring, so each input element is read from HBM once and the copies run
+// ahead of the math. The operand of the operator (p = r + beta p for CG,
+// v = w / h for an Arnoldi step, x as is for residuals) is formed ONCE per
+// point into a 3-plane shared-memory ring (planes i-1, i, i+1), and the fold
+// reads all seven neighbours from there in the reference's stored-column
+// order (problems.cpp:28-34, kernels.cpp:47-52 / 63-66), so the arithmetic is
+// bit-identical to the generic kernels.
+//
+// Reductions: a CTA's chunk of one plane (TJ rows = TJ*n contiguous
+// entries) is one perfect pairwise subtree (lanes -> warps -> CTA); its sum
+// goes to partials[plane * (n/TJ) + tile], which are contiguous aligned
+// blocks in global order, and the last CTA folds them pairwise. The result
+// is the reference's pairwise sum bit for bit (see gadi_common.cuh).
+#pragma once
+
+#include "gadi_kernels.cuh"
+
+namespace gadi {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <class T, int VEC>
+__device__ __forceinline__ void lds16(const T* p, T (&v)[VEC]) {
+  static_assert(VEC * sizeof(T) == 16, "16-byte chunks");
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) v[i] = t[i];
+}
+template <class T, int VEC>
+__device__ __forceinline__ void sts16(T* p, const T (&v)[VEC]) {
+  uint4 u;
+  T* t = reinterpret_cast<T*>(&u);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) t[i] = v[i];
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+struct St25Geo {
+  int n, lg;      // points per direction (power of two), log2 n
+  int TJ, lgTJ;   // rows per tile
+  int IL;         // planes per CTA
+  int TR, lgTR;   // 16-byte chunks per row
+  int CPT;        // chunks per thread per plane (power of two)
+  int njt;        // tiles per plane = n / TJ
+  int nblk;       // CTAs = njt * n / IL
+  int threads;
+  int stages;
+  int64_t nn;
+  size_t smem;    // dynamic shared memory bytes
+};
+
+constexpr int ST25_CPT_MAX = 4;
+
+// ------------------------------------------------------------ the kernel
+template <class P>
+__global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd, DevState* st) {
+  using T = typename P::T;
+  using Acc = typename P::Acc;
+  using R0 = typename P::R0;
+  constexpr int VEC = 16 / sizeof(T);
+  if (pol_in.skip(st)) return;
+  P pol = pol_in;
+  pol.prepare(st);  // device-resident scalars (e.g. CG beta) the host never sees
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  const int S = g.stages;
+  const int nin = pol.nin();
+  const int n = g.n;
+  const int pe = (g.TJ + 2) * n;  // elements of one staged plane (rows j0-1 .. j0+TJ)
+  T* raw = reinterpret_cast<T*>(smem + 128);
+  T* opr = raw + (size_t)S * P::NIN * pe;
+  __shared__ __align__(8) unsigned char redb0[32 * sizeof(double)];
+  __shared__ double redb1[32];
+  __shared__ int s_last;
+  R0* red0 = reinterpret_cast<R0*>(redb0);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int jt = blockIdx.x % g.njt, ic = blockIdx.x / g.njt;
+  const int j0 = jt << g.lgTJ, ib = ic * g.IL, ie = ib + g.IL;
+  const int rlo = max(j0 - 1, 0), rhi = min(j0 + g.TJ, n - 1);
+  const uint32_t bytes_in = (uint32_t)((rhi - rlo + 1) * n * sizeof(T));
+  const int soff = (rlo - (j0 - 1)) * n;
+  const int qlo = max(ib - 1, 0), qhi = min(ie, n - 1);
+
+  auto issue = [&](int q) {  // one thread
+    const int s = (q - qlo) % S;
+    mbar_expect_tx(&bar[s], (uint32_t)nin * bytes_in);
+    for (int k = 0; k < nin; ++k)
+      bulk_g2s(raw + ((size_t)s * P::NIN + k) * pe + soff, pol.in(k) + (int64_t)q * g.nn + (int64_t)rlo * n,
+               bytes_in, &bar[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int q = qlo; q <= qhi && q < qlo + S; ++q) issue(q);
+
+  // operand of plane q (all staged rows) into ring slot q % 3
+  auto build = [&](int q) {
+    const int s = (q - qlo) % S;
+    mbar_wait(&bar[s], (uint32_t)(((q - qlo) / S) & 1));
+    const T* rs = raw + (size_t)s * P::NIN * pe;
+    T* o = opr + (size_t)(q % 3) * pe;
+    const int nch = (rhi - rlo + 1) << g.lgTR;
+    for (int c = tid; c < nch; c += blockDim.x) {
+      const int idx = soff + c * VEC;
+      T v[VEC];
+      pol.make(rs, pe, idx, v);
+      sts16<T, VEC>(o + idx, v);
+    }
+  };
+
+  if (ib - 1 >= 0) build(ib - 1);
+  build(ib);
+  __syncthreads();
+  if (tid == 0) {
+    fence_proxy_async();
+    if (ib - 1 >= 0 && ib - 1 + S <= qhi) issue(ib - 1 + S);
+    if (ib + S <= qhi) issue(ib + S);
+  }
+
+  double mloc = 0.0;
+  int flag = 0;
+  for (int i = ib; i < ie; ++i) {
+    if (i + 1 <= n - 1) build(i + 1);
+    __syncthreads();
+    if (tid == 0 && i + 1 <= n - 1 && i + 1 + S <= qhi) {
+      fence_proxy_async();
+      issue(i + 1 + S);
+    }
+    const T* om = i > 0 ? opr + (size_t)((i - 1) % 3) * pe : nullptr;
+    const T* oc = opr + (size_t)(i % 3) * pe;
+    const T* op = i < n - 1 ? opr + (size_t)((i + 1) % 3) * pe : nullptr;
+    R0 a0[ST25_CPT_MAX];
+    double a1[ST25_CPT_MAX];
+#pragma unroll
+    for (int rr = 0; rr < ST25_CPT_MAX; ++rr) {
+      if (rr < g.CPT) {
+        const int c = ((warp * g.CPT + rr) << 5) + lane;  // chunk of the tile, row major
+        const int jl = c >> g.lgTR, k0 = (c & (g.TR - 1)) * VEC;
+        const int j = j0 + jl;
+        const int sidx = (jl + 1) * n + k0;
+        const int64_t e0 = (int64_t)i * g.nn + (int64_t)j * n + k0;
+        Acc acc[VEC];
+        pol.init(e0, acc);
+        const auto& c7 = pol.c7;
+        const auto f = pol.fold();
+        T cc[VEC], nb[VEC];
+        lds16<T, VEC>(oc + sidx, cc);
+        if (om) {
+          lds16<T, VEC>(om + sidx, nb);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[0], nb[v]);
+        }
+        if (j > 0) {
+          lds16<T, VEC>(oc + sidx - n, nb);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[1], nb[v]);
+        }
+        {
+          const T km = k0 > 0 ? oc[sidx - 1] : cc[0];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            if (v > 0) acc[v] = f(acc[v], c7[2], cc[v - 1]);
+            else if (k0 > 0) acc[v] = f(acc[v], c7[2], km);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[3], cc[v]);
+        {
+          const bool hasL = k0 + VEC < n;
+          const T kp = hasL ? oc[sidx + VEC] : cc[0];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            if (v < VEC - 1) acc[v] = f(acc[v], c7[4], cc[v + 1]);
+            else if (hasL) acc[v] = f(acc[v], c7[4], kp);
+          }
+        }
+        if (j < n - 1) {
+          lds16<T, VEC>(oc + sidx + n, nb);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[5], nb[v]);
+        }
+        if (op) {
+          lds16<T, VEC>(op + sidx, nb);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[6], nb[v]);
+        }
+        R0 c0 = Ar<R0>::zero();
+        double d0 = 0.0;
+        pol.epi(e0, acc, cc, c0, d0, mloc, flag);
+        if (P::HAS_R0) a0[rr] = warp_tree(c0, 32);
+        if (P::HAS_R1) a1[rr] = warp_tree(d0, 32);
+      }
+    }
+    // tree over this warp's CPT contiguous 32-chunk blocks, then over warps
+#pragma unroll
+    for (int s2 = 1; s2 < ST25_CPT_MAX; s2 <<= 1)
+#pragma unroll
+      for (int rr = 0; rr + s2 < ST25_CPT_MAX; rr += 2 * s2)
+        if (rr + s2 < g.CPT) {
+          if (P::HAS_R0) a0[rr] = Ar<R0>::add(a0[rr], a0[rr + s2]);
+          if (P::HAS_R1) a1[rr] = __dadd_rn(a1[rr], a1[rr + s2]);
+        }
+    if (P::HAS_R0 || P::HAS_R1) {
+      if (lane == 0) {
+        if (P::HAS_R0) red0[warp] = a0[0];
+        if (P::HAS_R1) redb1[warp] = a1[0];
+      }
+      __syncthreads();
+      if (warp == 0) {
+        R0 v0 = lane < nw ? red0[lane] : Ar<R0>::zero();
+        double v1 = lane < nw ? redb1[lane] : 0.0;
+        if (lane < nw) {
+          if (P::HAS_R0) v0 = warp_tree(v0, nw);
+          if (P::HAS_R1) v1 = warp_tree(v1, nw);
+        }
+        if (lane == 0) {
+          const int64_t slot = (int64_t)i * g.njt + jt;
+          if (P::HAS_R0) rd.part0[slot] = to_dbl(v0);
+          if (P::HAS_R1) rd.part1[slot] = v1;
+        }
+      }
+    }
+    __syncthreads();  // ring slot (i+2)%3 is rebuilt next iteration
+  }
+
+  // max / flags, then the grid ticket; the last CTA folds the partials
+  if (P::HAS_MAX) block_max_abs(&st->maxbits, mloc);
+  if (P::HAS_FLAG) or_flags(pol.flag_dst(st), flag);
+  if (tid == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(rd.ticket, 1u);
+    s_last = (t == (unsigned)g.nblk - 1u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t P_ = (int64_t)n * g.njt;  // partials (power of two)
+  const int B = blockDim.x;
+  R0 t0 = Ar<R0>::zero();
+  double t1 = 0.0;
+  int cnt;
+  if (P_ <= B) {
+    if (P::HAS_R0) t0 = tid < P_ ? from_dbl<R0>(__ldcg(rd.part0 + tid)) : Ar<R0>::zero();
+    if (P::HAS_R1) t1 = tid < P_ ? __ldcg(rd.part1 + tid) : 0.0;
+    cnt = (int)P_;
+  } else {
+    const int64_t Lr = P_ / B;
+    const double* p0 = rd.part0 + (int64_t)tid * Lr;
+    const double* p1 = rd.part1 + (int64_t)tid * Lr;
+    if (P::HAS_R0) t0 = run_pairwise<R0>(Lr, [&](int64_t j) { return from_dbl<R0>(__ldcg(p0 + j)); });
+    if (P::HAS_R1) t1 = run_pairwise<double>(Lr, [&](int64_t j) { return __ldcg(p1 + j); });
+    cnt = B;
+  }
+  if (P::HAS_R0) t0 = block_tree(t0, cnt, red0);
+  if (P::HAS_R1) t1 = block_tree(t1, cnt, redb1);
+  if (tid == 0) {
+    *rd.ticket = 0u;
+    __threadfence();
+    pol.finish(t0, t1, st);
+  }
+}
+
+// ------------------------------------------------------------ policies
+#define ST25_VEC (16 / (int)sizeof(T))
+
+// CG: p = r + beta p (first: p = r), q = H p, pap = dot(p, q)  (= k_cg_spmvp)
+template <class TS, class C>
+struct PolSpmvp {
+  using T = TS;
+  using Acc = C;
+  using R0 = C;
+  static constexpr int NIN = 2;
+  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false;
+  C c7[7];
+  const T* r;
+  const T* p_in;
+  T* p_out;
+  T* q;
+  C beta;
+  int first;
+  __device__ bool skip(DevState* st) const { return *(volatile int*)&st->cg_done; }
+  __device__ void prepare(DevState* st) { beta = from_dbl<C>(st->cg_beta); }
+  __device__ int nin() const { return first ? 1 : 2; }
+  __device__ const T* in(int k) const { return k == 0 ? r : p_in; }
+  __device__ void make(const T* rs, int pe, int idx, T (&v)[ST25_VEC]) const {
+    lds16<T, ST25_VEC>(rs + idx, v);
+    if (!first) {
+      T pv[ST25_VEC];
+      lds16<T, ST25_VEC>(rs + pe + idx, pv);
+#pragma unroll
+      for (int e = 0; e < ST25_VEC; ++e)
+        v[e] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(v[e]), Ar<C>::mul(beta, ld_c<T, C>(pv[e]))));
+    }
+  }
+  __device__ MatvecF<C, T> fold() const { return MatvecF<C, T>(); }
+  __device__ void init(int64_t, C (&acc)[ST25_VEC]) const {
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) acc[e] = Ar<C>::zero();
+  }
+  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const T (&cc)[ST25_VEC], C& c, double&, double&,
+                      int&) const {
+    T qv[ST25_VEC];
+    C tc[ST25_VEC];
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) {
+      qv[e] = st_t<T, C>(acc[e]);
+      tc[e] = Ar<C>::mul(ld_c<T, C>(cc[e]), ld_c<T, C>(qv[e]));
+    }
+    st_vec<T, ST25_VEC>(q, e0, qv);
+    st_vec<T, ST25_VEC>(p_out, e0, cc);
+    c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ void finish(C pap, double, DevState* st) const {
+    const double pd = to_dbl(pap);
+    st->cg_pap = pd;
+    if (pd == 0.0 || !isfinite(pd)) cg_finish(st, (st->cg_flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
+    else st->cg_a = to_dbl(div_c<C>(from_dbl<C>(st->cg_rs), pap));
+  }
+};
+
+// Arnoldi step: v_j = round(inv * w_prev) (stored), w = S v_j, h_0j = dot(w, v_0)  (= k_gm_matvec)
+template <class TS, class C>
+struct PolGmMatvec {
+  using T = TS;
+  using Acc = C;
+  using R0 = C;
+  static constexpr int NIN = 1;
+  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false;
+  C c7[7];
+  const T* wprev;
+  double inv;
+  T* vj;
+  const T* v0;
+  T* w;
+  __device__ bool skip(DevState*) const { return false; }
+  __device__ void prepare(DevState*) {}
+  __device__ int nin() const { return 1; }
+  __device__ const T* in(int) const { return wprev; }
+  __device__ void make(const T* rs, int, int idx, T (&v)[ST25_VEC]) const {
+    lds16<T, ST25_VEC>(rs + idx, v);
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) v[e] = from_dbl<T>(__dmul_rn(inv, to_dbl(v[e])));
+  }
+  __device__ MatvecF<C, T> fold() const { return MatvecF<C, T>(); }
+  __device__ void init(int64_t, C (&acc)[ST25_VEC]) const {
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) acc[e] = Ar<C>::zero();
+  }
+  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const T (&cc)[ST25_VEC], C& c, double&, double&,
+                      int&) const {
+    T wv[ST25_VEC], v0v[ST25_VEC];
+    C tc[ST25_VEC];
+    st_vec<T, ST25_VEC>(vj, e0, cc);
+    if (vj == v0) {
+#pragma unroll
+      for (int e = 0; e < ST25_VEC; ++e) v0v[e] = cc[e];
+    } else {
+      ld_vec<T, ST25_VEC>(v0, e0, v0v);
+    }
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) {
+      wv[e] = st_t<T, C>(acc[e]);
+      tc[e] = Ar<C>::mul(ld_c<T, C>(wv[e]), ld_c<T, C>(v0v[e]));
+    }
+    st_vec<T, ST25_VEC>(w, e0, wv);
+    c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ void finish(C h, double, DevState* st) const { st->hcol[0] = to_dbl(h); }
+};
+
+// GMRES restart residual r = rhs - S x (x != 0), max|r|, ||r||, finiteness (= k_gm_resid)
+template <class TS, class C>
+struct PolGmResid {
+  using T = TS;
+  using Acc = C;
+  using R0 = C;
+  static constexpr int NIN = 1;
+  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = true;
+  C c7[7];
+  const T* x;
+  const T* rhs;
+  T* r;
+  __device__ bool skip(DevState*) const { return false; }
+  __device__ void prepare(DevState*) {}
+  __device__ int nin() const { return 1; }
+  __device__ const T* in(int) const { return x; }
+  __device__ void make(const T* rs, int, int idx, T (&v)[ST25_VEC]) const { lds16<T, ST25_VEC>(rs + idx, v); }
+  __device__ ResidF<C, T> fold() const { return ResidF<C, T>(); }
+  __device__ void init(int64_t e0, C (&acc)[ST25_VEC]) const {
+    T bv[ST25_VEC];
+    ld_vec<T, ST25_VEC>(rhs, e0, bv);
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) acc[e] = ld_c<T, C>(bv[e]);
+  }
+  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const T (&)[ST25_VEC], C&, double& d, double& m,
+                      int& flag) const {
+    T rv[ST25_VEC];
+    double td[ST25_VEC];
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) {
+      rv[e] = st_t<T, C>(acc[e]);
+      const double dv = to_dbl(rv[e]);
+      td[e] = __dmul_rn(dv, dv);
+      flag |= finite_t(rv[e]) ? 0 : 1;
+      m = (dv == dv) ? fmax(m, fabs(dv)) : m;
+    }
+    st_vec<T, ST25_VEC>(r, e0, rv);
+    d = seg_sum<double, ST25_VEC>(td, ST25_VEC);
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ void finish(C, double ss, DevState* st) const { st->red_d = ss; }
+};
+
+// Outer residual s = b - A x in u_f (binary64 carried), max|s|, ||s||, e (= k_resid_A)
+template <int PF>
+struct PolResidA {
+  using T = double;
+  using Acc = double;
+  using R0 = double;
+  static constexpr int NIN = 1;
+  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false;
+  double c7[7];
+  const double* x;
+  const double* b;
+  double* s;
+  int scaling;
+  __device__ bool skip(DevState*) const { return false; }
+  __device__ void prepare(DevState*) {}
+  __device__ int nin() const { return 1; }
+  __device__ const double* in(int) const { return x; }
+  __device__ void make(const double* rs, int, int idx, double (&v)[2]) const { lds16<double, 2>(rs + idx, v); }
+  __device__ ResidAF<PF> fold() const { return ResidAF<PF>(); }
+  __device__ void init(int64_t e0, double (&acc)[2]) const { ld_vec<double, 2>(b, e0, acc); }
+  __device__ void epi(int64_t e0, const double (&acc)[2], const double (&)[2], double&, double& d, double& m,
+                      int&) const {
+    double td[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      td[e] = __dmul_rn(acc[e], acc[e]);
+      m = (acc[e] == acc[e]) ? fmax(m, fabs(acc[e])) : m;
+    }
+    if (s) st_vec<double, 2>(s, e0, acc);
+    d = seg_sum<double, 2>(td, 2);
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ void finish(double, double ss, DevState* st) const {
+    const double mx = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
+    st->res_ss = ss;
+    st->res_max = mx;
+    st->res_e = (scaling && mx != 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
+  }
+};
+
+#undef ST25_VEC
+
+}  // namespace gadi
