@@ -99,7 +99,8 @@ inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
 // Geometry of the 2.5D plane-marching stencil kernels (gadi_st25.cuh) for a
 // grid of n^3 points stored as `tsize`-byte values with `nin` staged inputs.
 // ok = false when the shape does not fit (then the generic kernels run).
-inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g) {
+inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_chunks = 512,
+                      bool ident = false) {
   const int vec = 16 / tsize;
   if (!is_pow2(n) || n % vec != 0 || n < 8) return false;
   const int64_t TR = n / vec;
@@ -109,7 +110,7 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g) {
   g.nn = n * n;
   g.TR = (int)TR;
   g.lgTR = ilog2(TR);
-  int64_t TJ = std::max<int64_t>(1, 512 / TR);
+  int64_t TJ = std::max<int64_t>(1, target_chunks / TR);
   TJ = std::min<int64_t>(TJ, n);
   const int64_t chunks = TJ * TR;
   g.threads = (int)std::min<int64_t>(256, chunks);
@@ -123,9 +124,11 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g) {
   IL = std::min<int64_t>(IL, n);
   g.IL = (int)IL;
   g.nblk = (int)(g.njt * (n / IL));
-  g.stages = 3;
+  // operand-ring kernels: 3 raw stages + a 3-plane ring; identity-operand
+  // kernels fold from the stages directly and need 4 of them
+  g.stages = ident ? 4 : 3;
   const int64_t pe = (TJ + 2) * n;
-  g.smem = 128 + (size_t)(g.stages * nin + 3) * pe * tsize;
+  g.smem = 128 + (size_t)(g.stages * nin + (ident ? 0 : 3)) * pe * tsize;
   if (g.smem > 200 * 1024) return false;
   return true;
 }
@@ -294,7 +297,7 @@ struct OuterA {
       else LV(VecTag<P_DOUBLE>{});
     };
     St25Geo g25;
-    if (h->stencil() && make_st25(h->n, 8, 1, g25)) {
+    if (h->stencil() && make_st25(h->n, 8, 1, g25, 1024, true)) {
       auto L = [&](auto pt) {
         constexpr int PF = decltype(pt)::v;
         PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x, h->d_b, s, scaling ? 1 : 0};
@@ -374,7 +377,9 @@ struct Engine final : EngineBase {
   int m_restart = 30;
   std::vector<T*> owned;
   bool st25 = false;  // 2.5D TMA stencil kernels (gadi_st25.cuh) for the operator passes
-  St25Geo g25;        // sized for two staged inputs; one-input policies reuse it
+  St25Geo g25;        // CG p-update + SpMV: two staged inputs + operand ring
+  St25Geo g25m;       // Arnoldi matvec: one staged input + operand ring
+  St25Geo g25i;       // GMRES residual: identity operand, folded from the stages
 
   T* vec() {
     T* v = dalloc<T>(h->N);
@@ -394,9 +399,8 @@ struct Engine final : EngineBase {
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
-      st25 = make_st25(h->n, sizeof(T), 2, g25);
-      St25Geo g1;
-      st25 = st25 && make_st25(h->n, sizeof(T), 1, g1);
+      st25 = make_st25(h->n, sizeof(T), 2, g25) && make_st25(h->n, sizeof(T), 1, g25m) &&
+             make_st25(h->n, sizeof(T), 1, g25i, 512, true);
     }
     m_restart = std::max(1, spec.restart);
     rhat = vec();
@@ -492,7 +496,7 @@ struct Engine final : EngineBase {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
       PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev, inv, vj, V, w};
-      launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      launch_st25(pol, g25m, h->stream, red_of(h), h->st);
       return true;
     } else {
       return false;
@@ -502,7 +506,7 @@ struct Engine final : EngineBase {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
       PolGmResid<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, x, rhs, gr};
-      launch_st25(pol, g25, h->stream, red_of(h), h->st);
+      launch_st25(pol, g25i, h->stream, red_of(h), h->st);
       return true;
     } else {
       return false;

@@ -460,6 +460,11 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   GADI_G;
   const double m = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
   const C mc = from_dbl<C>(m);
+  // w/m for binary16/32 operands: round(w * RN64(1/m)) is the correctly
+  // rounded quotient (the binary64 product is within 2^-52 of w/m, and a
+  // quotient of p-bit numbers is either exact in p bits or at least 2^-2p-1
+  // away from a p-bit rounding boundary, p <= 24); binary64 divides.
+  const double rinv = __ddiv_rn(1.0, m);
   C w0;
   double w1;
   seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
@@ -468,7 +473,9 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
     C tc[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-      const C qv = div_c<C>(ld_c<T, C>(wv[i]), mc);
+      C qv;
+      if constexpr (std::is_same<C, double>::value) qv = div_c<C>(ld_c<T, C>(wv[i]), mc);
+      else qv = Ar<C>::from_d(__dmul_rn(to_dbl(wv[i]), rinv));
       tc[i] = Ar<C>::mul(qv, qv);
     }
     c = seg_sum<C, G>(tc, s.len);

@@ -147,27 +147,45 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
     }
   };
 
-  if (ib - 1 >= 0) build(ib - 1);
-  build(ib);
-  __syncthreads();
-  if (tid == 0) {
-    fence_proxy_async();
-    if (ib - 1 >= 0 && ib - 1 + S <= qhi) issue(ib - 1 + S);
-    if (ib + S <= qhi) issue(ib + S);
+  // IDENT policies (the operand is input 0 as stored: residuals) fold
+  // straight from the staged planes: S >= 4 stages hold planes i-1, i, i+1
+  // while i+2.. are in flight, and no operand ring is built.
+  auto stage_of = [&](int q) { return raw + (size_t)((q - qlo) % S) * P::NIN * pe; };
+  auto wait_q = [&](int q) { mbar_wait(&bar[(q - qlo) % S], (uint32_t)(((q - qlo) / S) & 1)); };
+  if constexpr (P::IDENT) {
+    if (ib - 1 >= 0) wait_q(ib - 1);
+    wait_q(ib);
+  } else {
+    if (ib - 1 >= 0) build(ib - 1);
+    build(ib);
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async();
+      if (ib - 1 >= 0 && ib - 1 + S <= qhi) issue(ib - 1 + S);
+      if (ib + S <= qhi) issue(ib + S);
+    }
   }
 
   double mloc = 0.0;
   int flag = 0;
   for (int i = ib; i < ie; ++i) {
-    if (i + 1 <= n - 1) build(i + 1);
-    __syncthreads();
-    if (tid == 0 && i + 1 <= n - 1 && i + 1 + S <= qhi) {
-      fence_proxy_async();
-      issue(i + 1 + S);
+    const T *om, *oc, *op;
+    if constexpr (P::IDENT) {
+      if (i + 1 <= n - 1) wait_q(i + 1);
+      om = i > 0 ? stage_of(i - 1) : nullptr;
+      oc = stage_of(i);
+      op = i < n - 1 ? stage_of(i + 1) : nullptr;
+    } else {
+      if (i + 1 <= n - 1) build(i + 1);
+      __syncthreads();
+      if (tid == 0 && i + 1 <= n - 1 && i + 1 + S <= qhi) {
+        fence_proxy_async();
+        issue(i + 1 + S);
+      }
+      om = i > 0 ? opr + (size_t)((i - 1) % 3) * pe : nullptr;
+      oc = opr + (size_t)(i % 3) * pe;
+      op = i < n - 1 ? opr + (size_t)((i + 1) % 3) * pe : nullptr;
     }
-    const T* om = i > 0 ? opr + (size_t)((i - 1) % 3) * pe : nullptr;
-    const T* oc = opr + (size_t)(i % 3) * pe;
-    const T* op = i < n - 1 ? opr + (size_t)((i + 1) % 3) * pe : nullptr;
     R0 a0[ST25_CPT_MAX];
     double a1[ST25_CPT_MAX];
 #pragma unroll
@@ -260,6 +278,12 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
       }
     }
     __syncthreads();  // ring slot (i+2)%3 is rebuilt next iteration
+    if constexpr (P::IDENT) {  // plane i-1 is no longer read: refill its stage
+      if (tid == 0 && i - 1 >= qlo && i - 1 + S <= qhi) {
+        fence_proxy_async();
+        issue(i - 1 + S);
+      }
+    }
   }
 
   // max / flags, then the grid ticket; the last CTA folds the partials
@@ -309,7 +333,7 @@ struct PolSpmvp {
   using Acc = C;
   using R0 = C;
   static constexpr int NIN = 2;
-  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false;
+  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
   C c7[7];
   const T* r;
   const T* p_in;
@@ -365,7 +389,7 @@ struct PolGmMatvec {
   using Acc = C;
   using R0 = C;
   static constexpr int NIN = 1;
-  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false;
+  static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
   C c7[7];
   const T* wprev;
   double inv;
@@ -416,7 +440,7 @@ struct PolGmResid {
   using Acc = C;
   using R0 = C;
   static constexpr int NIN = 1;
-  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = true;
+  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = true, IDENT = true;
   C c7[7];
   const T* x;
   const T* rhs;
@@ -459,7 +483,7 @@ struct PolResidA {
   using Acc = double;
   using R0 = double;
   static constexpr int NIN = 1;
-  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false;
+  static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false, IDENT = true;
   double c7[7];
   const double* x;
   const double* b;
