@@ -19,6 +19,23 @@
  * bit-exact over all 65,536 encodings + random doubles in test_oracle_pin.py. */
 static double round_half(double x) {
   if (isnan(x) || isinf(x) || x == 0.0) return x;
+  {
+    /* normal binary16 range: round the 52-bit fraction to 10 bits in the
+     * integer domain (ties to even); a carry into the exponent is the
+     * correctly rounded next binade */
+    uint64_t u;
+    memcpy(&u, &x, 8);
+    const uint64_t sgn = u & 0x8000000000000000ull, mag = u & 0x7fffffffffffffffull;
+    const double ax = fabs(x);
+    if (ax >= 0x1p-14 && ax < 65520.0) {
+      const uint64_t keep = (mag >> 42) & 1u;
+      uint64_t m2 = (mag + (((uint64_t)1 << 41) - 1u) + keep) & ~(((uint64_t)1 << 42) - 1u);
+      m2 |= sgn;
+      double r;
+      memcpy(&r, &m2, 8);
+      return r;
+    }
+  }
   double ax = fabs(x);
   if (ax >= 65520.0) return copysign(INFINITY, x);
   int e = ilogb(ax);

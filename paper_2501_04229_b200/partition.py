@@ -1,0 +1,104 @@
+"""Host-side z-slab partition logic for the multi-GPU solve.
+
+The 3D grid's rows are i*n^2 + j*n + k with i slowest (problems.cpp:14), so
+rank r of G owns the contiguous planes [r*n/G, (r+1)*n/G): N/G consecutive
+unknowns. One 7-point operator application needs one halo plane from each
+neighbour; every dot product / norm needs one scalar exchange.
+
+Determinism and parity: with G and n powers of two each rank's slab is an
+aligned power-of-two block of the reference's pairwise-sum tree
+(kernels.cpp:33-39), so the G slab partials combined by a perfect binary tree
+in rank order give the single-device (and reference) value bit for bit.
+`allreduce_pairwise` does exactly that over any torch.distributed backend
+(all-gather of the G partials, then the same tree on every rank) instead of
+an allreduce whose summation order the backend chooses.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    world: int
+    n: int
+    plane_lo: int      # first owned plane
+    plane_hi: int      # one past the last owned plane
+    halo_lo: bool      # needs plane plane_lo-1 from rank-1
+    halo_hi: bool      # needs plane plane_hi from rank+1
+
+    @property
+    def planes(self) -> int:
+        return self.plane_hi - self.plane_lo
+
+    @property
+    def row_lo(self) -> int:
+        return self.plane_lo * self.n * self.n
+
+    @property
+    def rows(self) -> int:
+        return self.planes * self.n * self.n
+
+
+def is_pow2(v: int) -> bool:
+    return v > 0 and (v & (v - 1)) == 0
+
+
+def slab_plan(n: int, world: int, rank: int) -> Slab:
+    """Contiguous planes per rank; requires world | n (the bitwise-parity
+    guarantee additionally needs n and world powers of two)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if n % world:
+        raise ValueError(f"z-slab partition needs world ({world}) to divide n ({n})")
+    per = n // world
+    lo, hi = rank * per, (rank + 1) * per
+    return Slab(rank, world, n, lo, hi, lo > 0, hi < n)
+
+
+def pairwise_tree(values: Sequence, add: Callable):
+    """Perfect binary tree over len(values) (a power of two) in index order."""
+    vals = list(values)
+    if not is_pow2(len(vals)):
+        raise ValueError("pairwise_tree needs a power-of-two count")
+    while len(vals) > 1:
+        vals = [add(vals[i], vals[i + 1]) for i in range(0, len(vals), 2)]
+    return vals[0]
+
+
+def allreduce_pairwise(partial: float, add: Callable, group=None) -> float:
+    """Gather every rank's partial and fold them in rank order on every rank:
+    deterministic, identical everywhere, and equal to the single-device
+    pairwise sum when the slabs are aligned power-of-two blocks."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    t = torch.tensor([partial], dtype=torch.float64)
+    out = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return pairwise_tree([float(o.item()) for o in out], add)
+
+
+def exchange_halos(slab: Slab, lo_plane, hi_plane, group=None):
+    """Send my first/last owned plane to rank-1/rank+1 and receive theirs.
+    lo_plane / hi_plane are contiguous torch tensors (n*n values); returns
+    (halo_below, halo_above), None where there is no neighbour."""
+    import torch
+    import torch.distributed as dist
+
+    reqs = []
+    below = above = None
+    if slab.halo_lo:
+        below = torch.empty_like(lo_plane)
+        reqs.append(dist.irecv(below, slab.rank - 1, group=group))
+        reqs.append(dist.isend(lo_plane.contiguous(), slab.rank - 1, group=group))
+    if slab.halo_hi:
+        above = torch.empty_like(hi_plane)
+        reqs.append(dist.irecv(above, slab.rank + 1, group=group))
+        reqs.append(dist.isend(hi_plane.contiguous(), slab.rank + 1, group=group))
+    for r in reqs:
+        r.wait()
+    return below, above

@@ -1,0 +1,96 @@
+"""Generate the golden vectors in tests/golden/ from the REFERENCE itself.
+
+Runs the reference's own code (oracle/_ref/libgadi_ref.so, compiled from
+/root/reference/proj/core by oracle/Makefile.ref) on small seeded inputs and
+stores inputs + outputs as .npz fixtures. The CPU tests pin the oracle
+restatement to these files bit for bit, and the GPU tests compare the device
+path with them, so neither needs /root/reference at run time.
+
+    make -f oracle/Makefile.ref && python tests/golden/make_golden.py
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle import CG, DOUBLE, GMRES, HALF, SINGLE, Config, Oracle, Reference  # noqa: E402
+
+
+def main():
+    R = Reference()
+    o = Oracle()  # used only for the seeded generators (themselves pinned below)
+    out = {}
+
+    # 1. rounding KATs: all 65,536 binary16 encodings re-rounded, and random doubles
+    enc = np.arange(65536, dtype=np.uint16).view(np.float16).astype(np.float64)
+    enc = enc[np.isfinite(enc)]
+    rng = np.random.default_rng(20250104)
+    rand = rng.standard_normal(20000) * 10.0 ** rng.integers(-9, 6, 20000)
+    edge = np.array([65504.0, 65519.999, 65520.0, 2.0 ** -24, 2.0 ** -25, 1.5 * 2.0 ** -25, 3 * 2.0 ** -26,
+                     -0.0, 0.0, 1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11, 2.0 ** -14 * (1 - 2.0 ** -11)])
+    xs = np.concatenate([enc, rand, edge])
+    out["round_x"] = xs
+    for p, nm in ((HALF, "half"), (SINGLE, "single")):
+        out[f"round_{nm}"] = R.round(xs, p)
+
+    # 2. the reference generator (build_convdiff3d, beta = 1, x = ones)
+    for n in (3, 4, 8):
+        A, b = R.convdiff(n)
+        out[f"convdiff{n}_rp"], out[f"convdiff{n}_ci"], out[f"convdiff{n}_v"], out[f"convdiff{n}_b"] = A.rp, A.ci, A.v, b
+
+    # 3. kernels on convdiff n = 5 (N = 125, not a power of two) and n = 8
+    for n in (5, 8):
+        A, _ = R.convdiff(n)
+        x = rng.uniform(-1, 1, A.n)
+        bb = rng.uniform(-3, 3, A.n)
+        out[f"k{n}_x"], out[f"k{n}_b"] = x, bb
+        for p, nm in ((HALF, "h"), (SINGLE, "s"), (DOUBLE, "d")):
+            xr = R.round(x, p)
+            out[f"k{n}_xr_{nm}"] = xr
+            out[f"k{n}_matvec_{nm}"] = R.matvec(A, xr, p)
+            out[f"k{n}_resid_{nm}"] = R.residual(A, xr, bb, p, DOUBLE)
+            out[f"k{n}_dot_{nm}"] = np.array([R.dot(xr, R.round(bb, p), p)])
+            out[f"k{n}_norm2_{nm}"] = np.array([R.norm2(R.round(bb, p), p)])
+        H, S = R.regularize(A, 0.5)
+        out[f"k{n}_H_rp"], out[f"k{n}_H_ci"], out[f"k{n}_H_v"], out[f"k{n}_S_v"] = H.rp, H.ci, H.v, S.v
+        for p, nm in ((HALF, "h"), (SINGLE, "s"), (DOUBLE, "d")):
+            rhs = R.round(rng.uniform(-1, 1, A.n), p)
+            stop = R.norm2_64(rhs)
+            out[f"k{n}_rhs_{nm}"] = rhs
+            for meth, mn, M in ((CG, "cg", H), (GMRES, "gm", S)):
+                x, it, st = R.krylov(M, rhs, meth, 1e-6, 60, 10, p, stop)
+                out[f"k{n}_{mn}_{nm}_x"] = x
+                out[f"k{n}_{mn}_{nm}_info"] = np.array([it, st])
+
+    # 4. whole solves on seeded systems from the shared splitmix64 generator
+    solves = [("s16", 16, SINGLE, 0.1, 0, 0.0, 1.0), ("h16", 16, HALF, 0.1, 0, 0.0, 1.0),
+              ("d8", 8, DOUBLE, 0.5, 0, 0.0, 1.0), ("s8b", 8, SINGLE, 0.2, 1, -1.0, 1.0)]
+    for tag, n, ur, alpha, seed, lo, hi in solves:
+        A = o.convdiff(n)
+        _, b = o.make_rhs(A, seed, lo, hi)
+        cfg = Config.make(alpha=alpha, xi=1e-20, u_r=ur, method=CG, tol_epsilon=1e-12, max_inner_iters=50)
+        x, rep, hist = R.solve(A, b, cfg)
+        out[f"solve_{tag}_b"] = b
+        out[f"solve_{tag}_x"] = x
+        out[f"solve_{tag}_hist"] = hist
+        out[f"solve_{tag}_info"] = np.array([rep.status, rep.outer_iters, rep.inner_iter_totals,
+                                             rep.inner_stagnations], dtype=np.int64)
+        out[f"solve_{tag}_cfg"] = np.array([n, ur, alpha, seed, lo, hi])
+
+    # 5. GPR fit/predict through the reference's gpr.cpp (Eigen restated in oracle/eigen_shim)
+    sizes = np.array([8 ** 3, 12 ** 3, 16 ** 3, 24 ** 3, 32 ** 3, 48 ** 3, 64 ** 3], dtype=np.int64)
+    alphas = 0.5 * sizes.astype(np.float64) ** (-1.0 / 3.0) * (1.0 + 0.05 * rng.standard_normal(len(sizes)))
+    q = np.array([10 ** 3, 20 ** 3, 40 ** 3, 100 ** 3, 200 ** 3], dtype=np.int64)
+    mean, sd, params = R.gpr(sizes, alphas, q)
+    out["gpr_sizes"], out["gpr_alphas"], out["gpr_q"] = sizes, alphas, q
+    out["gpr_mean"], out["gpr_sd"], out["gpr_params"] = mean, sd, params
+
+    path = os.path.join(HERE, "reference_vectors.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes, {len(out)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
