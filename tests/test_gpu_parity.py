@@ -136,3 +136,42 @@ def test_device_dot_norm2_bitwise(orc, n, p):
     y = orc.round(rng.uniform(-1, 1, n), p)
     assert same([g.device_dot(x, y, g.Precision(p))], [orc.dot(x, y, p)])
     assert same([g.device_norm2(x, g.Precision(p))], [orc.norm2(x, p)])
+
+
+# ---- the device path against the reference's own outputs (tests/golden) ----
+GOLD = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "reference_vectors.npz")
+PREC = {"h": HALF, "s": SINGLE, "d": DOUBLE}
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+@pytest.mark.parametrize("n", [5, 8])
+@pytest.mark.parametrize("p", ["h", "s", "d"])
+@pytest.mark.parametrize("meth", ["cg", "gm"])
+def test_golden_krylov(gold, n, p, meth):
+    sysx = g.CudaGadiSystem(g.build_convdiff3d(n))
+    sysx.prepare(0.5, 1.0, g.Precision(PREC[p]),
+                 g.InnerSolverSpec(g.InnerMethod.Cg if meth == "cg" else g.InnerMethod.Gmres, 1e-6, 60, 10))
+    rhs = gold[f"k{n}_rhs_{p}"]
+    from oracle import Oracle
+    sysx.set_inner_stop_norm(Oracle().norm2_64(rhs))
+    x, it, st = sysx.solve_H(rhs) if meth == "cg" else sysx.solve_S(rhs)
+    assert [it, int(st)] == list(gold[f"k{n}_{meth}_{p}_info"])
+    assert same(x, gold[f"k{n}_{meth}_{p}_x"])
+
+
+@pytest.mark.parametrize("tag", ["s16", "h16", "d8", "s8b"])
+def test_golden_solve(gold, tag):
+    n, ur, alpha, seed, lo, hi = gold[f"solve_{tag}_cfg"]
+    S = g.build_convdiff3d(int(n))
+    cfg = g.GadiConfig(alpha=alpha, xi=1e-20, u_r=g.Precision(int(ur)),
+                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 50, 30))
+    res = g.gadi_ir_solve(S, gold[f"solve_{tag}_b"], g.hss_split(S), cfg)
+    info = gold[f"solve_{tag}_info"]
+    assert [int(res.report.status), res.report.outer_iters, res.report.inner_iter_totals,
+            res.report.inner_stagnations] == list(info)
+    assert same(res.x, gold[f"solve_{tag}_x"])
+    np.testing.assert_allclose(res.report.rel_residual_history, gold[f"solve_{tag}_hist"], rtol=HIST_RTOL, atol=0)
