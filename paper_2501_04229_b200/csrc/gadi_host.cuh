@@ -100,7 +100,8 @@ inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
 // grid of n^3 points stored as `tsize`-byte values with `nin` staged inputs.
 // ok = false when the shape does not fit (then the generic kernels run).
 inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_chunks = 512,
-                      bool ident = false) {
+                      bool ident = false, int ring_tsize = 0) {
+  if (ring_tsize == 0) ring_tsize = tsize;
   const int vec = 16 / tsize;
   if (!is_pow2(n) || n % vec != 0 || n < 8) return false;
   const int64_t TR = n / vec;
@@ -128,7 +129,14 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   // kernels fold from the stages directly and need 4 of them
   g.stages = ident ? 4 : 3;
   const int64_t pe = (TJ + 2) * n;
-  g.smem = 128 + (size_t)(g.stages * nin + (ident ? 0 : 3)) * pe * tsize;
+  auto bytes = [&]() {
+    return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)3 * pe * ring_tsize);
+  };
+  g.smem = bytes();
+  if (!ident && g.smem > 110 * 1024) {  // keep two CTAs per SM
+    g.stages = 2;
+    g.smem = bytes();
+  }
   if (g.smem > 200 * 1024) return false;
   return true;
 }
@@ -399,7 +407,8 @@ struct Engine final : EngineBase {
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
-      st25 = make_st25(h->n, sizeof(T), 2, g25) && make_st25(h->n, sizeof(T), 1, g25m) &&
+      constexpr int rsz = sizeof(typename RingOf<T, C>::type);
+      st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz) && make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz) &&
              make_st25(h->n, sizeof(T), 1, g25i, 512, true);
     }
     m_restart = std::max(1, spec.restart);

@@ -245,23 +245,27 @@ __device__ __forceinline__ void fold_seg(const Op& op, const Src& x, const Seg& 
 
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
+  static constexpr bool PACKED = true, NEG = false;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::add(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <class C, class T>
 struct ResidF {  // acc - coef * x (kernels.cpp:63-66)
+  static constexpr bool PACKED = true, NEG = true;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::sub(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <int P>
 struct ResidAF {  // binary64-carried residual rounded to u_f per op
+  static constexpr bool PACKED = false, NEG = false;
   __device__ __forceinline__ double operator()(double a, double coef, double xv) const {
     return round_p<P>(__dsub_rn(a, round_p<P>(__dmul_rn(coef, xv))));
   }
 };
 struct MatvecAF {  // b = A x in binary64 (problems.cpp:44)
+  static constexpr bool PACKED = false, NEG = false;
   __device__ __forceinline__ double operator()(double a, double coef, double xv) const {
     return __dadd_rn(a, __dmul_rn(coef, xv));
   }

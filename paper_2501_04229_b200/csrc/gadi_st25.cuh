@@ -70,6 +70,57 @@ __device__ __forceinline__ void sts16(T* p, const T (&v)[VEC]) {
   *reinterpret_cast<uint4*>(p) = u;
 }
 
+// VEC values of R from / to shared memory in 16-byte pieces.
+template <class R, int VEC>
+__device__ __forceinline__ void lds_vec(const R* p, R (&v)[VEC]) {
+  constexpr int per = 16 / sizeof(R);
+  static_assert(VEC % per == 0, "whole 16-byte pieces");
+#pragma unroll
+  for (int b = 0; b < VEC / per; ++b) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p + b * per);
+    const R* t = reinterpret_cast<const R*>(&u);
+#pragma unroll
+    for (int i = 0; i < per; ++i) v[b * per + i] = t[i];
+  }
+}
+template <class R, int VEC>
+__device__ __forceinline__ void sts_vec(R* p, const R (&v)[VEC]) {
+  constexpr int per = 16 / sizeof(R);
+#pragma unroll
+  for (int b = 0; b < VEC / per; ++b) {
+    uint4 u;
+    R* t = reinterpret_cast<R*>(&u);
+#pragma unroll
+    for (int i = 0; i < per; ++i) t[i] = v[b * per + i];
+    *reinterpret_cast<uint4*>(p + b * per) = u;
+  }
+}
+
+// acc[v] = f(acc[v], coef, x[v]) for all v, except v = 0 / v = VEC-1 when the
+// neighbour is absent (skip0 / skipL). binary32 matvec / residual folds use
+// the paired FADD2/FMUL2 (one RN rounding per lane, the same values as the
+// scalar __fadd_rn/__fmul_rn; a - c*x == a + (-c)*x exactly in IEEE).
+template <class F, class A, class X, int VEC>
+__device__ __forceinline__ void fold_vec(const F& f, A (&acc)[VEC], A coef, const X (&x)[VEC], bool skip0,
+                                         bool skipL) {
+  const A a0 = acc[0], aL = acc[VEC - 1];
+  if constexpr (std::is_same<A, float>::value && std::is_same<X, float>::value && (VEC % 2 == 0) && F::PACKED) {
+    const float cf = F::NEG ? -coef : coef;
+    const float2 c2 = make_float2(cf, cf);
+#pragma unroll
+    for (int v = 0; v < VEC; v += 2) {
+      const float2 r = __fadd2_rn(make_float2(acc[v], acc[v + 1]), __fmul2_rn(c2, make_float2(x[v], x[v + 1])));
+      acc[v] = r.x;
+      acc[v + 1] = r.y;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], coef, x[v]);
+  }
+  if (skip0) acc[0] = a0;
+  if (skipL) acc[VEC - 1] = aL;
+}
+
 struct St25Geo {
   int n, lg;      // points per direction (power of two), log2 n
   int TJ, lgTJ;   // rows per tile
@@ -92,6 +143,8 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   using T = typename P::T;
   using Acc = typename P::Acc;
   using R0 = typename P::R0;
+  using RT = typename P::RT;  // operand ring element: C when widening binary16 is free, else T
+  static_assert(!P::IDENT || std::is_same<RT, T>::value, "identity operands are folded from the stages");
   constexpr int VEC = 16 / sizeof(T);
   if (pol_in.skip(st)) return;
   P pol = pol_in;
@@ -103,7 +156,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   const int n = g.n;
   const int pe = (g.TJ + 2) * n;  // elements of one staged plane (rows j0-1 .. j0+TJ)
   T* raw = reinterpret_cast<T*>(smem + 128);
-  T* opr = raw + (size_t)S * P::NIN * pe;
+  RT* opr = reinterpret_cast<RT*>(raw + (size_t)S * P::NIN * pe);
   __shared__ __align__(8) unsigned char redb0[32 * sizeof(double)];
   __shared__ double redb1[32];
   __shared__ int s_last;
@@ -137,13 +190,13 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
     const int s = (q - qlo) % S;
     mbar_wait(&bar[s], (uint32_t)(((q - qlo) / S) & 1));
     const T* rs = raw + (size_t)s * P::NIN * pe;
-    T* o = opr + (size_t)(q % 3) * pe;
+    RT* o = opr + (size_t)(q % 3) * pe;
     const int nch = (rhi - rlo + 1) << g.lgTR;
     for (int c = tid; c < nch; c += blockDim.x) {
       const int idx = soff + c * VEC;
-      T v[VEC];
+      RT v[VEC];
       pol.make(rs, pe, idx, v);
-      sts16<T, VEC>(o + idx, v);
+      sts_vec<RT, VEC>(o + idx, v);
     }
   };
 
@@ -169,7 +222,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   double mloc = 0.0;
   int flag = 0;
   for (int i = ib; i < ie; ++i) {
-    const T *om, *oc, *op;
+    const RT *om, *oc, *op;
     if constexpr (P::IDENT) {
       if (i + 1 <= n - 1) wait_q(i + 1);
       om = i > 0 ? stage_of(i - 1) : nullptr;
@@ -200,46 +253,37 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
         pol.init(e0, acc);
         const auto& c7 = pol.c7;
         const auto f = pol.fold();
-        T cc[VEC], nb[VEC];
-        lds16<T, VEC>(oc + sidx, cc);
+        RT cc[VEC], nb[VEC];
+        lds_vec<RT, VEC>(oc + sidx, cc);
+        // the seven neighbours in stored-column order; an absent neighbour is
+        // skipped, never folded as a zero (fold_vec restores acc there)
         if (om) {
-          lds16<T, VEC>(om + sidx, nb);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[0], nb[v]);
+          lds_vec<RT, VEC>(om + sidx, nb);
+          fold_vec(f, acc, c7[0], nb, false, false);
         }
         if (j > 0) {
-          lds16<T, VEC>(oc + sidx - n, nb);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[1], nb[v]);
+          lds_vec<RT, VEC>(oc + sidx - n, nb);
+          fold_vec(f, acc, c7[1], nb, false, false);
         }
-        {
-          const T km = k0 > 0 ? oc[sidx - 1] : cc[0];
+        nb[0] = k0 > 0 ? oc[sidx - 1] : cc[0];
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            if (v > 0) acc[v] = f(acc[v], c7[2], cc[v - 1]);
-            else if (k0 > 0) acc[v] = f(acc[v], c7[2], km);
-          }
-        }
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[3], cc[v]);
+        for (int v = 1; v < VEC; ++v) nb[v] = cc[v - 1];
+        fold_vec(f, acc, c7[2], nb, k0 == 0, false);
+        fold_vec(f, acc, c7[3], cc, false, false);
         {
           const bool hasL = k0 + VEC < n;
-          const T kp = hasL ? oc[sidx + VEC] : cc[0];
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            if (v < VEC - 1) acc[v] = f(acc[v], c7[4], cc[v + 1]);
-            else if (hasL) acc[v] = f(acc[v], c7[4], kp);
-          }
+          for (int v = 0; v < VEC - 1; ++v) nb[v] = cc[v + 1];
+          nb[VEC - 1] = hasL ? oc[sidx + VEC] : cc[0];
+          fold_vec(f, acc, c7[4], nb, false, !hasL);
         }
         if (j < n - 1) {
-          lds16<T, VEC>(oc + sidx + n, nb);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[5], nb[v]);
+          lds_vec<RT, VEC>(oc + sidx + n, nb);
+          fold_vec(f, acc, c7[5], nb, false, false);
         }
         if (op) {
-          lds16<T, VEC>(op + sidx, nb);
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c7[6], nb[v]);
+          lds_vec<RT, VEC>(op + sidx, nb);
+          fold_vec(f, acc, c7[6], nb, false, false);
         }
         R0 c0 = Ar<R0>::zero();
         double d0 = 0.0;
@@ -326,12 +370,24 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
 // ------------------------------------------------------------ policies
 #define ST25_VEC (16 / (int)sizeof(T))
 
+// The operand ring holds binary16 operands widened to binary32 when the
+// arithmetic is binary32 (exact; saves a conversion per neighbour use).
+template <class T, class C>
+struct RingOf {
+  using type = T;
+};
+template <>
+struct RingOf<__half, float> {
+  using type = float;
+};
+
 // CG: p = r + beta p (first: p = r), q = H p, pap = dot(p, q)  (= k_cg_spmvp)
 template <class TS, class C>
 struct PolSpmvp {
   using T = TS;
   using Acc = C;
   using R0 = C;
+  using RT = typename RingOf<T, C>::type;
   static constexpr int NIN = 2;
   static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
   C c7[7];
@@ -345,32 +401,37 @@ struct PolSpmvp {
   __device__ void prepare(DevState* st) { beta = from_dbl<C>(st->cg_beta); }
   __device__ int nin() const { return first ? 1 : 2; }
   __device__ const T* in(int k) const { return k == 0 ? r : p_in; }
-  __device__ void make(const T* rs, int pe, int idx, T (&v)[ST25_VEC]) const {
-    lds16<T, ST25_VEC>(rs + idx, v);
-    if (!first) {
+  __device__ void make(const T* rs, int pe, int idx, RT (&v)[ST25_VEC]) const {
+    T rv[ST25_VEC];
+    lds16<T, ST25_VEC>(rs + idx, rv);
+    if (first) {
+#pragma unroll
+      for (int e = 0; e < ST25_VEC; ++e) v[e] = ld_c<T, RT>(rv[e]);
+    } else {
       T pv[ST25_VEC];
       lds16<T, ST25_VEC>(rs + pe + idx, pv);
 #pragma unroll
       for (int e = 0; e < ST25_VEC; ++e)
-        v[e] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(v[e]), Ar<C>::mul(beta, ld_c<T, C>(pv[e]))));
+        v[e] = ld_c<T, RT>(st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[e]), Ar<C>::mul(beta, ld_c<T, C>(pv[e])))));
     }
   }
-  __device__ MatvecF<C, T> fold() const { return MatvecF<C, T>(); }
+  __device__ MatvecF<C, RT> fold() const { return MatvecF<C, RT>(); }
   __device__ void init(int64_t, C (&acc)[ST25_VEC]) const {
 #pragma unroll
     for (int e = 0; e < ST25_VEC; ++e) acc[e] = Ar<C>::zero();
   }
-  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const T (&cc)[ST25_VEC], C& c, double&, double&,
+  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const RT (&cc)[ST25_VEC], C& c, double&, double&,
                       int&) const {
-    T qv[ST25_VEC];
+    T qv[ST25_VEC], pv[ST25_VEC];
     C tc[ST25_VEC];
 #pragma unroll
     for (int e = 0; e < ST25_VEC; ++e) {
       qv[e] = st_t<T, C>(acc[e]);
-      tc[e] = Ar<C>::mul(ld_c<T, C>(cc[e]), ld_c<T, C>(qv[e]));
+      pv[e] = st_t<T, RT>(cc[e]);  // exact: cc holds a T value
+      tc[e] = Ar<C>::mul(ld_c<RT, C>(cc[e]), ld_c<T, C>(qv[e]));
     }
     st_vec<T, ST25_VEC>(q, e0, qv);
-    st_vec<T, ST25_VEC>(p_out, e0, cc);
+    st_vec<T, ST25_VEC>(p_out, e0, pv);
     c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
   }
   __device__ int* flag_dst(DevState* st) const { return &st->flags; }
@@ -388,6 +449,7 @@ struct PolGmMatvec {
   using T = TS;
   using Acc = C;
   using R0 = C;
+  using RT = typename RingOf<T, C>::type;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
   C c7[7];
@@ -400,31 +462,37 @@ struct PolGmMatvec {
   __device__ void prepare(DevState*) {}
   __device__ int nin() const { return 1; }
   __device__ const T* in(int) const { return wprev; }
-  __device__ void make(const T* rs, int, int idx, T (&v)[ST25_VEC]) const {
-    lds16<T, ST25_VEC>(rs + idx, v);
+  __device__ void make(const T* rs, int, int idx, RT (&v)[ST25_VEC]) const {
+    T wv[ST25_VEC];
+    lds16<T, ST25_VEC>(rs + idx, wv);
 #pragma unroll
-    for (int e = 0; e < ST25_VEC; ++e) v[e] = from_dbl<T>(__dmul_rn(inv, to_dbl(v[e])));
+    for (int e = 0; e < ST25_VEC; ++e) v[e] = ld_c<T, RT>(from_dbl<T>(__dmul_rn(inv, to_dbl(wv[e]))));
   }
-  __device__ MatvecF<C, T> fold() const { return MatvecF<C, T>(); }
+  __device__ MatvecF<C, RT> fold() const { return MatvecF<C, RT>(); }
   __device__ void init(int64_t, C (&acc)[ST25_VEC]) const {
 #pragma unroll
     for (int e = 0; e < ST25_VEC; ++e) acc[e] = Ar<C>::zero();
   }
-  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const T (&cc)[ST25_VEC], C& c, double&, double&,
+  __device__ void epi(int64_t e0, const C (&acc)[ST25_VEC], const RT (&cc)[ST25_VEC], C& c, double&, double&,
                       int&) const {
-    T wv[ST25_VEC], v0v[ST25_VEC];
-    C tc[ST25_VEC];
-    st_vec<T, ST25_VEC>(vj, e0, cc);
+    T wv[ST25_VEC], vv[ST25_VEC];
+    C v0c[ST25_VEC], tc[ST25_VEC];
+#pragma unroll
+    for (int e = 0; e < ST25_VEC; ++e) vv[e] = st_t<T, RT>(cc[e]);
+    st_vec<T, ST25_VEC>(vj, e0, vv);
     if (vj == v0) {
 #pragma unroll
-      for (int e = 0; e < ST25_VEC; ++e) v0v[e] = cc[e];
+      for (int e = 0; e < ST25_VEC; ++e) v0c[e] = ld_c<RT, C>(cc[e]);
     } else {
+      T v0v[ST25_VEC];
       ld_vec<T, ST25_VEC>(v0, e0, v0v);
+#pragma unroll
+      for (int e = 0; e < ST25_VEC; ++e) v0c[e] = ld_c<T, C>(v0v[e]);
     }
 #pragma unroll
     for (int e = 0; e < ST25_VEC; ++e) {
       wv[e] = st_t<T, C>(acc[e]);
-      tc[e] = Ar<C>::mul(ld_c<T, C>(wv[e]), ld_c<T, C>(v0v[e]));
+      tc[e] = Ar<C>::mul(ld_c<T, C>(wv[e]), v0c[e]);
     }
     st_vec<T, ST25_VEC>(w, e0, wv);
     c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
@@ -439,6 +507,7 @@ struct PolGmResid {
   using T = TS;
   using Acc = C;
   using R0 = C;
+  using RT = TS;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = true, IDENT = true;
   C c7[7];
@@ -482,6 +551,7 @@ struct PolResidA {
   using T = double;
   using Acc = double;
   using R0 = double;
+  using RT = double;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false, IDENT = true;
   double c7[7];
