@@ -245,14 +245,17 @@ __device__ __forceinline__ void fold_seg(const Op& op, const Src& x, const Seg& 
 
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
-  static constexpr bool PACKED = true, NEG = false;
+  // PACKED = false: ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2
+  // into one FFMA2 (a single rounding) despite .rn and -fmad=false, which
+  // breaks the reference's two-rounding fold; the scalar path stays exact.
+  static constexpr bool PACKED = false, NEG = false;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::add(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <class C, class T>
 struct ResidF {  // acc - coef * x (kernels.cpp:63-66)
-  static constexpr bool PACKED = true, NEG = true;
+  static constexpr bool PACKED = false, NEG = true;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::sub(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r
 // ||r||_2 in binary64 for the next stop test; overflow checks
 // (inner_solver.cpp:66-77).
 template <class T, class C, int VEC>
-__global__ void __launch_bounds__(256) k_cg_update(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+__global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
                                                    const T* __restrict__ q, int first, Geo g, Red rd,
                                                    DevState* st) {
   if (*(volatile int*)&st->cg_done) return;

@@ -370,15 +370,14 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
 // ------------------------------------------------------------ policies
 #define ST25_VEC (16 / (int)sizeof(T))
 
-// The operand ring holds binary16 operands widened to binary32 when the
-// arithmetic is binary32 (exact; saves a conversion per neighbour use).
+// Element type of the operand ring. Widening binary16 operands to binary32
+// in the ring (exact, one conversion per point instead of per use) was
+// measured slower on B200 (r01: CG SpMV 356 -> 438 us): the doubled ring
+// forces a 2-stage TMA ring to keep two CTAs per SM. The ring stays in the
+// storage type.
 template <class T, class C>
 struct RingOf {
   using type = T;
-};
-template <>
-struct RingOf<__half, float> {
-  using type = float;
 };
 
 // CG: p = r + beta p (first: p = r), q = H p, pap = dot(p, q)  (= k_cg_spmvp)
