@@ -123,7 +123,7 @@ typedef struct {
   int64_t launches;           /* device kernels launched by this call      */
 } gadi_report;
 
-typedef enum { GADI_PROBLEM_STENCIL7 = 0, GADI_PROBLEM_CSR = 1 } gadi_problem_kind;
+typedef enum { GADI_PROBLEM_STENCIL7 = 0, GADI_PROBLEM_CSR = 1, GADI_PROBLEM_BAND = 2 } gadi_problem_kind;
 
 /* Problem description. STENCIL7 is the reference's 3D convection-diffusion
  * operator (problems.cpp:8-43) applied matrix free: grid n^3, row
@@ -142,6 +142,13 @@ typedef struct {
   const int64_t* row_ptr;
   const int64_t* col_idx;
   const double* values;
+  /* BAND (BASELINE configs[3], generated on the device): n_rows rows, k_off
+   * distinct off-diagonal columns per row uniform in [i-band, i+band]\{i}
+   * (clipped to [0, n_rows)), values U[-1,1], diagonal 1.1 * sum|off|,
+   * splitmix64 stream `seed` (the oracle's orc_band_csr, bit for bit). */
+  int64_t band;
+  int32_t k_off;
+  uint64_t seed;
 } gadi_problem_desc;
 
 typedef struct {

@@ -122,7 +122,8 @@ class _Problem(C.Structure):
     _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("t1", C.c_double), ("t2", C.c_double),
                 ("t3", C.c_double), ("n_rows", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.POINTER(C.c_int64)), ("col_idx", C.POINTER(C.c_int64)),
-                ("values", C.POINTER(C.c_double))]
+                ("values", C.POINTER(C.c_double)), ("band", C.c_int64), ("k_off", C.c_int32),
+                ("seed", C.c_uint64)]
 
 
 class _DevOpts(C.Structure):
@@ -299,6 +300,25 @@ class Stencil7:
 
     def _desc(self):
         return _Problem(0, self.n, self.t1, self.t2, self.t3, 0, 0, None, None, None)
+
+
+@dataclass
+class BandRandom:
+    """BASELINE configs[3], generated on the device: n_rows rows with k_off
+    distinct off-diagonal columns uniform within +-band of the diagonal,
+    values U[-1,1], diagonal 1.1 * row abs sum (strictly diagonally dominant,
+    H positive definite); splitmix64 stream `seed` (oracle: orc_band_csr)."""
+    n_rows: int
+    k_off: int = 26
+    band: int = 4096
+    seed: int = 2
+
+    def _desc(self):
+        return _Problem(2, 0, 0.0, 0.0, 0.0, self.n_rows, 0, None, None, None, self.band, self.k_off, self.seed)
+
+
+def build_band_csr(n_rows: int, k_off: int = 26, band: int = 4096, seed: int = 2) -> BandRandom:
+    return BandRandom(n_rows, k_off, band, seed)
 
 
 def build_convdiff3d(n: int, r: Optional[float] = None, beta: Optional[float] = None) -> Stencil7:

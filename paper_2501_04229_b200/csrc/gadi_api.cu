@@ -5,6 +5,52 @@ using namespace gadi_host;
 
 namespace {
 
+// hss_split on the device (splitting.cpp:12-20; gadi_csr.cuh): A^T by column
+// counts + scan + scatter + per-row sort, then the per-row union of A, A^T and
+// the diagonal with M = (A+A^T)/2, N = (A-A^T)/2 in binary64; plus the SELL
+// image of A (binary64, 2 rows per lane) for the outer residual.
+void device_split(gadi_handle* h) {
+  cudaStream_t s = h->stream;
+  const int64_t N = h->N, nnz = h->nnzA;
+  const dim3 gN = ew_grid(N), gZ = ew_grid(nnz);
+  int* cnt = dalloc<int>(N + 1);
+  CK(cudaMemsetAsync(cnt, 0, (N + 1) * sizeof(int), s));
+  k_count_cols<<<gZ, 256, 0, s>>>(h->d_ciA, nnz, cnt);
+  int64_t* c64 = dalloc<int64_t>(N + 1);
+  k_i32_to_i64<<<ew_grid(N + 1), 256, 0, s>>>(cnt, c64, N + 1);
+  CKL();
+  int64_t* trp = dalloc<int64_t>(N + 1);
+  scan_i64(s, c64, trp, N + 1);
+  unsigned long long* next = dalloc<unsigned long long>(N);
+  CK(cudaMemcpyAsync(next, trp, N * 8, cudaMemcpyDeviceToDevice, s));
+  int32_t* tci = dalloc<int32_t>(nnz);
+  double* tv = dalloc<double>(nnz);
+  k_scatter_t<<<gN, 256, 0, s>>>(N, h->d_rpA, h->d_ciA, h->d_vA, next, tci, tv);
+  k_sort_rows<<<gN, 256, 0, s>>>(N, trp, tci, tv);
+  // union pattern: count, scan, fill
+  k_union<false><<<gN, 256, 0, s>>>(N, h->d_rpA, h->d_ciA, h->d_vA, trp, tci, tv, c64, nullptr, nullptr, nullptr,
+                                    nullptr, nullptr, nullptr);
+  CKL();
+  CK(cudaMemsetAsync(c64 + N, 0, 8, s));
+  h->d_urp = dalloc<int64_t>(N + 1);
+  scan_i64(s, c64, h->d_urp, N + 1);
+  CK(cudaMemcpy(&h->nnzHS, h->d_urp + N, 8, cudaMemcpyDeviceToHost));
+  h->d_uci = dalloc<int32_t>(h->nnzHS);
+  h->d_mv = dalloc<double>(h->nnzHS);
+  h->d_nv = dalloc<double>(h->nnzHS);
+  h->d_dpos = dalloc<int64_t>(N);
+  h->d_din = dalloc<uint8_t>(N);
+  k_union<true><<<gN, 256, 0, s>>>(N, h->d_rpA, h->d_ciA, h->d_vA, trp, tci, tv, nullptr, h->d_urp, h->d_uci,
+                                   h->d_mv, h->d_nv, h->d_dpos, h->d_din);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  for (void* p : {(void*)cnt, (void*)c64, (void*)trp, (void*)next, (void*)tci, (void*)tv}) cudaFree(p);
+  h->launches += 7;
+  // SELL image of A for the binary64 residual (2 rows per lane: 16-byte loads)
+  build_sell_layout(s, N, ilog2(64), h->d_rpA, h->d_ciA, h->sellA);
+  h->sellA.val = fill_sell_values<double, P_DOUBLE>(s, N, h->sellA, h->d_rpA, h->d_vA, nullptr, nullptr, 0.0);
+}
+
 EngineBase* make_engine(gadi_handle* h, const gadi_inner_spec& sp, double a, double om, int ur, int acc) {
   const bool st = h->stencil();
   if (ur == GADI_DOUBLE) return (st ? make_engine_st_d64 : make_engine_csr_d64)(h, sp, a, om, ur, acc);
@@ -298,22 +344,26 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
     CK(cudaMemcpy(h->d_rpA, rp, (n + 1) * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_ciA, ci32.data(), d->nnz * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_vA, d->values, d->nnz * 8, cudaMemcpyHostToDevice));
-    HostCsr P;
-    hss_split_host(n, rp, d->col_idx, d->values, P, h->Mv, h->Nv, h->diag_in);
-    h->nnzHS = P.rp[n];
-    h->diag_pos.resize(n);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k)
-        if (P.ci[k] == i) h->diag_pos[i] = k;
-    std::vector<int32_t> hci(P.ci.begin(), P.ci.end());
-    h->d_rpHS = dalloc<int64_t>(n + 1);
-    h->d_ciHS = dalloc<int32_t>(h->nnzHS);
-    CK(cudaMemcpy(h->d_rpHS, P.rp.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_ciHS, hci.data(), h->nnzHS * 4, cudaMemcpyHostToDevice));
+  } else if (d->kind == GADI_PROBLEM_BAND) {
+    // BASELINE configs[3] generated on the device (bit for bit orc_band_csr)
+    const int64_t n = d->n_rows;
+    if (n < 2 || d->k_off < 1 || d->k_off > 31 || d->band < d->k_off || n - 1 < d->k_off)
+      throw Err(GADI_E_CONTRACT, "band: need 1 <= k_off <= 31, band >= k_off, n_rows > k_off");
+    if (n >= (int64_t(1) << 31)) throw Err(GADI_E_UNSUPPORTED, "band: n_rows must be < 2^31");
+    h->N = n;
+    h->nnzA = n * (int64_t)(d->k_off + 1);
+    h->d_rpA = dalloc<int64_t>(n + 1);
+    h->d_ciA = dalloc<int32_t>(h->nnzA);
+    h->d_vA = dalloc<double>(h->nnzA);
+    k_iota_scaled<<<ew_grid(n + 1), 256>>>(h->d_rpA, n + 1, d->k_off + 1);
+    k_band_gen<<<ew_grid(n), 256>>>(n, d->k_off, d->band, d->seed, h->d_ciA, h->d_vA);
+    CKL();
+    CK(cudaDeviceSynchronize());
   } else {
     throw Err(GADI_E_CONTRACT, "unknown problem kind");
   }
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  if (!h->stencil()) device_split(h.get());
   const int64_t N = h->N;
   h->d_x = dalloc<double>(N);
   h->d_b = dalloc<double>(N);
@@ -345,10 +395,12 @@ int gadi_cuda_destroy(gadi_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->eng.reset();
-  for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_rpHS, (void*)h->d_ciHS,
-                  (void*)h->d_x, (void*)h->d_b, (void*)h->d_s, (void*)h->d_t64, (void*)h->st,
-                  (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_ticket})
+  for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_urp, (void*)h->d_uci,
+                  (void*)h->d_mv, (void*)h->d_nv, (void*)h->d_dpos, (void*)h->d_din, (void*)h->d_x,
+                  (void*)h->d_b, (void*)h->d_s, (void*)h->d_t64, (void*)h->st, (void*)h->d_part0,
+                  (void*)h->d_part1, (void*)h->d_ticket})
     if (p) cudaFree(p);
+  h->sellA.release();
   if (h->h_st) cudaFreeHost(h->h_st);
   if (h->h_done) cudaFreeHost(h->h_done);
   for (cudaEvent_t ev : {h->ev0, h->ev1, h->evA, h->evB, h->evC})

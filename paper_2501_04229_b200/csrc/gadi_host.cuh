@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cub/device/device_scan.cuh>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -23,6 +24,7 @@
 #include "../../include/gadi_cuda.h"
 #include "gadi_kernels.cuh"
 #include "gadi_st25.cuh"
+#include "gadi_csr.cuh"
 
 using namespace gadi;
 
@@ -231,22 +233,43 @@ inline void hss_split_host(int64_t n, const int64_t* rp, const int64_t* ci, cons
 // ==================================================================== handle
 struct EngineBase;
 
+// A SELL image (gadi_csr.cuh) owned on the device.
+struct SellImage {
+  int lgSR = 0;
+  int64_t entries = 0;
+  int64_t* soff = nullptr;
+  uint16_t* len = nullptr;
+  int32_t* col = nullptr;
+  void* val = nullptr;
+  void release() {
+    for (void* p : {(void*)soff, (void*)len, (void*)col, val})
+      if (p) cudaFree(p);
+    soff = nullptr;
+    len = nullptr;
+    col = nullptr;
+    val = nullptr;
+  }
+};
+
 struct gadi_handle {
   int device = 0;
   cudaStream_t stream = nullptr;
   int kind = GADI_PROBLEM_STENCIL7;
   int64_t N = 0, n = 0;
   double t1 = 0, t2 = 0, t3 = 0;
-  // CSR A (device) and the HSS pattern (device) + fp64 M/N values (host)
+  // sparse A (CSR, device) and its SELL image for the binary64 residual
   int64_t* d_rpA = nullptr;
   int32_t* d_ciA = nullptr;
   double* d_vA = nullptr;
   int64_t nnzA = 0, nnzHS = 0;
-  int64_t* d_rpHS = nullptr;
-  int32_t* d_ciHS = nullptr;
-  std::vector<double> Mv, Nv;
-  std::vector<int64_t> diag_pos;  // position of (i,i) in the HS pattern
-  std::vector<uint8_t> diag_in;
+  SellImage sellA;
+  // the HSS split on the union pattern (device): M, N in binary64, the
+  // position of each diagonal entry and whether M's own pattern had it
+  int64_t* d_urp = nullptr;
+  int32_t* d_uci = nullptr;
+  double *d_mv = nullptr, *d_nv = nullptr;
+  int64_t* d_dpos = nullptr;
+  uint8_t* d_din = nullptr;
   // outer vectors (binary64)
   double *d_x = nullptr, *d_b = nullptr, *d_s = nullptr, *d_t64 = nullptr;
   // reductions / state
@@ -266,6 +289,61 @@ struct gadi_handle {
 
   bool stencil() const { return kind == GADI_PROBLEM_STENCIL7; }
 };
+
+namespace gadi_host {
+
+template <class T>
+T* dalloc(int64_t n);
+
+// exclusive prefix sum of n int64 values (in -> out, out[n] = total when in[n] = 0)
+inline void scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n) {
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, s));
+  void* t = nullptr;
+  CK(cudaMalloc(&t, tmp));
+  CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, n, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(t);
+}
+
+// SELL layout (slice offsets, row lengths, column image) of a device CSR
+// pattern with 2^lgSR rows per slice (gadi_csr.cuh).
+inline void build_sell_layout(cudaStream_t s, int64_t N, int lgSR, const int64_t* rp, const int32_t* ci,
+                              SellImage& L) {
+  const int64_t SR = int64_t(1) << lgSR, ns = (N + SR - 1) / SR;
+  L.lgSR = lgSR;
+  int64_t* wid = dalloc<int64_t>(ns + 1);
+  CK(cudaMemsetAsync(wid, 0, (ns + 1) * 8, s));
+  L.len = dalloc<uint16_t>(N);
+  k_sell_width<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(N, lgSR, rp, wid, L.len);
+  CKL();
+  L.soff = dalloc<int64_t>(ns + 1);
+  scan_i64(s, wid, L.soff, ns + 1);
+  cudaFree(wid);
+  CK(cudaMemcpy(&L.entries, L.soff + ns, 8, cudaMemcpyDeviceToHost));
+  L.col = dalloc<int32_t>(L.entries);
+  CK(cudaMemsetAsync(L.col, 0, L.entries * 4, s));
+  k_sell_fill<double, P_DOUBLE><<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
+      N, lgSR, rp, ci, nullptr, L.soff, L.col, (double*)nullptr, nullptr, nullptr, 0.0);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+}
+
+// values of a device CSR (binary64) into a SELL layout as VO, rounded to
+// precision PR, the diagonal shifted by alpha when dpos is given.
+template <class VO, int PR>
+inline VO* fill_sell_values(cudaStream_t s, int64_t N, const SellImage& L, const int64_t* rp, const double* val,
+                            const int64_t* dpos, const uint8_t* din, double alpha) {
+  VO* out = dalloc<VO>(L.entries);
+  CK(cudaMemsetAsync(out, 0, L.entries * sizeof(VO), s));
+  k_sell_fill<VO, PR><<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, L.lgSR, rp, nullptr, val, L.soff, nullptr,
+                                                                  out, dpos, din, alpha);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  return out;
+}
+
+}  // namespace gadi_host
 
 namespace gadi_host {
 
@@ -318,7 +396,8 @@ struct OuterA {
       Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
       go(op);
     } else {
-      Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
+      Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
+                      static_cast<const double*>(h->sellA.val)};
       go(op);
     }
     CKL();
@@ -333,7 +412,8 @@ struct OuterA {
       Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
       go(op);
     } else {
-      Csr<double> op{h->N, h->d_rpA, h->d_ciA, h->d_vA};
+      Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
+                      static_cast<const double*>(h->sellA.val)};
       go(op);
     }
     CKL();
@@ -378,10 +458,12 @@ struct Engine final : EngineBase {
   bool aligned;
   Geo geo;
   static constexpr int VA = 16 / sizeof(T);
+  static constexpr bool SPARSE = !std::is_same<Op, Stencil7<C>>::value;
   // CG / GMRES work vectors
   T *pA = nullptr, *pB = nullptr, *q = nullptr, *wA = nullptr, *wB = nullptr, *gr = nullptr, *V = nullptr;
-  C* dH = nullptr;  // CSR values (device)
+  C* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
   C* dS = nullptr;
+  SellImage sHS;
   int m_restart = 30;
   std::vector<T*> owned;
   bool st25 = false;  // 2.5D TMA stencil kernels (gadi_st25.cuh) for the operator passes
@@ -431,6 +513,7 @@ struct Engine final : EngineBase {
     for (T* v : owned) cudaFree(v);
     if (dH) cudaFree(dH);
     if (dS) cudaFree(dS);
+    sHS.release();
   }
 
   static C cval(double v, int ur) {
@@ -459,23 +542,20 @@ struct Engine final : EngineBase {
         opS.c[k] = cval(Sc[k], u_r);
       }
     } else {
-      const int64_t nnz = h->nnzHS;
-      std::vector<C> hv(nnz), sv(nnz);
-      for (int64_t k = 0; k < nnz; ++k) {
-        hv[k] = cval(h->Mv[k], u_r);
-        sv[k] = cval(h->Nv[k], u_r);
-      }
-      for (int64_t i = 0; i < h->N; ++i) {
-        const int64_t k = h->diag_pos[i];
-        hv[k] = cval(h->diag_in[i] ? 1.0 * h->Mv[k] + alpha : alpha, u_r);
-        sv[k] = cval(h->diag_in[i] ? 1.0 * h->Nv[k] + alpha : alpha, u_r);
-      }
-      dH = dalloc<C>(nnz);
-      dS = dalloc<C>(nnz);
-      CK(cudaMemcpy(dH, hv.data(), nnz * sizeof(C), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(dS, sv.data(), nnz * sizeof(C), cudaMemcpyHostToDevice));
-      opH = Op{h->N, h->d_rpHS, h->d_ciHS, dH};
-      opS = Op{h->N, h->d_rpHS, h->d_ciHS, dS};
+      // SELL image of the union pattern with VA rows per lane, values of
+      // H / S rounded to u_r (rounded_copy, inner_solver.cpp:41-45) on the device
+      build_sell_layout(h->stream, h->N, ilog2(32 * VA), h->d_urp, h->d_uci, sHS);
+      auto fill = [&](const double* src) -> C* {
+        if (u_r == GADI_HALF)
+          return fill_sell_values<C, P_HALF>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+        if (u_r == GADI_SINGLE)
+          return fill_sell_values<C, P_SINGLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+        return fill_sell_values<C, P_DOUBLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+      };
+      dH = fill(h->d_mv);
+      dS = fill(h->d_nv);
+      opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH};
+      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS};
     }
   }
 
@@ -555,8 +635,13 @@ struct Engine final : EngineBase {
       const int first = it == 0;
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        if (!spmvp25(o, r, p_in, p_out, first))
+        if constexpr (SPARSE) {  // p-update as its own pass: a gathered operand is not re-formed per nonzero
+          k_cg_pupd<T, C, V_><<<geo.nblk, nt, 0, s>>>(r, p_in, p_out, first, geo, h->st);
+          k_cg_spmvp<Op, T, C, V_, false><<<geo.nblk, nt, 0, s>>>(o, r, p_out, p_out, q, first, geo, rd, h->st);
+          ++h->launches;
+        } else if (!spmvp25(o, r, p_in, p_out, first)) {
           k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
+        }
         k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st);
       });
       CKL();
@@ -628,8 +713,13 @@ struct Engine final : EngineBase {
         T* w = (j & 1) ? wB : wA;
         V2([&](auto vt) {
           constexpr int V_ = decltype(vt)::v;
-          if (!gmmatvec25(o, wprev, inv, vj, w))
+          if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
+            k_scale<T, V_><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
+            k_gm_matvec<Op, T, C, V_, false><<<geo.nblk, nt, 0, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st);
+            ++h->launches;
+          } else if (!gmmatvec25(o, wprev, inv, vj, w)) {
             k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
+          }
           for (int i = 0; i <= j; ++i) {
             T* vi = V + (int64_t)i * N;
             if (i < j) {

@@ -319,16 +319,17 @@ __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int ma
 // p_out = r + beta p_in (or r on the first iteration; inner_solver.cpp:53,76),
 // q = H p_out, pap = dot(p_out, q); then alpha = rs / pap or `break`
 // (inner_solver.cpp:62-65).
-template <class Op, class T, class C, int VEC>
+// FUSE = false (sparse operators, where a gathered operand would be re-formed
+// per nonzero): p_in already holds the updated p (k_cg_pupd) and is only read.
+template <class Op, class T, class C, int VEC, bool FUSE = true>
 __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r, const T* __restrict__ p_in,
                                                   T* __restrict__ p_out, T* __restrict__ q, int first, Geo g,
                                                   Red rd, DevState* st) {
   if (*(volatile int*)&st->cg_done) return;
   GADI_G;
-  const PUpdSrc<T, C> src{r, p_in, from_dbl<C>(st->cg_beta), first};
   C w0;
   double w1;
-  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+  auto body = [&](const Seg& s, C& c, const auto& src) {
     C acc[G];
     T pv[G], qv[G];
 #pragma unroll
@@ -341,9 +342,16 @@ __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r
       tc[i] = Ar<C>::mul(ld_c<T, C>(pv[i]), ld_c<T, C>(qv[i]));
     }
     store_seg<T, VEC, G>(q, s, qv);
-    store_seg<T, VEC, G>(p_out, s, pv);
+    if (FUSE) store_seg<T, VEC, G>(p_out, s, pv);
     c = seg_sum<C, G>(tc, s.len);
-  }, w0, w1);
+  };
+  if constexpr (FUSE) {
+    const PUpdSrc<T, C> src{r, p_in, from_dbl<C>(st->cg_beta), first};
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  } else {
+    const PlainSrc<T> src{p_in};
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  }
   C pap;
   double dummy;
   if (grid_finish(w0, w1, g, rd, pap, dummy)) {
@@ -356,6 +364,26 @@ __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r
       st->cg_a = to_dbl(div_c<C>(from_dbl<C>(st->cg_rs), pap));
     }
   }
+}
+
+// p_out = r + beta p_in, or r on the first iteration (inner_solver.cpp:53,76);
+// the separate pass used with sparse operators.
+template <class T, class C, int VEC>
+__global__ void __launch_bounds__(256) k_cg_pupd(const T* __restrict__ r, const T* __restrict__ p_in,
+                                                 T* __restrict__ p_out, int first, Geo g, DevState* st) {
+  if (*(volatile int*)&st->cg_done) return;
+  GADI_G;
+  const PUpdSrc<T, C> src{r, p_in, from_dbl<C>(st->cg_beta), first};
+  seg_each<VEC>(g, [&](const Seg& s) {
+    T v[G];
+    if constexpr (VEC > 1) {
+      src.template vec<VEC>(s.lo, v);
+    } else {
+#pragma unroll
+      for (int i = 0; i < G; ++i) v[i] = i < s.len ? src.at(s.lo + i) : from_dbl<T>(0.0);
+    }
+    store_seg<T, VEC, G>(p_out, s, v);
+  });
 }
 
 // x += a p (x = 0 + a p on the first iteration); r -= a q; rs' = dot(r, r);

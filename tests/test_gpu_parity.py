@@ -175,3 +175,28 @@ def test_golden_solve(gold, tag):
             res.report.inner_stagnations] == list(info)
     assert same(res.x, gold[f"solve_{tag}_x"])
     np.testing.assert_allclose(res.report.rel_residual_history, gold[f"solve_{tag}_hist"], rtol=HIST_RTOL, atol=0)
+
+
+# ---- BASELINE configs[3] family: device generator, device HSS split, SELL kernels ----
+@pytest.mark.parametrize("N,k,band", [(4096, 26, 256), (1000, 8, 40)])
+def test_band_generator_split_and_solve(orc, N, k, band):
+    A = orc.band(N, k, band, 2)
+    Bg = g.build_band_csr(N, k, band, 2)
+    s = g.CudaGadiSystem(Bg)
+    x = np.random.default_rng(N).uniform(-1, 1, N)
+    assert same(s.apply("A", x), orc.matvec(A, x, DOUBLE))  # generator + SELL(A), bit for bit
+    H, S = orc.regularize(A, 0.7)
+    s.prepare(0.7, 1.0, g.Precision.Single, g.InnerSolverSpec(g.InnerMethod.Cg, 1e-6, 10, 30))
+    xs = orc.round(x, SINGLE)
+    for name, M in (("H", H), ("S", S)):  # device split + SELL(H, S)
+        Mr = type(M)(M.n, M.rp, M.ci, orc.round(M.v, SINGLE))
+        assert same(s.apply(name, xs), orc.matvec(Mr, xs, SINGLE)), name
+    s.close()
+    _, b = orc.make_rhs(A, 1, -1.0, 1.0)
+    cfg = Config.make(alpha=2.0, xi=1e-20, u_r=SINGLE, method=CG, tol_epsilon=1e-12, max_inner_iters=20)
+    wx, wrep, _ = orc.solve(A, b, cfg)
+    res = g.gadi_ir_solve(Bg, b, g.hss_split(Bg), g.GadiConfig(
+        alpha=2.0, xi=1e-20, u_r=g.Precision.Single, inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 20, 30)))
+    assert int(res.report.status) == wrep.status == 0
+    assert res.report.outer_iters == wrep.outer_iters
+    assert same(res.x, wx)
