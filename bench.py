@@ -39,10 +39,15 @@ WORKLOADS = {
                seed=1, lo=-1.0, hi=1.0, s_r=2, name="convdiff3d n=512 beta=100 fp16-storage/fp32-accum inner"),
     "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.05, eps=1e-12, max_inner=20, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=4, name="convdiff3d n=256 beta=10 fp32 inner"),
+    # BASELINE configs[3]: general nonsymmetric CSR, N = 2^24, 26 off-diagonals per row
+    # uniform within +-4096 (seed 2), diagonal 1.1 x row abs sum; generated + split on the device
+    "c4": dict(kind="band", N=1 << 24, k_off=26, band=4096, mseed=2, u_r=0, accum=1, alpha=4.0, eps=1e-12,
+               max_inner=5, restart=30, seed=1, lo=-1.0, hi=1.0, s_r=2,
+               name="band CSR N=2^24 27 nnz/row +-4096 fp16-storage/fp32-accum inner"),
 }
 # outer iterations the device solve needs for each workload (measured on B200,
 # profiles/); used only to project the CPU reference's time-to-solution
-OUTER_ITERS = {"c3": 796, "c2": 366}
+OUTER_ITERS = {"c3": 796, "c2": 366, "c4": 39}
 
 
 def load_peaks():
@@ -112,9 +117,15 @@ def cpu_reference_sample(wl, threads_note=True):
     o = Oracle()
     use_ref = Reference.available()
     R = Reference() if use_ref else o
-    ns = 64
-    r = wl["beta"] / (2.0 * (wl["n"] + 1.0))
-    A = o.convdiff(ns, 6.0, -1.0 - r, -1.0 + r)
+    if wl.get("kind") == "band":  # the same generator at N = 2^16 (C4 cannot be split in host RAM)
+        ns, N_s, N_t = None, 1 << 16, wl["N"]
+        A = o.band(N_s, wl["k_off"], wl["band"], wl["mseed"])
+        r = 0.0
+    else:
+        ns = 64
+        N_s, N_t = ns ** 3, wl["n"] ** 3
+        r = wl["beta"] / (2.0 * (wl["n"] + 1.0))
+        A = o.convdiff(ns, 6.0, -1.0 - r, -1.0 + r)
     _, b = o.make_rhs(A, wl["seed"], wl["lo"], wl["hi"])
     # the reference's FP16 Krylov accumulates dots in binary16 and breaks on
     # overflow at these sizes (SURVEY §0 finding 1); time its FP32 path
@@ -124,16 +135,98 @@ def cpu_reference_sample(wl, threads_note=True):
     t = time.perf_counter()
     R.solve(A, b, cfg)
     dt = time.perf_counter() - t
-    N_s, N_t = ns ** 3, wl["n"] ** 3
     per_outer_t = dt * N_t / N_s
     proj = per_outer_t * OUTER_ITERS[wl_key(wl)]
+    what = (f"band CSR N={N_s}" if ns is None else f"n={ns} (N={N_s}) with r={r:.5f}")
     return {
         "value": proj, "unit": "s", "cores": 1, "kind": "reference" if use_ref else "port",
-        "sample": (f"1 GADI-IR outer step (fp32 CG/GMRES, max_inner={wl['max_inner']}) at n={ns} "
-                   f"(N={N_s}) with r={r:.5f}: {dt:.2f} s; projected x{N_t // N_s} elements and "
+        "sample": (f"1 GADI-IR outer step incl. setup (fp32 CG/GMRES, max_inner={wl['max_inner']}) on "
+                   f"{what}: {dt:.2f} s; projected x{N_t // N_s} elements and "
                    f"x{OUTER_ITERS[wl_key(wl)]} outer steps (projected, single-threaded: the "
                    f"reference has no intra-solve parallelism)"),
     }
+
+
+def c5_data():
+    """BASELINE configs[4]: m = 4096 pairs, log10 N ~ U[4,8], alpha = 0.5 N^(-1/3)
+    (1 + 0.05 N(0,1)) (seed 3); 65,536 query sizes log10 N ~ U[4,8]. Sizes are
+    rounded to integers (the reference's index_t sizes) and made unique."""
+    import numpy as np
+    rng = np.random.default_rng(3)
+    sizes = np.unique(np.round(10.0 ** rng.uniform(4, 8, 4096 + 64)))[:4096]
+    alphas = 0.5 * sizes ** (-1.0 / 3.0) * (1.0 + 0.05 * rng.standard_normal(len(sizes)))
+    q = np.round(10.0 ** rng.uniform(4, 8, 65536))
+    var = max(float(np.mean((alphas - alphas.mean()) ** 2)), 1e-8)
+    return sizes, alphas, q, (var, 1.0, 1e-4)  # sigma_f2 = var(y) (the grid's middle), l = 1, sn2 = 1e-4
+
+
+def run_c5(args, rank, world):
+    """GPR alpha predictor (BASELINE configs[4]): one step = fit (fixed hypers,
+    m x m Gram + Cholesky) + predict 65,536 queries (mean + std)."""
+    import numpy as np
+    sizes, alphas, q, fixed = c5_data()
+    metric = "GPR fit+predict time (m=4096, q=65536)"
+    cfg = {"workload": "GPR alpha predictor m=4096 q=65536", "m": len(sizes), "q": len(q),
+           "sigma_f2": fixed[0], "length": fixed[1], "sigma_n2": fixed[2]}
+    if args.impl == "reference":
+        if rank == 0:
+            cb = c5_cpu_sample(sizes, alphas, q, fixed)
+            print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "s",
+                              "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                              "higher_is_better": False, "dtype": "f64", "data": "synthetic", "config": cfg,
+                              "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "s",
+                                                          "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    import paper_2501_04229_b200 as g
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+
+    def step():
+        m = g.gpr_fit(sizes, alphas, fixed=fixed)
+        out = m.predict(q)
+        m.close()
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        mean, sd = step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t) / args.steps
+    out = {"metric": metric, "value": dt, "unit": "s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+           "e2e": {"value": dt, "unit": "s", "h2d_bytes_per_step": 8 * (2 * len(sizes) + len(q)),
+                   "d2h_bytes_per_step": 16 * len(q)},
+           "note": "host-timed end to end (inputs/outputs are host arrays); Cholesky via cuSOLVER Dpotrf, "
+                   "variances via cuBLAS Dtrsm: library fp64 path, no tensor cores yet",
+           "flops": {"cholesky": len(sizes) ** 3 / 3, "trsm": len(sizes) ** 2 * len(q)},
+           "prediction_sample": {"mean_min": float(mean.min()), "mean_max": float(mean.max()),
+                                 "sd_max": float(sd.max())}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = c5_cpu_sample(sizes, alphas, q, fixed)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def c5_cpu_sample(sizes, alphas, q, fixed):
+    """The oracle restatement of fit/predict (gpr.cpp:72-169; the reference's
+    gpr.cpp needs Eigen, absent here) on one host core: the full fit plus 256
+    of the 65,536 queries, projected linearly in the query count."""
+    from oracle import Oracle
+    o = Oracle()
+    t = time.perf_counter()
+    o.gpr(sizes, alphas, q[:1], fixed=fixed)
+    t_fit = time.perf_counter() - t
+    t = time.perf_counter()
+    o.gpr(sizes, alphas, q[:257], fixed=fixed)
+    t_q = (time.perf_counter() - t - t_fit) / 256
+    proj = t_fit + t_q * len(q)
+    return {"value": proj, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"fit m={len(sizes)} ({t_fit:.1f} s) + 256 queries ({t_q * 1e3:.1f} ms each), "
+                      f"projected to {len(q)} queries"}
 
 
 def wl_key(wl):
@@ -149,18 +242,26 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=list(WORKLOADS))
+    ap.add_argument("--workload", default="c3", choices=list(WORKLOADS) + ["c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "c5":
+        return run_c5(args, rank, world)
+    wl = WORKLOADS[args.workload]
     metric = "GADI-IR time-to-1e-10 residual"
-    cfg_json = {"workload": wl["name"], "n": wl["n"], "N": wl["n"] ** 3, "beta": wl["beta"],
-                "alpha": wl["alpha"], "omega": 1.0, "inner": "cg(H)/gmres(S)", "max_inner": wl["max_inner"],
-                "tol_epsilon": wl["eps"], "xi": 1e-20, "l2": "inputs larger than L2 (x, b: 8N bytes each)",
+    band = wl.get("kind") == "band"
+    Nw = wl["N"] if band else wl["n"] ** 3
+    cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": 1.0, "inner": "cg(H)/gmres(S)",
+                "max_inner": wl["max_inner"], "tol_epsilon": wl["eps"], "xi": 1e-20,
+                "l2": "inputs larger than L2 (x, b: 8N bytes each)",
                 "parallelism": f"replicas{world}" if world > 1 else "single"}
+    if band:
+        cfg_json.update(k_off=wl["k_off"], band=wl["band"], matrix_seed=wl["mseed"])
+    else:
+        cfg_json.update(n=wl["n"], beta=wl["beta"])
 
     if args.impl == "reference":
         if rank != 0:
@@ -182,7 +283,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
+    if band:
+        S = g.build_band_csr(wl["N"], wl["k_off"], wl["band"], wl["mseed"])
+    else:
+        S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
     sysx = g.CudaGadiSystem(S, device=local)
     N = S.n_rows
     xt = torch.empty(N, dtype=torch.float64, device="cuda")
@@ -227,8 +331,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         solve_s, e2e_s = t.tolist()
     peak, peak_kind = load_peaks()
-    # inner CG sweep: B_CG = 11 N s_r bytes per iteration
+    # inner CG sweep: B_CG = 11 N s_r bytes per iteration; a
+    # sparse H adds nnz(H) (s_r value + 4 index) + 4 (N+1) row bytes per SpMV
     bytes_it = 11 * N * wl["s_r"]
+    if band:
+        bytes_it += sysx.nnz()[1] * (wl["s_r"] + 4) + 4 * (N + 1)
     cg_gbs = bytes_it * h_it / (h_ms / 1e3) / 1e9 if h_ms > 0 else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
@@ -242,7 +349,8 @@ def main():
         + " inner", "data": "synthetic (seeded splitmix64 x_true, b = A x_true)", "config": cfg_json,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(reps[0].h2d_bytes),
                 "d2h_bytes_per_step": int(reps[0].d2h_bytes)},
-        "roofline": {"bound": "hbm", "kernel": "inner CG iteration (spmv+p-update, axpys+dots)",
+        "roofline": {"bound": "hbm", "kernel": ("inner CG iteration (p-update, SELL spmv + p.q, axpys + dots)"
+                                                if band else "inner CG iteration (spmv+p-update, axpys+dots)"),
                      "achieved": cg_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic,
                      "algorithmic_bytes_per_iter": bytes_it},

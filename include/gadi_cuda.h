@@ -210,6 +210,8 @@ int gadi_cuda_history(const gadi_handle* h, double* out, int32_t cap);
 
 /* Device kernels this handle has launched so far (bench / driver evidence). */
 int64_t gadi_cuda_launch_count(const gadi_handle* h);
+/* Stored entries of A and of the H/S union pattern (0 for matrix-free stencils). */
+int gadi_cuda_nnz(const gadi_handle* h, int64_t* nnz_a, int64_t* nnz_hs);
 
 /* ---- operator-level kernels (parity tests; each is one device pass) ---- */
 

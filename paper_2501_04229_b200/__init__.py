@@ -182,6 +182,7 @@ def lib():
     L.gadi_gpr_destroy.argtypes = [C.c_void_p]
     L.gadi_cuda_launch_count.argtypes = [C.c_void_p]
     L.gadi_cuda_launch_count.restype = C.c_int64
+    L.gadi_cuda_nnz.argtypes = [C.c_void_p, _i64p, _i64p]
     _lib = L
     return L
 
@@ -374,6 +375,12 @@ class CudaGadiSystem:
 
     def dim(self):
         return self.n
+
+    def nnz(self):
+        """(stored entries of A, of the H/S union pattern); (0, 0) for stencils."""
+        a, hs = C.c_int64(), C.c_int64()
+        _check(lib().gadi_cuda_nnz(self._h, C.byref(a), C.byref(hs)))
+        return a.value, hs.value
 
     def set_rhs(self, b):
         self._b = _f64(b)

@@ -3,6 +3,10 @@
 
 using namespace gadi_host;
 
+namespace gadi_host {
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace gadi_host
+
 namespace {
 
 // hss_split on the device (splitting.cpp:12-20; gadi_csr.cuh): A^T by column
@@ -576,6 +580,13 @@ int gadi_cuda_apply(gadi_handle* h, int32_t which, const double* x, double* y) {
 }
 
 int64_t gadi_cuda_launch_count(const gadi_handle* h) { return h ? h->launches : 0; }
+
+int gadi_cuda_nnz(const gadi_handle* h, int64_t* nnz_a, int64_t* nnz_hs) {
+  if (!h || !nnz_a || !nnz_hs) return GADI_E_CONTRACT;
+  *nnz_a = h->nnzA;
+  *nnz_hs = h->nnzHS;
+  return GADI_OK;
+}
 
 static int reduce_test(int32_t device, int32_t p, const double* x, const double* y, int64_t n, double* out,
                        bool norm) {
