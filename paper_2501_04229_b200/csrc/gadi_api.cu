@@ -51,7 +51,7 @@ void device_split(gadi_handle* h) {
   for (void* p : {(void*)cnt, (void*)c64, (void*)trp, (void*)next, (void*)tci, (void*)tv}) cudaFree(p);
   h->launches += 7;
   // SELL image of A for the binary64 residual (2 rows per lane: 16-byte loads)
-  build_sell_layout(s, N, ilog2(64), h->d_rpA, h->d_ciA, h->sellA);
+  build_sell_layout(s, N, ilog2(64), h->d_rpA, h->d_ciA, h->sellA, h->max_band < 32768);
   h->sellA.val = fill_sell_values<double, P_DOUBLE>(s, N, h->sellA, h->d_rpA, h->d_vA, nullptr, nullptr, 0.0);
 }
 
@@ -339,6 +339,10 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
           throw Err(GADI_E_CONTRACT, "column indices must be strictly increasing within a row");
       }
     }
+    h->max_band = 0;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+        h->max_band = std::max<int64_t>(h->max_band, std::llabs(d->col_idx[k] - i));
     h->N = n;
     h->nnzA = d->nnz;
     std::vector<int32_t> ci32(d->col_idx, d->col_idx + d->nnz);
@@ -355,6 +359,7 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
       throw Err(GADI_E_CONTRACT, "band: need 1 <= k_off <= 31, band >= k_off, n_rows > k_off");
     if (n >= (int64_t(1) << 31)) throw Err(GADI_E_UNSUPPORTED, "band: n_rows must be < 2^31");
     h->N = n;
+    h->max_band = d->band;
     h->nnzA = n * (int64_t)(d->k_off + 1);
     h->d_rpA = dalloc<int64_t>(n + 1);
     h->d_ciA = dalloc<int32_t>(h->nnzA);

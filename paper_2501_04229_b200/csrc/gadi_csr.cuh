@@ -27,8 +27,9 @@ struct Sell {
   int lgSR;                              // log2(rows per slice)
   const int64_t* __restrict__ soff;      // slice start offsets (entries)
   const uint16_t* __restrict__ len;      // row lengths
-  const int32_t* __restrict__ col;
+  const int32_t* __restrict__ col;       // absolute columns, or null and
   const V* __restrict__ val;
+  const int16_t* __restrict__ off;       // column - row (narrow band: 2 bytes per entry)
 
   template <int VEC, class Src, class X, class Acc, class F>
   __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {
@@ -40,6 +41,20 @@ struct Sell {
     int ln[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) ln[v] = len[e0 + v];
+    if (off) {
+#pragma unroll 2
+      for (int k = 0; k < width; ++k) {
+        const int64_t pos = base + (int64_t)k * SR;
+        int16_t ov[VEC];
+        V vv[VEC];
+        ld_vec<int16_t, VEC>(off, pos, ov);
+        ld_vec<V, VEC>(val, pos, vv);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (k < ln[v]) acc[v] = f(acc[v], vv[v], x.at(e0 + v + ov[v]));
+      }
+      return;
+    }
     for (int k = 0; k < width; ++k) {
       const int64_t pos = base + (int64_t)k * SR;
       int32_t cv[VEC];
@@ -230,8 +245,8 @@ static __global__ void k_sell_width(int64_t N, int lgSR, const int64_t* __restri
 template <class VO, int PR>
 __global__ void k_sell_fill(int64_t N, int lgSR, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ val, const int64_t* __restrict__ soff,
-                            int32_t* __restrict__ cout, VO* __restrict__ vout, const int64_t* __restrict__ dpos,
-                            const uint8_t* __restrict__ din, double alpha) {
+                            int32_t* __restrict__ cout, int16_t* __restrict__ oout, VO* __restrict__ vout,
+                            const int64_t* __restrict__ dpos, const uint8_t* __restrict__ din, double alpha) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= N) return;
   const int64_t SR = int64_t(1) << lgSR;
@@ -240,6 +255,7 @@ __global__ void k_sell_fill(int64_t N, int lgSR, const int64_t* __restrict__ rp,
   for (int64_t k = b; k < e; ++k) {
     const int64_t pos = base + (k - b) * SR;
     if (cout) cout[pos] = ci[k];
+    if (oout) oout[pos] = (int16_t)(ci[k] - r);
     if (vout) {
       double x = val[k];
       if (dpos && k == dpos[r]) x = din[r] ? __dadd_rn(__dmul_rn(1.0, x), alpha) : alpha;

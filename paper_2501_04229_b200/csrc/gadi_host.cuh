@@ -15,6 +15,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -104,6 +105,7 @@ inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
 inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_chunks = 512,
                       bool ident = false, int ring_tsize = 0) {
   if (ring_tsize == 0) ring_tsize = tsize;
+  if (const char* e = std::getenv("GADI_ST25_CHUNKS")) target_chunks = std::max(32, std::atoi(e));  // tuning knob
   const int vec = 16 / tsize;
   if (!is_pow2(n) || n % vec != 0 || n < 8) return false;
   const int64_t TR = n / vec;
@@ -129,14 +131,15 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   g.nblk = (int)(g.njt * (n / IL));
   // operand-ring kernels: 3 raw stages + a 3-plane ring; identity-operand
   // kernels fold from the stages directly and need 4 of them
-  g.stages = ident ? 4 : 3;
+  g.stages = ident ? 4 : 4;
+  if (const char* e = std::getenv("GADI_ST25_STAGES")) g.stages = std::max(2, std::atoi(e));  // tuning knob
   const int64_t pe = (TJ + 2) * n;
   auto bytes = [&]() {
     return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)3 * pe * ring_tsize);
   };
   g.smem = bytes();
-  if (!ident && g.smem > 110 * 1024) {  // keep two CTAs per SM
-    g.stages = 2;
+  while (g.stages > 2 && g.smem > 112 * 1024) {  // keep two CTAs per SM
+    --g.stages;
     g.smem = bytes();
   }
   if (g.smem > 200 * 1024) return false;
@@ -239,14 +242,16 @@ struct SellImage {
   int64_t entries = 0;
   int64_t* soff = nullptr;
   uint16_t* len = nullptr;
-  int32_t* col = nullptr;
+  int32_t* col = nullptr;  // absolute columns, or
+  int16_t* off = nullptr;  // column - row when every |column - row| < 2^15 (4 B/nnz instead of 6 in fp16)
   void* val = nullptr;
   void release() {
-    for (void* p : {(void*)soff, (void*)len, (void*)col, val})
+    for (void* p : {(void*)soff, (void*)len, (void*)col, (void*)off, val})
       if (p) cudaFree(p);
     soff = nullptr;
     len = nullptr;
     col = nullptr;
+    off = nullptr;
     val = nullptr;
   }
 };
@@ -262,6 +267,7 @@ struct gadi_handle {
   int32_t* d_ciA = nullptr;
   double* d_vA = nullptr;
   int64_t nnzA = 0, nnzHS = 0;
+  int64_t max_band = INT64_MAX;  // max |column - row| of A (the HSS union has the same band)
   SellImage sellA;
   // the HSS split on the union pattern (device): M, N in binary64, the
   // position of each diagonal entry and whether M's own pattern had it
@@ -309,7 +315,7 @@ inline void scan_i64(cudaStream_t s, const int64_t* in, int64_t* out, int64_t n)
 // SELL layout (slice offsets, row lengths, column image) of a device CSR
 // pattern with 2^lgSR rows per slice (gadi_csr.cuh).
 inline void build_sell_layout(cudaStream_t s, int64_t N, int lgSR, const int64_t* rp, const int32_t* ci,
-                              SellImage& L) {
+                              SellImage& L, bool rel) {
   const int64_t SR = int64_t(1) << lgSR, ns = (N + SR - 1) / SR;
   L.lgSR = lgSR;
   int64_t* wid = dalloc<int64_t>(ns + 1);
@@ -321,10 +327,15 @@ inline void build_sell_layout(cudaStream_t s, int64_t N, int lgSR, const int64_t
   scan_i64(s, wid, L.soff, ns + 1);
   cudaFree(wid);
   CK(cudaMemcpy(&L.entries, L.soff + ns, 8, cudaMemcpyDeviceToHost));
-  L.col = dalloc<int32_t>(L.entries);
-  CK(cudaMemsetAsync(L.col, 0, L.entries * 4, s));
+  if (rel) {
+    L.off = dalloc<int16_t>(L.entries);
+    CK(cudaMemsetAsync(L.off, 0, L.entries * 2, s));
+  } else {
+    L.col = dalloc<int32_t>(L.entries);
+    CK(cudaMemsetAsync(L.col, 0, L.entries * 4, s));
+  }
   k_sell_fill<double, P_DOUBLE><<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
-      N, lgSR, rp, ci, nullptr, L.soff, L.col, (double*)nullptr, nullptr, nullptr, 0.0);
+      N, lgSR, rp, ci, nullptr, L.soff, L.col, L.off, (double*)nullptr, nullptr, nullptr, 0.0);
   CKL();
   CK(cudaStreamSynchronize(s));
 }
@@ -337,7 +348,7 @@ inline VO* fill_sell_values(cudaStream_t s, int64_t N, const SellImage& L, const
   VO* out = dalloc<VO>(L.entries);
   CK(cudaMemsetAsync(out, 0, L.entries * sizeof(VO), s));
   k_sell_fill<VO, PR><<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, L.lgSR, rp, nullptr, val, L.soff, nullptr,
-                                                                  out, dpos, din, alpha);
+                                                                  nullptr, out, dpos, din, alpha);
   CKL();
   CK(cudaStreamSynchronize(s));
   return out;
@@ -397,7 +408,7 @@ struct OuterA {
       go(op);
     } else {
       Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
-                      static_cast<const double*>(h->sellA.val)};
+                      static_cast<const double*>(h->sellA.val), h->sellA.off};
       go(op);
     }
     CKL();
@@ -413,7 +424,7 @@ struct OuterA {
       go(op);
     } else {
       Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
-                      static_cast<const double*>(h->sellA.val)};
+                      static_cast<const double*>(h->sellA.val), h->sellA.off};
       go(op);
     }
     CKL();
@@ -544,7 +555,7 @@ struct Engine final : EngineBase {
     } else {
       // SELL image of the union pattern with VA rows per lane, values of
       // H / S rounded to u_r (rounded_copy, inner_solver.cpp:41-45) on the device
-      build_sell_layout(h->stream, h->N, ilog2(32 * VA), h->d_urp, h->d_uci, sHS);
+      build_sell_layout(h->stream, h->N, ilog2(32 * VA), h->d_urp, h->d_uci, sHS, h->max_band < 32768);
       auto fill = [&](const double* src) -> C* {
         if (u_r == GADI_HALF)
           return fill_sell_values<C, P_HALF>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
@@ -554,8 +565,8 @@ struct Engine final : EngineBase {
       };
       dH = fill(h->d_mv);
       dS = fill(h->d_nv);
-      opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH};
-      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS};
+      opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH, sHS.off};
+      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS, sHS.off};
     }
   }
 

@@ -221,7 +221,32 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
 
   double mloc = 0.0;
   int flag = 0;
+  // identity-operand policies start each point from a global vector (b, rhs):
+  // those loads are issued one plane ahead so their latency hides behind a
+  // plane of folding
+  auto chunk_e0 = [&](int ii, int rr) -> int64_t {
+    const int c = ((warp * g.CPT + rr) << 5) + lane;
+    return (int64_t)ii * g.nn + (int64_t)(j0 + (c >> g.lgTR)) * n + (c & (g.TR - 1)) * VEC;
+  };
+  Acc nxt[ST25_CPT_MAX][VEC];
+  if constexpr (P::IDENT) {
+#pragma unroll
+    for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
+      if (rr < g.CPT) pol.init(chunk_e0(ib, rr), nxt[rr]);
+  }
   for (int i = ib; i < ie; ++i) {
+    Acc cur[ST25_CPT_MAX][VEC];
+    if constexpr (P::IDENT) {
+#pragma unroll
+      for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) cur[rr][v] = nxt[rr][v];
+      if (i + 1 < ie) {
+#pragma unroll
+        for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
+          if (rr < g.CPT) pol.init(chunk_e0(i + 1, rr), nxt[rr]);
+      }
+    }
     const RT *om, *oc, *op;
     if constexpr (P::IDENT) {
       if (i + 1 <= n - 1) wait_q(i + 1);
@@ -250,7 +275,12 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
         const int sidx = (jl + 1) * n + k0;
         const int64_t e0 = (int64_t)i * g.nn + (int64_t)j * n + k0;
         Acc acc[VEC];
-        pol.init(e0, acc);
+        if constexpr (P::IDENT) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = cur[rr][v];
+        } else {
+          pol.init(e0, acc);
+        }
         const auto& c7 = pol.c7;
         const auto f = pol.fold();
         RT cc[VEC], nb[VEC];
