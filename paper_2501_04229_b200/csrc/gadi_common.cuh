@@ -134,6 +134,16 @@ __device__ __forceinline__ void ld_vec(const T* __restrict__ p, int64_t e0, T (&
     const T* t = reinterpret_cast<const T*>(&u);
 #pragma unroll
     for (int i = 0; i < VEC; ++i) v[i] = t[i];
+  } else if constexpr (VEC * sizeof(T) == 8) {
+    uint2 u = __ldg(reinterpret_cast<const uint2*>(p + e0));
+    const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = t[i];
+  } else if constexpr (VEC * sizeof(T) == 4) {
+    unsigned u = __ldg(reinterpret_cast<const unsigned*>(p + e0));
+    const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v[i] = t[i];
   } else {
 #pragma unroll
     for (int i = 0; i < VEC; ++i) v[i] = p[e0 + i];

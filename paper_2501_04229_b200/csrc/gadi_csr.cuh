@@ -23,6 +23,7 @@ namespace gadi {
 
 template <class V>
 struct Sell {
+  using value_type = V;  // the storage format's values (exact: they are rounded to u_r)
   int64_t N;
   int lgSR;                              // log2(rows per slice)
   const int64_t* __restrict__ soff;      // slice start offsets (entries)
@@ -39,11 +40,18 @@ struct Sell {
     const int64_t base = soff[s] + (e0 & (SR - 1));
     const int width = (int)((soff[s + 1] - soff[s]) >> lgSR);
     int ln[VEC];
+    uint16_t lv[VEC];
+    ld_vec<uint16_t, VEC>(len, e0, lv);
+    int lmax = 0;  // this lane's longest row: the padding beyond it is never read
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) ln[v] = len[e0 + v];
+    for (int v = 0; v < VEC; ++v) {
+      ln[v] = lv[v];
+      lmax = max(lmax, ln[v]);
+    }
+    if (lmax > width) lmax = width;
     if (off) {
 #pragma unroll 2
-      for (int k = 0; k < width; ++k) {
+      for (int k = 0; k < lmax; ++k) {
         const int64_t pos = base + (int64_t)k * SR;
         int16_t ov[VEC];
         V vv[VEC];
@@ -51,11 +59,11 @@ struct Sell {
         ld_vec<V, VEC>(val, pos, vv);
 #pragma unroll
         for (int v = 0; v < VEC; ++v)
-          if (k < ln[v]) acc[v] = f(acc[v], vv[v], x.at(e0 + v + ov[v]));
+          if (k < ln[v]) acc[v] = f(acc[v], ld_c<V, Acc>(vv[v]), x.at(e0 + v + ov[v]));
       }
       return;
     }
-    for (int k = 0; k < width; ++k) {
+    for (int k = 0; k < lmax; ++k) {
       const int64_t pos = base + (int64_t)k * SR;
       int32_t cv[VEC];
       V vv[VEC];
@@ -75,7 +83,7 @@ struct Sell {
       ld_vec<V, VEC>(val, pos, vv);
 #pragma unroll
       for (int v = 0; v < VEC; ++v)
-        if (k < ln[v]) acc[v] = f(acc[v], vv[v], x.at(cv[v]));
+        if (k < ln[v]) acc[v] = f(acc[v], ld_c<V, Acc>(vv[v]), x.at(cv[v]));
     }
   }
 };

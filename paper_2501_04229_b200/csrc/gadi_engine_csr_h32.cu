@@ -3,6 +3,6 @@
 
 namespace gadi_host {
 GADI_ENGINE_FACTORY(make_engine_csr_h32) {
-  return new Engine<Sell<float>, __half, float>(h, sp, a, om, ur, acc);
+  return new Engine<Sell<__half>, __half, float>(h, sp, a, om, ur, acc);
 }
 }  // namespace gadi_host

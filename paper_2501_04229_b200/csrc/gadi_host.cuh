@@ -95,6 +95,34 @@ inline Geo make_geo(int64_t N, int vec) {
   return g;
 }
 
+// Operand window of a banded sparse operator staged in shared memory
+// (gadi_kernels.cuh stage_window): the band passed to the kernel (0 = read the
+// operand from global memory) and the dynamic shared memory it needs. Used
+// when the window is small and not dominated by the halo (band <= 2 block rows).
+struct Window {
+  int64_t band = 0;
+  size_t bytes = 0;
+};
+inline Window window_for(const Geo& g, int vec, size_t tsize, int64_t max_band, bool aligned) {
+  Window w;
+  static const bool disabled = std::getenv("GADI_NO_WINDOW") != nullptr;  // A/B measurement knob
+  if (disabled || !aligned || vec <= 1 || max_band == INT64_MAX) return w;
+  const int64_t br = (int64_t)g.W * g.R * g.L * vec;
+  const int64_t band = std::max<int64_t>(max_band, 1);
+  const size_t bytes = (size_t)(br + 2 * band + vec) * tsize;
+  // > 64 KB costs more occupancy than the gathers gain (measured: the binary64
+  // residual on A with a 96 KB window ran 1.65 ms vs 1.28 ms reading x from L1/L2)
+  if (band > 2 * br || bytes > 64 * 1024) return w;
+  w.band = band;
+  w.bytes = bytes;
+  return w;
+}
+template <class K>
+inline void smem_attr(K kern, size_t bytes) {
+  if (bytes > 48 * 1024)
+    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
 inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
   return (N % vec == 0) && is_pow2(N / vec) && (!stencil || n % vec == 0);
 }
@@ -379,11 +407,14 @@ struct OuterA {
     CK(cudaMemsetAsync(&h->st->maxbits, 0, sizeof(unsigned long long), h->stream));
     const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
     const Geo g = make_geo(h->N, al ? 2 : 1);
+    const Window win = h->stencil() ? Window{} : window_for(g, 2, sizeof(double), h->max_band, al);
     auto go = [&](auto op) {
       auto L = [&](auto pt, auto vt) {
         constexpr int PF = decltype(pt)::v, V = decltype(vt)::v;
-        k_resid_A<decltype(op), PF, V><<<g.nblk, g.threads(), 0, h->stream>>>(op, x, h->d_b, s,
-                                                                               scaling ? 1 : 0, g, red_of(h), h->st);
+        auto kern = k_resid_A<decltype(op), PF, V>;
+        smem_attr(kern, win.bytes);
+        kern<<<g.nblk, g.threads(), win.bytes, h->stream>>>(op, x, h->d_b, s, scaling ? 1 : 0, g, red_of(h), h->st,
+                                                            win.band);
       };
       auto LV = [&](auto pt) {
         if (al) L(pt, VecTag<2>{});
@@ -472,8 +503,9 @@ struct Engine final : EngineBase {
   static constexpr bool SPARSE = !std::is_same<Op, Stencil7<C>>::value;
   // CG / GMRES work vectors
   T *pA = nullptr, *pB = nullptr, *q = nullptr, *wA = nullptr, *wB = nullptr, *gr = nullptr, *V = nullptr;
-  C* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
-  C* dS = nullptr;
+  using OV = typename Op::value_type;
+  OV* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
+  OV* dS = nullptr;
   SellImage sHS;
   int m_restart = 30;
   std::vector<T*> owned;
@@ -481,6 +513,7 @@ struct Engine final : EngineBase {
   St25Geo g25;        // CG p-update + SpMV: two staged inputs + operand ring
   St25Geo g25m;       // Arnoldi matvec: one staged input + operand ring
   St25Geo g25i;       // GMRES residual: identity operand, folded from the stages
+  Window win;         // sparse operators: operand window in shared memory
 
   T* vec() {
     T* v = dalloc<T>(h->N);
@@ -499,6 +532,7 @@ struct Engine final : EngineBase {
     const int64_t N = h->N;
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
+    if constexpr (SPARSE) win = window_for(geo, VA, sizeof(T), h->max_band, aligned);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       constexpr int rsz = sizeof(typename RingOf<T, C>::type);
       st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz) && make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz) &&
@@ -556,12 +590,12 @@ struct Engine final : EngineBase {
       // SELL image of the union pattern with VA rows per lane, values of
       // H / S rounded to u_r (rounded_copy, inner_solver.cpp:41-45) on the device
       build_sell_layout(h->stream, h->N, ilog2(32 * VA), h->d_urp, h->d_uci, sHS, h->max_band < 32768);
-      auto fill = [&](const double* src) -> C* {
+      auto fill = [&](const double* src) -> OV* {
         if (u_r == GADI_HALF)
-          return fill_sell_values<C, P_HALF>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+          return fill_sell_values<OV, P_HALF>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
         if (u_r == GADI_SINGLE)
-          return fill_sell_values<C, P_SINGLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
-        return fill_sell_values<C, P_DOUBLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+          return fill_sell_values<OV, P_SINGLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+        return fill_sell_values<OV, P_DOUBLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
       };
       dH = fill(h->d_mv);
       dS = fill(h->d_nv);
@@ -648,7 +682,9 @@ struct Engine final : EngineBase {
         constexpr int V_ = decltype(vt)::v;
         if constexpr (SPARSE) {  // p-update as its own pass: a gathered operand is not re-formed per nonzero
           k_cg_pupd<T, C, V_><<<geo.nblk, nt, 0, s>>>(r, p_in, p_out, first, geo, h->st);
-          k_cg_spmvp<Op, T, C, V_, false><<<geo.nblk, nt, 0, s>>>(o, r, p_out, p_out, q, first, geo, rd, h->st);
+          auto kern = k_cg_spmvp<Op, T, C, V_, false>;
+          smem_attr(kern, win.bytes);
+          kern<<<geo.nblk, nt, win.bytes, s>>>(o, r, p_out, p_out, q, first, geo, rd, h->st, win.band);
           ++h->launches;
         } else if (!spmvp25(o, r, p_in, p_out, first)) {
           k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
@@ -690,8 +726,12 @@ struct Engine final : EngineBase {
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        if (x_zero || !gmresid25(o, x, rhs))
-          k_gm_resid<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st);
+        if (x_zero || !gmresid25(o, x, rhs)) {
+          auto kern = k_gm_resid<Op, T, C, V_>;
+          const size_t sm = x_zero ? 0 : win.bytes;
+          smem_attr(kern, sm);
+          kern<<<geo.nblk, nt, sm, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st, x_zero ? 0 : win.band);
+        }
         k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
       });
       CKL();
@@ -726,7 +766,9 @@ struct Engine final : EngineBase {
           constexpr int V_ = decltype(vt)::v;
           if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
             k_scale<T, V_><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
-            k_gm_matvec<Op, T, C, V_, false><<<geo.nblk, nt, 0, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st);
+            auto kern = k_gm_matvec<Op, T, C, V_, false>;
+            smem_attr(kern, win.bytes);
+            kern<<<geo.nblk, nt, win.bytes, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st, win.band);
             ++h->launches;
           } else if (!gmmatvec25(o, wprev, inv, vj, w)) {
             k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);

@@ -243,6 +243,34 @@ __device__ __forceinline__ void fold_seg(const Op& op, const Src& x, const Seg& 
   }
 }
 
+// Rows a block covers on the aligned path (seg_run's contiguous W*R*L segments).
+template <int VEC>
+__device__ __forceinline__ int64_t block_rows(const Geo& g) {
+  return (int64_t)g.W * g.R * g.L * VEC;
+}
+
+// Stage x[block rows +- band] in dynamic shared memory (banded sparse operators).
+template <class T, int VEC>
+__device__ __forceinline__ SmemSrc<T> stage_window(const T* __restrict__ x, const Geo& g, int64_t band) {
+  extern __shared__ __align__(16) unsigned char gadi_wsm[];
+  T* w = reinterpret_cast<T*>(gadi_wsm);
+  const int64_t BR = block_rows<VEC>(g), r0 = (int64_t)blockIdx.x * BR;
+  int64_t lo = r0 - band;
+  lo = lo < 0 ? 0 : (lo & ~(int64_t)(VEC - 1));
+  int64_t hi = r0 + BR + band;
+  hi = hi > g.N ? g.N : hi;
+  const int64_t len = hi - lo;
+  for (int64_t i = (int64_t)threadIdx.x * VEC; i < len; i += (int64_t)blockDim.x * VEC) {
+    if (VEC * sizeof(T) == 16 && i + VEC <= len) {
+      *reinterpret_cast<uint4*>(w + i) = __ldg(reinterpret_cast<const uint4*>(x + lo + i));
+    } else {
+      for (int k = 0; k < VEC && i + k < len; ++k) w[i + k] = x[lo + i + k];
+    }
+  }
+  __syncthreads();
+  return SmemSrc<T>{w, lo};
+}
+
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
   // PACKED = false: ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2
@@ -324,7 +352,7 @@ __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int ma
 template <class Op, class T, class C, int VEC, bool FUSE = true>
 __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r, const T* __restrict__ p_in,
                                                   T* __restrict__ p_out, T* __restrict__ q, int first, Geo g,
-                                                  Red rd, DevState* st) {
+                                                  Red rd, DevState* st, int64_t wband = 0) {
   if (*(volatile int*)&st->cg_done) return;
   GADI_G;
   C w0;
@@ -347,6 +375,9 @@ __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r
   };
   if constexpr (FUSE) {
     const PUpdSrc<T, C> src{r, p_in, from_dbl<C>(st->cg_beta), first};
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  } else if (VEC > 1 && wband > 0) {
+    const SmemSrc<T> src = stage_window<T, VEC>(p_in, g, wband);
     seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
   } else {
     const PlainSrc<T> src{p_in};
@@ -452,20 +483,19 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
 template <class Op, class T, class C, int VEC>
 __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x, int x_zero,
                                                   const T* __restrict__ rhs, T* __restrict__ r, Geo g, Red rd,
-                                                  DevState* st) {
+                                                  DevState* st, int64_t wband = 0) {
   GADI_G;
   int bad = 0;
   double m = 0.0;
   C w0;
   double w1;
-  seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) {
+  auto body = [&](const Seg& s, double& d, const auto& src) {
     T bv[G], xc[G], rv[G];
     load_seg<T, VEC, G>(rhs, s, bv);
     C acc[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
-    if (x_zero) fold_seg<VEC, G>(op, ZeroSrc<T>{}, s, acc, ResidF<C, T>(), xc);
-    else fold_seg<VEC, G>(op, PlainSrc<T>{x}, s, acc, ResidF<C, T>(), xc);
+    fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -479,7 +509,17 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
     }
     store_seg<T, VEC, G>(r, s, rv);
     d = seg_sum<double, G>(td, s.len);
-  }, w0, w1);
+  };
+  if (x_zero) {
+    const ZeroSrc<T> src{};
+    seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
+  } else if (VEC > 1 && wband > 0) {
+    const SmemSrc<T> src = stage_window<T, VEC>(x, g, wband);
+    seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
+  } else {
+    const PlainSrc<T> src{x};
+    seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
+  }
   block_max_abs(&st->maxbits, m);
   or_flags(&st->flags, bad);
   C dc;
@@ -546,21 +586,18 @@ __global__ void __launch_bounds__(256) k_scale(const T* __restrict__ src, T* __r
 template <class Op, class T, class C, int VEC, bool SCALED>
 __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ wprev, double inv,
                                                    T* vj, const T* v0,
-                                                   T* __restrict__ w, Geo g, Red rd, DevState* st) {
+                                                   T* __restrict__ w, Geo g, Red rd, DevState* st,
+                                                   int64_t wband = 0) {
   GADI_G;
   C w0;
   double w1;
-  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+  auto body = [&](const Seg& s, C& c, const auto& src) {
     C acc[G];
     T vv[G], wv[G], v0v[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) acc[i] = Ar<C>::zero();
-    if constexpr (SCALED) {
-      fold_seg<VEC, G>(op, ScaleSrc<T>{wprev, inv}, s, acc, MatvecF<C, T>(), vv);
-      store_seg<T, VEC, G>(vj, s, vv);
-    } else {
-      fold_seg<VEC, G>(op, PlainSrc<T>{vj}, s, acc, MatvecF<C, T>(), vv);
-    }
+    fold_seg<VEC, G>(op, src, s, acc, MatvecF<C, T>(), vv);
+    if constexpr (SCALED) store_seg<T, VEC, G>(vj, s, vv);
 #pragma unroll
     for (int i = 0; i < G; ++i) wv[i] = st_t<T, C>(acc[i]);
     store_seg<T, VEC, G>(w, s, wv);
@@ -574,7 +611,17 @@ __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ 
 #pragma unroll
     for (int i = 0; i < G; ++i) tc[i] = Ar<C>::mul(ld_c<T, C>(wv[i]), ld_c<T, C>(v0v[i]));
     c = seg_sum<C, G>(tc, s.len);
-  }, w0, w1);
+  };
+  if constexpr (SCALED) {
+    const ScaleSrc<T> src{wprev, inv};
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  } else if (VEC > 1 && wband > 0) {
+    const SmemSrc<T> src = stage_window<T, VEC>(vj, g, wband);
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  } else {
+    const PlainSrc<T> src{vj};
+    seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
+  }
   C h;
   double dummy;
   if (grid_finish(w0, w1, g, rd, h, dummy)) st->hcol[0] = to_dbl(h);
@@ -658,13 +705,13 @@ __global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero
 template <class Op, int PF, int VEC>
 __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict__ x, const double* __restrict__ b,
                                                  double* __restrict__ sv, int scaling, Geo g, Red rd,
-                                                 DevState* st) {
+                                                 DevState* st, int64_t wband = 0) {
   GADI_G;
   double m = 0.0, w0, w1;
-  seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) {
+  auto body = [&](const Seg& s, double& d, const auto& src) {
     double acc[G], xc[G];
     load_seg<double, VEC, G>(b, s, acc);
-    fold_seg<VEC, G>(op, PlainSrc<double>{x}, s, acc, ResidAF<PF>(), xc);
+    fold_seg<VEC, G>(op, src, s, acc, ResidAF<PF>(), xc);
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -673,7 +720,14 @@ __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict
     }
     if (sv) store_seg<double, VEC, G>(sv, s, acc);
     d = seg_sum<double, G>(td, s.len);
-  }, w0, w1);
+  };
+  if (VEC > 1 && wband > 0) {
+    const SmemSrc<double> src = stage_window<double, VEC>(x, g, wband);
+    seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) { body(s, d, src); }, w0, w1);
+  } else {
+    const PlainSrc<double> src{x};
+    seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) { body(s, d, src); }, w0, w1);
+  }
   block_max_abs(&st->maxbits, m);
   double dummy, ss;
   if (grid_finish(w0, w1, g, rd, dummy, ss)) {

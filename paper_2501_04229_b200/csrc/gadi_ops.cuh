@@ -26,6 +26,29 @@ struct PlainSrc {
   __device__ __forceinline__ T at(int64_t e) const { return p[e]; }
 };
 
+// The operand window [lo, lo + len) of a banded sparse operator staged in
+// shared memory: gathers x[col] hit shared memory (a few bank-conflict
+// wavefronts per warp instruction) instead of scattered L1 sectors.
+template <class T>
+struct SmemSrc {
+  const T* w;  // window in shared memory
+  int64_t lo;  // global index of w[0] (a multiple of the segment width)
+  template <int VEC>
+  __device__ __forceinline__ void vec(int64_t e0, T (&v)[VEC]) const {
+    const T* p = w + (e0 - lo);
+    if constexpr (VEC * sizeof(T) == 16) {
+      const uint4 u = *reinterpret_cast<const uint4*>(p);
+      const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = t[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) v[i] = p[i];
+    }
+  }
+  __device__ __forceinline__ T at(int64_t e) const { return w[e - lo]; }
+};
+
 template <class T>
 struct ZeroSrc {  // the x = 0 start vector (+0 everywhere), no memory traffic
   template <int VEC>
@@ -77,6 +100,7 @@ struct ScaleSrc {  // v = round(inv * w), inv in binary64 (scale, kernels.cpp:16
 // in the reference CSR.
 template <class V>
 struct Stencil7 {
+  using value_type = V;
   int64_t n, nn, N;
   V c[7];
   int lg;  // log2(n) when n is a power of two (always on the aligned path), else -1
@@ -148,6 +172,7 @@ struct Stencil7 {
 // sparse.cpp:166-178) and differ only in values.
 template <class V>
 struct Csr {
+  using value_type = V;
   int64_t N;
   const int64_t* __restrict__ rp;
   const int32_t* __restrict__ ci;

@@ -10,6 +10,7 @@ from bench_cfg import WORKLOADS  # noqa
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c3")
 ap.add_argument("--outer", type=int, default=2)
+ap.add_argument("--repeat", type=int, default=1)
 a = ap.parse_args()
 wl = WORKLOADS[a.workload]
 S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
@@ -20,6 +21,7 @@ sysx.make_rhs(wl["seed"], wl["lo"], wl["hi"], xt.data_ptr(), b.data_ptr())
 cfg = g.GadiConfig(alpha=wl["alpha"], xi=1e-20, u_r=g.Precision(wl["u_r"]), accum=g.Accum(wl["accum"]),
                    inner=g.InnerSolverSpec(g.InnerMethod.Cg, wl["eps"], wl["max_inner"], wl["restart"]),
                    max_outer_iters=a.outer)
-rep = sysx.solve_device(b.data_ptr(), x.data_ptr(), cfg)
-print(f"outer={rep.outer_iters} cg={rep.h_iters} gmres={rep.s_iters} solve_ms={rep.solve_ms:.1f} "
+for _ in range(a.repeat):
+    rep = sysx.solve_device(b.data_ptr(), x.data_ptr(), cfg)
+    print(f"outer={rep.outer_iters} cg={rep.h_iters} gmres={rep.s_iters} solve_ms={rep.solve_ms:.1f} "
       f"h_ms={rep.h_ms:.1f} s_ms={rep.s_ms:.1f} outer_ms={rep.outer_ms:.1f} launches={rep.launches}")
