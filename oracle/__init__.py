@@ -135,6 +135,8 @@ class Oracle:
         L.orc_regularize.argtypes = [C.POINTER(_OrcCsr), C.c_double, _i64p, _i64p, _f64p, _f64p]
         L.orc_krylov.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, C.c_double, C.c_int, C.c_int,
                                  C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.orc_krylov_af.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, C.c_double, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.orc_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, _f64p, C.POINTER(Config), _f64p, _f64p,
                                 C.c_int, C.POINTER(Report)]
         L.orc_gpr.argtypes = [_f64p, _f64p, C.c_int, C.POINTER(GprOpts), _f64p, C.c_int, _f64p,
@@ -227,13 +229,15 @@ class Oracle:
         self.L.orc_regularize(C.byref(oc), alpha, _p(rp, _i64p), _p(ci, _i64p), _p(vh), _p(vs))
         return CSR(A.n, rp, ci, vh), CSR(A.n, rp, ci, vs)
 
-    def krylov(self, M: CSR, rhs, method, eps, max_inner, restart, fmt, stop_norm):
+    def krylov(self, M: CSR, rhs, method, eps, max_inner, restart, fmt, stop_norm, af=None):
+        """af: arithmetic format (None = fmt, the reference); SINGLE over HALF
+        storage restates the device's GADI_ACCUM_FP32 inner mode."""
         rhs = np.ascontiguousarray(rhs, np.float64)
         x = np.zeros(M.n)
         it, st = C.c_int(), C.c_int()
         oc = _oc(M)
-        self.L.orc_krylov(C.byref(oc), _p(rhs), method, eps, max_inner, restart, fmt, stop_norm,
-                          _p(x), C.byref(it), C.byref(st))
+        self.L.orc_krylov_af(C.byref(oc), _p(rhs), method, eps, max_inner, restart, fmt,
+                             fmt if af is None else af, stop_norm, _p(x), C.byref(it), C.byref(st))
         return x, it.value, st.value
 
     def solve(self, A: CSR, b, cfg: Config, x0=None, cap=100000):

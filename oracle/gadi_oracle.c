@@ -305,7 +305,22 @@ int64_t orc_regularize(const orc_csr* A, double alpha, int64_t* rpH, int64_t* ci
   return c;
 }
 
-/* -------------------------------------------------------------------- krylov */
+/* -------------------------------------------------------------------- krylov
+ * The Krylov solvers take a storage format `fmt` (u_r: every vector entry
+ * and matrix value is a u_r number) and an arithmetic format `af`. af == fmt
+ * is the reference (inner_solver.cpp: every op rounded to u_r). af = binary32
+ * with fmt = binary16 restates the device's GADI_ACCUM_FP32 mode (binary16
+ * storage, binary32 arithmetic and accumulation; not in the reference): each
+ * op is rounded to af, each stored vector entry once more to fmt. */
+static void matvec_s(const orc_csr* A, const double* x, int af, int fmt, double* y) {
+  orc_matvec(A, x, af, y);
+  if (fmt != af)
+    for (int64_t i = 0; i < A->n; ++i) y[i] = R(y[i], fmt);
+}
+static void axpy_s(double a, const double* x, const double* y, int64_t n, int af, int fmt, double* z) {
+  for (int64_t i = 0; i < n; ++i) z[i] = R(R(y[i] + R(a * x[i], af), af), fmt);
+}
+
 static void rounded_values(const orc_csr* A, int fmt, orc_csr* out, double* buf) {
   *out = *A;
   for (int64_t k = 0; k < A->rp[A->n]; ++k) buf[k] = R(A->v[k], fmt);
@@ -313,7 +328,7 @@ static void rounded_values(const orc_csr* A, int fmt, orc_csr* out, double* buf)
 }
 
 /* cg_solve, inner_solver.cpp:47-83. */
-static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_inner, int fmt,
+static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_inner, int fmt, int af,
                     double stop_norm, double* x, int* iters) {
   const int64_t n = A0->n;
   double* vb = (double*)malloc((size_t)A0->rp[n] * sizeof(double) + 8);
@@ -328,7 +343,7 @@ static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_in
     r[i] = R(rhs[i], fmt);
     p[i] = r[i];
   }
-  double rs = orc_dot(r, r, n, fmt);
+  double rs = orc_dot(r, r, n, af);
   int status = GADI_INNER_STAGNATED, it;
   int done = 0;
   for (it = 0; it < max_inner; ++it) {
@@ -338,21 +353,21 @@ static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_in
       done = 1;
       break;
     }
-    orc_matvec(&A, p, fmt, Ap);
-    const double pap = orc_dot(p, Ap, n, fmt);
+    matvec_s(&A, p, af, fmt, Ap);
+    const double pap = orc_dot(p, Ap, n, af);
     if (pap == 0.0 || !isfinite(pap)) break;
-    const double a = R(rs / pap, fmt);
-    orc_axpy(a, p, x, n, fmt, x);
-    orc_axpy(-a, Ap, r, n, fmt, r);
-    const double rs_new = orc_dot(r, r, n, fmt);
+    const double a = R(rs / pap, af);
+    axpy_s(a, p, x, n, af, fmt, x);
+    axpy_s(-a, Ap, r, n, af, fmt, r);
+    const double rs_new = orc_dot(r, r, n, af);
     if (!isfinite(rs_new) || !all_finite(r, n)) {
       *iters = it + 1;
       status = GADI_INNER_OVERFLOW;
       done = 1;
       break;
     }
-    const double beta = R(rs_new / rs, fmt);
-    orc_axpy(beta, p, r, n, fmt, p);
+    const double beta = R(rs_new / rs, af);
+    axpy_s(beta, p, r, n, af, fmt, p);
     rs = rs_new;
   }
   if (!done) {
@@ -368,7 +383,7 @@ static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_in
 
 /* gmres_solve, inner_solver.cpp:85-194. */
 static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max_inner, int restart,
-                       int fmt, double stop_norm, double* x, int* iters) {
+                       int fmt, int af, double stop_norm, double* x, int* iters) {
   const int64_t n = A0->n;
   double* vb = (double*)malloc((size_t)A0->rp[n] * sizeof(double) + 8);
   orc_csr A;
@@ -387,12 +402,12 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
   for (int64_t i = 0; i < n; ++i) x[i] = 0.0;
   int total = 0, status = -1;
   while (total < max_inner) {
-    orc_residual(&A, x, rhs, fmt, fmt, r);
+    orc_residual(&A, x, rhs, af, fmt, r);
     if (!all_finite(r, n)) {
       status = GADI_INNER_OVERFLOW;
       break;
     }
-    const double beta = orc_norm2(r, n, fmt);
+    const double beta = orc_norm2(r, n, af);
     if (orc_norm2_64(r, n) <= target) {
       status = GADI_INNER_CONVERGED;
       break;
@@ -407,13 +422,13 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
     g[0] = beta;
     int j = 0, happy = 0;
     for (; j < m && total < max_inner; ++j, ++total) {
-      orc_matvec(&A, V + (size_t)j * n, fmt, w);
+      matvec_s(&A, V + (size_t)j * n, af, fmt, w);
       for (int i = 0; i <= j; ++i) {
-        const double h = orc_dot(w, V + (size_t)i * n, n, fmt);
+        const double h = orc_dot(w, V + (size_t)i * n, n, af);
         HC(i, j) = h;
-        orc_axpy(-h, V + (size_t)i * n, w, n, fmt, w);
+        axpy_s(-h, V + (size_t)i * n, w, n, af, fmt, w);
       }
-      const double h1 = orc_norm2(w, n, fmt);
+      const double h1 = orc_norm2(w, n, af);
       HC(j + 1, j) = h1;
       if (!isfinite(h1)) {
         status = GADI_INNER_OVERFLOW;
@@ -424,26 +439,26 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
         ++nv;
       }
       for (int i = 0; i < j; ++i) {
-        const double t1 = R(R(cs[i] * HC(i, j), fmt) + R(sn[i] * HC(i + 1, j), fmt), fmt);
-        const double t2 = R(R(cs[i] * HC(i + 1, j), fmt) - R(sn[i] * HC(i, j), fmt), fmt);
+        const double t1 = R(R(cs[i] * HC(i, j), af) + R(sn[i] * HC(i + 1, j), af), af);
+        const double t2 = R(R(cs[i] * HC(i + 1, j), af) - R(sn[i] * HC(i, j), af), af);
         HC(i, j) = t1;
         HC(i + 1, j) = t2;
       }
       const double a = HC(j, j), b = HC(j + 1, j);
-      const double denom = R(hypot(a, b), fmt);
+      const double denom = R(hypot(a, b), af);
       if (denom == 0.0) {
         happy = 1;
         ++j;
         ++total;
         break;
       }
-      cs[j] = R(a / denom, fmt);
-      sn[j] = R(b / denom, fmt);
+      cs[j] = R(a / denom, af);
+      sn[j] = R(b / denom, af);
       HC(j, j) = denom;
       HC(j + 1, j) = 0.0;
       const double gj = g[j];
-      g[j] = R(cs[j] * gj, fmt);
-      g[j + 1] = R(-sn[j] * gj, fmt);
+      g[j] = R(cs[j] * gj, af);
+      g[j + 1] = R(-sn[j] * gj, af);
       if (fabs(g[j + 1]) <= target || h1 == 0.0) {
         happy = 1;
         ++j;
@@ -453,16 +468,16 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
     }
     for (int i = j - 1; i >= 0; --i) {
       double acc = g[i];
-      for (int k = i + 1; k < j; ++k) acc = R(acc - R(HC(i, k) * y[k], fmt), fmt);
-      y[i] = R(acc / HC(i, i), fmt);
+      for (int k = i + 1; k < j; ++k) acc = R(acc - R(HC(i, k) * y[k], af), af);
+      y[i] = R(acc / HC(i, i), af);
     }
-    for (int i = 0; i < j; ++i) orc_axpy(y[i], V + (size_t)i * n, x, n, fmt, x);
+    for (int i = 0; i < j; ++i) axpy_s(y[i], V + (size_t)i * n, x, n, af, fmt, x);
     if (!all_finite(x, n)) {
       status = GADI_INNER_OVERFLOW;
       break;
     }
     if (happy) {
-      orc_residual(&A, x, rhs, fmt, fmt, r);
+      orc_residual(&A, x, rhs, af, fmt, r);
       if (orc_norm2_64(r, n) <= target) {
         status = GADI_INNER_CONVERGED;
         break;
@@ -486,13 +501,17 @@ out:
 }
 
 /* krylov_solve, inner_solver.cpp:198-204. */
+int orc_krylov_af(const orc_csr* M, const double* rhs, int method, double eps, int max_inner, int restart,
+                  int fmt, int af, double stop_norm, double* x, int* iters, int* status) {
+  if (method == GADI_INNER_CG)
+    *status = cg_solve(M, rhs, eps, max_inner, fmt, af, stop_norm, x, iters);
+  else
+    *status = gmres_solve(M, rhs, eps, max_inner, restart, fmt, af, stop_norm, x, iters);
+  return 0;
+}
 int orc_krylov(const orc_csr* M, const double* rhs, int method, double eps, int max_inner, int restart,
                int fmt, double stop_norm, double* x, int* iters, int* status) {
-  if (method == GADI_INNER_CG)
-    *status = cg_solve(M, rhs, eps, max_inner, fmt, stop_norm, x, iters);
-  else
-    *status = gmres_solve(M, rhs, eps, max_inner, restart, fmt, stop_norm, x, iters);
-  return 0;
+  return orc_krylov_af(M, rhs, method, eps, max_inner, restart, fmt, fmt, stop_norm, x, iters, status);
 }
 
 /* -------------------------------------------------------------------- solver */
@@ -510,6 +529,9 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
   if (cfg->inner.method == GADI_INNER_LU_DIRECT) return GADI_E_UNSUPPORTED;
   const double xi = cfg->xi > 0.0 ? cfg->xi : (cfg->u == D ? 1e-26 : cfg->u == GADI_SINGLE ? 1e-8 : 1e-4);
   const int ur_p = cfg->u_r, u_p = cfg->u;
+  /* inner arithmetic: u_r (the reference), or binary32 over binary16 storage
+   * under GADI_ACCUM_FP32 (gadi_cuda.h; the device's h32 engine) */
+  const int af_p = (cfg->accum == GADI_ACCUM_FP32 && ur_p == GADI_HALF) ? GADI_SINGLE : ur_p;
 
   memset(rep, 0, sizeof(*rep));
   rep->status = GADI_MAX_ITERS;
@@ -589,15 +611,15 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
     if (k >= cfg->max_outer_iters) { rep->status = GADI_MAX_ITERS; break; }
 
     int it = 0, st = 0;
-    orc_krylov(&H, rhat, cfg->inner.method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
-               cfg->inner.restart, ur_p, stop_norm, z, &it, &st);
+    orc_krylov_af(&H, rhat, cfg->inner.method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
+                  cfg->inner.restart, ur_p, af_p, stop_norm, z, &it, &st);
     rep->inner_iter_totals += it;
     rep->h_iters += it;
     if (st == GADI_INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
     if (st == GADI_INNER_STAGNATED) ++rep->inner_stagnations;
     orc_scale(p_rounded, z, n, ur_p, pz);
-    orc_krylov(&S, pz, s_method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
-               cfg->inner.restart, ur_p, stop_norm, yv, &it, &st);
+    orc_krylov_af(&S, pz, s_method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
+                  cfg->inner.restart, ur_p, af_p, stop_norm, yv, &it, &st);
     rep->inner_iter_totals += it;
     rep->s_iters += it;
     if (st == GADI_INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }

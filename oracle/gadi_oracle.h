@@ -71,6 +71,10 @@ int64_t orc_regularize(const orc_csr* A, double alpha, int64_t* rpH, int64_t* ci
 /* ---- inner_solver.cpp:47-194 ---- */
 int orc_krylov(const orc_csr* M, const double* rhs, int method, double eps, int max_inner, int restart,
                int fmt, double stop_norm, double* x, int* iters, int* status);
+/* the same with arithmetic format af over storage format fmt (af == fmt is
+ * the reference; af = binary32 over binary16 = the device's GADI_ACCUM_FP32) */
+int orc_krylov_af(const orc_csr* M, const double* rhs, int method, double eps, int max_inner, int restart,
+                  int fmt, int af, double stop_norm, double* x, int* iters, int* status);
 
 /* ---- solver.cpp:57-179 + 250-258 (gadi_ir_solve on a CSR system) ---- */
 int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,

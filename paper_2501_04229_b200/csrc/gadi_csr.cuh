@@ -31,6 +31,9 @@ struct Sell {
   const int32_t* __restrict__ col;       // absolute columns, or null and
   const V* __restrict__ val;
   const int16_t* __restrict__ off;       // column - row (narrow band: 2 bytes per entry)
+  const uint8_t* __restrict__ zf = nullptr;  // per-row zflag summary (k_sell_zflags), when built
+
+  __device__ __forceinline__ int zflags(int64_t row) const { return zf[row]; }
 
   template <int VEC, class Src, class X, class Acc, class F>
   __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {
@@ -87,6 +90,19 @@ struct Sell {
     }
   }
 };
+
+// Per-row OR of zflag over the stored coefficients of a SELL image.
+template <class V>
+__global__ void k_sell_zflags(int64_t N, int lgSR, const int64_t* __restrict__ soff, const uint16_t* __restrict__ len,
+                              const V* __restrict__ val, uint8_t* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const int64_t SR = int64_t(1) << lgSR;
+  const int64_t base = soff[r >> lgSR] + (r & (SR - 1));
+  int f = 0;
+  for (int k = 0; k < len[r]; ++k) f |= zflag(val[base + (int64_t)k * SR]);
+  out[r] = (uint8_t)f;
+}
 
 // ------------------------------------------------------------ generator
 #define GADI_VALSALT 0x5851F42D4C957F2Dull

@@ -506,6 +506,7 @@ struct Engine final : EngineBase {
   using OV = typename Op::value_type;
   OV* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
   OV* dS = nullptr;
+  uint8_t *zfH = nullptr, *zfS = nullptr;  // per-row zflag summaries of H / S (residual from x = 0)
   SellImage sHS;
   int m_restart = 30;
   std::vector<T*> owned;
@@ -559,6 +560,8 @@ struct Engine final : EngineBase {
     if (dH) cudaFree(dH);
     if (dS) cudaFree(dS);
     sHS.release();
+    if (zfH) cudaFree(zfH);
+    if (zfS) cudaFree(zfS);
   }
 
   static C cval(double v, int ur) {
@@ -599,8 +602,17 @@ struct Engine final : EngineBase {
       };
       dH = fill(h->d_mv);
       dS = fill(h->d_nv);
-      opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH, sHS.off};
-      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS, sHS.off};
+      auto zflags = [&](const OV* v) {
+        uint8_t* z = dalloc<uint8_t>(h->N);
+        k_sell_zflags<OV><<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, sHS.lgSR, sHS.soff, sHS.len,
+                                                                                 v, z);
+        CKL();
+        return z;
+      };
+      zfH = zflags(dH);
+      zfS = zflags(dS);
+      opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH, sHS.off, zfH};
+      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS, sHS.off, zfS};
     }
   }
 

@@ -476,6 +476,19 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
 }
 
 // ================================================================ GMRES
+// acc - c_1*0 - c_2*0 - ... in the row's stored order, from the row's zflag
+// summary alone: coef*0 is +0, -0 (sign bit set) or NaN (coef not finite);
+// subtracting +-0 leaves a nonzero acc unchanged, turns -0 into +0 once any
+// -0 is subtracted, and a NaN term gives the canonical NaN. Bitwise the same
+// as the fold over x = 0 without reading the matrix.
+template <class C>
+__device__ __forceinline__ C zero_resid(C acc, int f) {
+  const C z = Ar<C>::zero();
+  if (f & 2) return Ar<C>::sub(acc, Ar<C>::mul(Ar<C>::from_d(INFINITY), z));
+  if (f & 1) return Ar<C>::sub(acc, Ar<C>::neg(z));
+  return acc;
+}
+
 // r = rhs - S x in the inner arithmetic (inner_solver.cpp:97 / :182, the
 // two-stage residual kernels.cpp:56-69; x_zero: the restart from x = 0,
 // folded over +0 without reading x), max|r| (for norm2), ||r||_2 (binary64),
@@ -495,7 +508,13 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
     C acc[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
-    fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
+    if constexpr (std::is_same<std::decay_t<decltype(src)>, ZeroSrc<T>>::value) {
+#pragma unroll
+      for (int i = 0; i < G; ++i)
+        if (GADI_LIVE(i)) acc[i] = zero_resid(acc[i], op.zflags(s.lo + i));
+    } else {
+      fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
+    }
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -540,6 +559,12 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   // quotient of p-bit numbers is either exact in p bits or at least 2^-2p-1
   // away from a p-bit rounding boundary, p <= 24); binary64 divides.
   const double rinv = __ddiv_rn(1.0, m);
+  // binary16 operands in binary32 arithmetic: Markstein's correction of the
+  // product with y = RN(1/m) (two FMAs) gives the correctly rounded quotient
+  // without binary64 work; checked exhaustively against RN(w/m) over all
+  // binary16 pairs 0 <= w <= m (tools/check_markstein.c).
+  constexpr bool MK = std::is_same<T, __half>::value && std::is_same<C, float>::value;
+  const float mf = (float)m, yf = MK ? __frcp_rn(mf) : 0.f;
   C w0;
   double w1;
   seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
@@ -549,8 +574,15 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       C qv;
-      if constexpr (std::is_same<C, double>::value) qv = div_c<C>(ld_c<T, C>(wv[i]), mc);
-      else qv = Ar<C>::from_d(__dmul_rn(to_dbl(wv[i]), rinv));
+      if constexpr (std::is_same<C, double>::value) {
+        qv = div_c<C>(ld_c<T, C>(wv[i]), mc);
+      } else if constexpr (MK) {
+        const float wf = __half2float(wv[i]);
+        const float q0 = __fmul_rn(wf, yf);
+        qv = __fmaf_rn(__fmaf_rn(-q0, mf, wf), yf, q0);
+      } else {
+        qv = Ar<C>::from_d(__dmul_rn(to_dbl(wv[i]), rinv));
+      }
       tc[i] = Ar<C>::mul(qv, qv);
     }
     c = seg_sum<C, G>(tc, s.len);

@@ -94,6 +94,15 @@ struct ScaleSrc {  // v = round(inv * w), inv in binary64 (scale, kernels.cpp:16
   __device__ __forceinline__ T at(int64_t e) const { return f(w[e]); }
 };
 
+// Sign/finiteness summary of one stored coefficient, for the residual from
+// x = 0: bit 0 = the sign bit is set (coef * +0 = -0), bit 1 = not finite
+// (coef * 0 = NaN). See zero_resid (gadi_kernels.cuh).
+template <class V>
+__device__ __forceinline__ int zflag(V c) {
+  const double d = to_dbl(c);
+  return (signbit(d) ? 1 : 0) | (isfinite(d) ? 0 : 2);
+}
+
 // 3D convection-diffusion 7-point operator, matrix free (problems.cpp:8-43):
 // row i*n^2 + j*n + k; c[] = {i-1, j-1, k-1, centre, k+1, j+1, i+1}, the
 // stored-column order. Boundary neighbours are absent (not zero-valued), as
@@ -163,6 +172,29 @@ struct Stencil7 {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc[v] = f(acc[v], c[6], nb[v]);
     }
+  }
+
+  // OR of zflag over the row's stored coefficients (the ones fold visits).
+  __device__ __forceinline__ int zflags(int64_t e) const {
+    int64_t k, j, i;
+    if (lg >= 0) {
+      k = e & (n - 1);
+      j = (e >> lg) & (n - 1);
+      i = e >> (2 * lg);
+    } else {
+      k = e % n;
+      const int64_t r = e / n;
+      j = r % n;
+      i = r / n;
+    }
+    int f = zflag(c[3]);
+    if (i > 0) f |= zflag(c[0]);
+    if (j > 0) f |= zflag(c[1]);
+    if (k > 0) f |= zflag(c[2]);
+    if (k + 1 < n) f |= zflag(c[4]);
+    if (j + 1 < n) f |= zflag(c[5]);
+    if (i + 1 < n) f |= zflag(c[6]);
+    return f;
   }
 };
 

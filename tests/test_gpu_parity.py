@@ -200,3 +200,117 @@ def test_band_generator_split_and_solve(orc, N, k, band):
     assert int(res.report.status) == wrep.status == 0
     assert res.report.outer_iters == wrep.outer_iters
     assert same(res.x, wx)
+
+
+@pytest.mark.parametrize("fmt", [HALF, SINGLE, DOUBLE])
+@pytest.mark.parametrize("method", [CG, GMRES])
+def test_band_krylov_bitwise(orc, fmt, method):
+    """SELL kernels with the shared-memory operand window (N = 2^13, band 300)
+    against the oracle's Krylov solvers; the right-hand side carries +-0 entries
+    so the GMRES residual from x = 0 exercises the zflag shortcut."""
+    N, k, band, alpha = 8192, 26, 300, 3.0
+    A = orc.band(N, k, band, 3)
+    H, Sm = orc.regularize(A, alpha)
+    rhs = orc.round(np.random.default_rng(fmt).uniform(-1, 1, N), fmt)
+    rhs[::7] = 0.0
+    rhs[3::7] = -0.0
+    stop = orc.norm2_64(rhs)
+    eps, max_inner, restart = 1e-8, 40, 12
+    s = g.CudaGadiSystem(g.build_band_csr(N, k, band, 3))
+    s.prepare(alpha, 1.0, g.Precision(fmt), g.InnerSolverSpec(g.InnerMethod(method), eps, max_inner, restart))
+    s.set_inner_stop_norm(stop)
+    x, it, st = s.solve_H(rhs) if method == CG else s.solve_S(rhs)
+    wx, wit, wst = orc.krylov(H if method == CG else Sm, rhs, method, eps, max_inner, restart, fmt, stop)
+    assert (it, int(st)) == (wit, wst)
+    assert same(x, wx)
+
+
+@pytest.mark.parametrize("n,fmt", [(8, HALF), (8, SINGLE), (5, DOUBLE), (16, HALF)])
+def test_gmres_zero_start_signed_zeros(orc, n, fmt):
+    """r = rhs - S*0 keeps -0 only in rows whose stored coefficients are all
+    sign-clear (the reference's fold; gadi_kernels.cuh zero_resid)."""
+    S, A = stencil_and_csr(orc, n)
+    alpha = 0.5
+    _, Sm = orc.regularize(A, alpha)
+    rhs = orc.round(np.random.default_rng(n + fmt).uniform(-1, 1, A.n), fmt)
+    rhs[::3] = -0.0
+    rhs[1::5] = 0.0
+    stop = orc.norm2_64(rhs)
+    sysx = g.CudaGadiSystem(S)
+    sysx.prepare(alpha, 1.0, g.Precision(fmt), g.InnerSolverSpec(g.InnerMethod.Gmres, 1e-6, 30, 7))
+    sysx.set_inner_stop_norm(stop)
+    x, it, st = sysx.solve_S(rhs)
+    wx, wit, wst = orc.krylov(Sm, rhs, GMRES, 1e-6, 30, 7, fmt, stop)
+    assert (it, int(st)) == (wit, wst)
+    assert same(x, wx)
+
+
+@pytest.mark.parametrize("sparse", [False, True])
+def test_gmres_overflowed_coefficients(orc, sparse):
+    """alpha beyond binary16 range: S's diagonal rounds to inf, the residual
+    from x = 0 is NaN in those rows, GMRES reports Overflow like the reference."""
+    n, alpha = 8, 1e5
+    S, A = stencil_and_csr(orc, n)
+    _, Sm = orc.regularize(A, alpha)
+    rhs = orc.round(np.random.default_rng(1).uniform(-1, 1, A.n), HALF)
+    stop = orc.norm2_64(rhs)
+    sysx = g.CudaGadiSystem(g.SparseMatrix(A.n, A.n, A.rp, A.ci, A.v) if sparse else S)
+    sysx.prepare(alpha, 1.0, g.Precision.Half, g.InnerSolverSpec(g.InnerMethod.Gmres, 1e-6, 30, 7))
+    sysx.set_inner_stop_norm(stop)
+    x, it, st = sysx.solve_S(rhs)
+    wx, wit, wst = orc.krylov(Sm, rhs, GMRES, 1e-6, 30, 7, HALF, stop)
+    assert (it, int(st)) == (wit, wst)
+    assert int(st) == 2  # Overflow
+    assert same(x, wx)
+
+
+@pytest.mark.parametrize("kind", ["stencil", "band"])
+def test_solve_accum_fp32_matches_oracle(orc, kind):
+    """binary16 storage with binary32 arithmetic (the C3/C4 inner mode,
+    GADI_ACCUM_FP32): whole solves bit for bit against the oracle."""
+    if kind == "stencil":
+        S, A = stencil_and_csr(orc, 16, r=0.5)
+        dev = S
+    else:
+        A = orc.band(4096, 26, 256, 5)
+        dev = g.build_band_csr(4096, 26, 256, 5)
+    _, b = orc.make_rhs(A, 1, -1.0, 1.0)
+    alpha = 0.4 if kind == "stencil" else 4.0
+    cfg = Config.make(alpha=alpha, xi=1e-20, u_r=HALF, method=CG, tol_epsilon=1e-12, max_inner_iters=5,
+                      stall_window=400, accum=1)
+    wx, wrep, _ = orc.solve(A, b, cfg)
+    res = g.gadi_ir_solve(dev, b, g.hss_split(dev), g.GadiConfig(
+        alpha=alpha, xi=1e-20, u_r=g.Precision.Half, accum=g.Accum.Fp32, stall_window=400,
+        inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30)))
+    assert int(res.report.status) == wrep.status
+    assert res.report.outer_iters == wrep.outer_iters
+    assert res.report.inner_iter_totals == wrep.inner_iter_totals
+    assert same(res.x, wx)
+
+
+@pytest.mark.parametrize("kind", ["stencil", "band"])
+@pytest.mark.parametrize("method", [CG, GMRES])
+def test_krylov_accum_fp32_bitwise(orc, kind, method):
+    """GADI_ACCUM_FP32 (binary16 storage, binary32 arithmetic): CG / GMRES bit
+    for bit against the oracle's restatement of that mode (af = SINGLE)."""
+    if kind == "stencil":
+        S, A = stencil_and_csr(orc, 16, r=0.3)
+        dev = S
+    else:
+        A = orc.band(8192, 26, 300, 4)
+        dev = g.build_band_csr(8192, 26, 300, 4)
+    alpha = 0.6 if kind == "stencil" else 3.0
+    H, Sm = orc.regularize(A, alpha)
+    rhs = orc.round(np.random.default_rng(11).uniform(-1, 1, A.n), HALF)
+    rhs[5::9] = -0.0
+    stop = orc.norm2_64(rhs)
+    eps, max_inner, restart = 1e-9, 40, 12
+    sysx = g.CudaGadiSystem(dev)
+    sysx.prepare(alpha, 1.0, g.Precision.Half, g.InnerSolverSpec(g.InnerMethod(method), eps, max_inner, restart),
+                 g.Accum.Fp32)
+    sysx.set_inner_stop_norm(stop)
+    x, it, st = sysx.solve_H(rhs) if method == CG else sysx.solve_S(rhs)
+    wx, wit, wst = orc.krylov(H if method == CG else Sm, rhs, method, eps, max_inner, restart, HALF, stop,
+                              af=SINGLE)
+    assert (it, int(st)) == (wit, wst)
+    assert same(x, wx)
