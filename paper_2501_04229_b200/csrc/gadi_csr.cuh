@@ -34,6 +34,13 @@ struct Sell {
   const uint8_t* __restrict__ zf = nullptr;  // per-row zflag summary (k_sell_zflags), when built
 
   __device__ __forceinline__ int zflags(int64_t row) const { return zf[row]; }
+  template <int VEC>
+  __device__ __forceinline__ void zflags_vec(int64_t e0, int (&f)[VEC]) const {
+    uint8_t z[VEC];
+    ld_vec<uint8_t, VEC>(zf, e0, z);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) f[v] = z[v];
+  }
 
   template <int VEC, class Src, class X, class Acc, class F>
   __device__ __forceinline__ void fold(const Src& x, int64_t e0, Acc (&acc)[VEC], F f, X (&cc)[VEC]) const {

@@ -157,31 +157,47 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   IL = std::min<int64_t>(IL, n);
   g.IL = (int)IL;
   g.nblk = (int)(g.njt * (n / IL));
-  // operand-ring kernels: 3 raw stages + a 3-plane ring; identity-operand
-  // kernels fold from the stages directly and need 4 of them
-  g.stages = ident ? 4 : 4;
-  if (const char* e = std::getenv("GADI_ST25_STAGES")) g.stages = std::max(2, std::atoi(e));  // tuning knob
+  // operand-ring kernels: raw stages + a 4-plane operand ring; identity-
+  // operand kernels fold from the stages directly and need 4 of them
+  g.stages = 4;
   const int64_t pe = (TJ + 2) * n;
   auto bytes = [&]() {
-    return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)3 * pe * ring_tsize);
+    return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)4 * pe * ring_tsize);
   };
-  g.smem = bytes();
-  while (g.stages > 2 && g.smem > 112 * 1024) {  // keep two CTAs per SM
-    --g.stages;
-    g.smem = bytes();
+  // stages in [2 (4 for identity operands), 4]: the most CTAs per SM (228 KB
+  // of shared memory, ~4 KB static + 1 KB reserved per CTA), then the most stages
+  auto ctas = [&]() { return (int)((228 * 1024) / (bytes() + 5 * 1024)); };
+  int best = g.stages, bc = ctas();
+  for (int st = g.stages - 1; st >= (ident ? 4 : 2); --st) {
+    g.stages = st;
+    if (ctas() > bc) {
+      bc = ctas();
+      best = st;
+    }
   }
+  g.stages = best;
+  if (const char* e = std::getenv("GADI_ST25_STAGES")) g.stages = std::max(2, std::atoi(e));  // tuning knob
+  g.smem = bytes();
   if (g.smem > 200 * 1024) return false;
   return true;
 }
 
-template <class P>
-inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+template <class P, int CPT>
+inline void launch_st25_cpt(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
   static bool attr = false;  // one attribute call per instantiation
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_st25<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_st25<P, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  k_st25<P><<<g.nblk, g.threads, g.smem, s>>>(pol, g, rd, st);
+  k_st25<P, CPT><<<g.nblk, g.threads, g.smem, s>>>(pol, g, rd, st);
+}
+template <class P>
+inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  switch (g.CPT) {  // chunks per thread per plane, a compile-time loop count
+    case 1: return launch_st25_cpt<P, 1>(pol, g, s, rd, st);
+    case 2: return launch_st25_cpt<P, 2>(pol, g, s, rd, st);
+    default: return launch_st25_cpt<P, 4>(pol, g, s, rd, st);
+  }
 }
 
 template <int V>
@@ -585,9 +601,15 @@ struct Engine final : EngineBase {
       opH.nn = opS.nn = h->n * h->n;
       opH.N = opS.N = h->N;
       opH.lg = opS.lg = lg_of(h->n);
+      auto zf = [&](double v) {  // zflag of the u_r-rounded coefficient (gadi_ops.cuh)
+        const double r = hround(v, u_r);
+        return (uint8_t)((std::signbit(r) ? 1 : 0) | (std::isfinite(r) ? 0 : 2));
+      };
       for (int k = 0; k < 7; ++k) {
         opH.c[k] = cval(Hc[k], u_r);
         opS.c[k] = cval(Sc[k], u_r);
+        opH.zc[k] = zf(Hc[k]);
+        opS.zc[k] = zf(Sc[k]);
       }
     } else {
       // SELL image of the union pattern with VA rows per lane, values of

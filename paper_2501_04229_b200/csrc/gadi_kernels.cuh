@@ -273,17 +273,19 @@ __device__ __forceinline__ SmemSrc<T> stage_window(const T* __restrict__ x, cons
 
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
-  // PACKED = false: ptxas (CUDA 12.9) contracts mul.rn.f32x2 + add.rn.f32x2
-  // into one FFMA2 (a single rounding) despite .rn and -fmad=false, which
-  // breaks the reference's two-rounding fold; the scalar path stays exact.
-  static constexpr bool PACKED = false, NEG = false;
+  // PACKED: binary32 folds may pair the products (FMUL2, fold_vec in
+  // gadi_st25.cuh) but keep the adds scalar: ptxas (CUDA 12.9) contracts
+  // mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 (a single rounding) despite
+  // .rn and -fmad=false, which would break the reference's two-rounding fold;
+  // FMUL2 + scalar FADD is never contracted (checked in the SASS).
+  static constexpr bool PACKED = std::is_same<C, float>::value, NEG = false;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::add(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <class C, class T>
 struct ResidF {  // acc - coef * x (kernels.cpp:63-66)
-  static constexpr bool PACKED = false, NEG = true;
+  static constexpr bool PACKED = std::is_same<C, float>::value, NEG = true;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
     return Ar<C>::sub(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
@@ -509,9 +511,16 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
 #pragma unroll
     for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
     if constexpr (std::is_same<std::decay_t<decltype(src)>, ZeroSrc<T>>::value) {
+      if constexpr (VEC > 1) {
+        int fl[VEC];
+        op.template zflags_vec<VEC>(s.lo, fl);
 #pragma unroll
-      for (int i = 0; i < G; ++i)
-        if (GADI_LIVE(i)) acc[i] = zero_resid(acc[i], op.zflags(s.lo + i));
+        for (int i = 0; i < G; ++i) acc[i] = zero_resid(acc[i], fl[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+          if (GADI_LIVE(i)) acc[i] = zero_resid(acc[i], op.zflags(s.lo + i));
+      }
     } else {
       fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
     }

@@ -113,6 +113,7 @@ struct Stencil7 {
   int64_t n, nn, N;
   V c[7];
   int lg;  // log2(n) when n is a power of two (always on the aligned path), else -1
+  uint8_t zc[7];  // zflag of each coefficient (set by the engine; see zflags)
 
   // Fold for the VEC consecutive elements e0..e0+VEC-1 of one grid row
   // (aligned path: e0 % VEC == 0 and n % VEC == 0; VEC == 1 is any element).
@@ -187,14 +188,39 @@ struct Stencil7 {
       j = r % n;
       i = r / n;
     }
-    int f = zflag(c[3]);
-    if (i > 0) f |= zflag(c[0]);
-    if (j > 0) f |= zflag(c[1]);
-    if (k > 0) f |= zflag(c[2]);
-    if (k + 1 < n) f |= zflag(c[4]);
-    if (j + 1 < n) f |= zflag(c[5]);
-    if (i + 1 < n) f |= zflag(c[6]);
+    int f = zc[3];
+    if (i > 0) f |= zc[0];
+    if (j > 0) f |= zc[1];
+    if (k > 0) f |= zc[2];
+    if (k + 1 < n) f |= zc[4];
+    if (j + 1 < n) f |= zc[5];
+    if (i + 1 < n) f |= zc[6];
     return f;
+  }
+  // the same for the VEC points e0.. of one grid row (aligned path)
+  template <int VEC>
+  __device__ __forceinline__ void zflags_vec(int64_t e0, int (&f)[VEC]) const {
+    int64_t k0, j, i;
+    if (lg >= 0) {
+      k0 = e0 & (n - 1);
+      j = (e0 >> lg) & (n - 1);
+      i = e0 >> (2 * lg);
+    } else {
+      k0 = e0 % n;
+      const int64_t r = e0 / n;
+      j = r % n;
+      i = r / n;
+    }
+    int b = zc[3];
+    if (i > 0) b |= zc[0];
+    if (j > 0) b |= zc[1];
+    if (j + 1 < n) b |= zc[5];
+    if (i + 1 < n) b |= zc[6];
+    const int mid = b | zc[2] | zc[4];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) f[v] = mid;
+    f[0] = b | (k0 > 0 ? zc[2] : 0) | (VEC > 1 || k0 + 1 < n ? zc[4] : 0);
+    if (VEC > 1) f[VEC - 1] = b | zc[2] | (k0 + VEC < n ? zc[4] : 0);
   }
 };
 

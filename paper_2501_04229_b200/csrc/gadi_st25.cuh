@@ -97,21 +97,20 @@ __device__ __forceinline__ void sts_vec(R* p, const R (&v)[VEC]) {
 }
 
 // acc[v] = f(acc[v], coef, x[v]) for all v, except v = 0 / v = VEC-1 when the
-// neighbour is absent (skip0 / skipL). binary32 matvec / residual folds use
-// the paired FADD2/FMUL2 (one RN rounding per lane, the same values as the
-// scalar __fadd_rn/__fmul_rn; a - c*x == a + (-c)*x exactly in IEEE).
+// neighbour is absent (skip0 / skipL). binary32 matvec / residual folds pair
+// the products (FMUL2: one RN rounding per lane, the same values as scalar
+// __fmul_rn) and keep the adds scalar (see MatvecF::PACKED).
 template <class F, class A, class X, int VEC>
 __device__ __forceinline__ void fold_vec(const F& f, A (&acc)[VEC], A coef, const X (&x)[VEC], bool skip0,
                                          bool skipL) {
   const A a0 = acc[0], aL = acc[VEC - 1];
-  if constexpr (std::is_same<A, float>::value && std::is_same<X, float>::value && (VEC % 2 == 0) && F::PACKED) {
-    const float cf = F::NEG ? -coef : coef;
-    const float2 c2 = make_float2(cf, cf);
+  if constexpr (std::is_same<A, float>::value && (VEC % 2 == 0) && F::PACKED) {
+    const float2 c2 = make_float2(coef, coef);
 #pragma unroll
     for (int v = 0; v < VEC; v += 2) {
-      const float2 r = __fadd2_rn(make_float2(acc[v], acc[v + 1]), __fmul2_rn(c2, make_float2(x[v], x[v + 1])));
-      acc[v] = r.x;
-      acc[v + 1] = r.y;
+      const float2 pr = __fmul2_rn(c2, make_float2(ld_c<X, float>(x[v]), ld_c<X, float>(x[v + 1])));
+      acc[v] = F::NEG ? __fsub_rn(acc[v], pr.x) : __fadd_rn(acc[v], pr.x);
+      acc[v + 1] = F::NEG ? __fsub_rn(acc[v + 1], pr.y) : __fadd_rn(acc[v + 1], pr.y);
     }
   } else {
 #pragma unroll
@@ -119,6 +118,23 @@ __device__ __forceinline__ void fold_vec(const F& f, A (&acc)[VEC], A coef, cons
   }
   if (skip0) acc[0] = a0;
   if (skipL) acc[VEC - 1] = aL;
+}
+
+// out[v] = a * x[v] rounded in C; binary32 pairs the products (FMUL2).
+template <class C, class X, int VEC>
+__device__ __forceinline__ void mul_vec(C a, const X (&x)[VEC], C (&out)[VEC]) {
+  if constexpr (std::is_same<C, float>::value && VEC % 2 == 0) {
+    const float2 a2 = make_float2(a, a);
+#pragma unroll
+    for (int v = 0; v < VEC; v += 2) {
+      const float2 pr = __fmul2_rn(a2, make_float2(ld_c<X, float>(x[v]), ld_c<X, float>(x[v + 1])));
+      out[v] = pr.x;
+      out[v + 1] = pr.y;
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) out[v] = Ar<C>::mul(a, ld_c<X, C>(x[v]));
+  }
 }
 
 struct St25Geo {
@@ -136,9 +152,10 @@ struct St25Geo {
 };
 
 constexpr int ST25_CPT_MAX = 4;
+constexpr int ST25_IL_MAX = 32;  // planes per CTA (make_st25)
 
 // ------------------------------------------------------------ the kernel
-template <class P>
+template <class P, int CPT>
 __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd, DevState* st) {
   using T = typename P::T;
   using Acc = typename P::Acc;
@@ -161,6 +178,10 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   __shared__ double redb1[32];
   __shared__ int s_last;
   R0* red0 = reinterpret_cast<R0*>(redb0);
+  // per-(plane, warp) partial sums, folded over the warps once after the
+  // plane loop (no block barrier per plane for the reductions)
+  static_assert(!(P::HAS_R0 && P::HAS_R1), "one reduced quantity per policy");
+  __shared__ double plb[ST25_IL_MAX * 8];  // R0 values are held exactly in binary64
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int jt = blockIdx.x % g.njt, ic = blockIdx.x / g.njt;
@@ -185,12 +206,14 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   if (tid == 0)
     for (int q = qlo; q <= qhi && q < qlo + S; ++q) issue(q);
 
-  // operand of plane q (all staged rows) into ring slot q % 3
+  // operand of plane q (all staged rows) into ring slot q % 4: building
+  // plane i+1 overwrites plane i-3, last read by the fold of plane i-2, which
+  // precedes the barrier after building plane i; one barrier per plane.
   auto build = [&](int q) {
     const int s = (q - qlo) % S;
     mbar_wait(&bar[s], (uint32_t)(((q - qlo) / S) & 1));
     const T* rs = raw + (size_t)s * P::NIN * pe;
-    RT* o = opr + (size_t)(q % 3) * pe;
+    RT* o = opr + (size_t)(q & 3) * pe;
     const int nch = (rhi - rlo + 1) << g.lgTR;
     for (int c = tid; c < nch; c += blockDim.x) {
       const int idx = soff + c * VEC;
@@ -225,26 +248,24 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   // those loads are issued one plane ahead so their latency hides behind a
   // plane of folding
   auto chunk_e0 = [&](int ii, int rr) -> int64_t {
-    const int c = ((warp * g.CPT + rr) << 5) + lane;
+    const int c = ((warp * CPT + rr) << 5) + lane;
     return (int64_t)ii * g.nn + (int64_t)(j0 + (c >> g.lgTR)) * n + (c & (g.TR - 1)) * VEC;
   };
-  Acc nxt[ST25_CPT_MAX][VEC];
+  Acc nxt[CPT][VEC];
   if constexpr (P::IDENT) {
 #pragma unroll
-    for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
-      if (rr < g.CPT) pol.init(chunk_e0(ib, rr), nxt[rr]);
+    for (int rr = 0; rr < CPT; ++rr) pol.init(chunk_e0(ib, rr), nxt[rr]);
   }
   for (int i = ib; i < ie; ++i) {
-    Acc cur[ST25_CPT_MAX][VEC];
+    Acc cur[CPT][VEC];
     if constexpr (P::IDENT) {
 #pragma unroll
-      for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
+      for (int rr = 0; rr < CPT; ++rr)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) cur[rr][v] = nxt[rr][v];
       if (i + 1 < ie) {
 #pragma unroll
-        for (int rr = 0; rr < ST25_CPT_MAX; ++rr)
-          if (rr < g.CPT) pol.init(chunk_e0(i + 1, rr), nxt[rr]);
+        for (int rr = 0; rr < CPT; ++rr) pol.init(chunk_e0(i + 1, rr), nxt[rr]);
       }
     }
     const RT *om, *oc, *op;
@@ -260,16 +281,16 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
         fence_proxy_async();
         issue(i + 1 + S);
       }
-      om = i > 0 ? opr + (size_t)((i - 1) % 3) * pe : nullptr;
-      oc = opr + (size_t)(i % 3) * pe;
-      op = i < n - 1 ? opr + (size_t)((i + 1) % 3) * pe : nullptr;
+      om = i > 0 ? opr + (size_t)((i - 1) & 3) * pe : nullptr;
+      oc = opr + (size_t)(i & 3) * pe;
+      op = i < n - 1 ? opr + (size_t)((i + 1) & 3) * pe : nullptr;
     }
-    R0 a0[ST25_CPT_MAX];
-    double a1[ST25_CPT_MAX];
+    R0 a0[CPT];
+    double a1[CPT];
 #pragma unroll
-    for (int rr = 0; rr < ST25_CPT_MAX; ++rr) {
-      if (rr < g.CPT) {
-        const int c = ((warp * g.CPT + rr) << 5) + lane;  // chunk of the tile, row major
+    for (int rr = 0; rr < CPT; ++rr) {
+      {
+        const int c = ((warp * CPT + rr) << 5) + lane;  // chunk of the tile, row major
         const int jl = c >> g.lgTR, k0 = (c & (g.TR - 1)) * VEC;
         const int j = j0 + jl;
         const int sidx = (jl + 1) * n + k0;
@@ -324,40 +345,50 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
     }
     // tree over this warp's CPT contiguous 32-chunk blocks, then over warps
 #pragma unroll
-    for (int s2 = 1; s2 < ST25_CPT_MAX; s2 <<= 1)
+    for (int s2 = 1; s2 < CPT; s2 <<= 1)
 #pragma unroll
-      for (int rr = 0; rr + s2 < ST25_CPT_MAX; rr += 2 * s2)
-        if (rr + s2 < g.CPT) {
+      for (int rr = 0; rr + s2 < CPT; rr += 2 * s2) {
           if (P::HAS_R0) a0[rr] = Ar<R0>::add(a0[rr], a0[rr + s2]);
           if (P::HAS_R1) a1[rr] = __dadd_rn(a1[rr], a1[rr + s2]);
         }
-    if (P::HAS_R0 || P::HAS_R1) {
-      if (lane == 0) {
-        if (P::HAS_R0) red0[warp] = a0[0];
-        if (P::HAS_R1) redb1[warp] = a1[0];
-      }
-      __syncthreads();
-      if (warp == 0) {
-        R0 v0 = lane < nw ? red0[lane] : Ar<R0>::zero();
-        double v1 = lane < nw ? redb1[lane] : 0.0;
-        if (lane < nw) {
-          if (P::HAS_R0) v0 = warp_tree(v0, nw);
-          if (P::HAS_R1) v1 = warp_tree(v1, nw);
-        }
-        if (lane == 0) {
-          const int64_t slot = (int64_t)i * g.njt + jt;
-          if (P::HAS_R0) rd.part0[slot] = to_dbl(v0);
-          if (P::HAS_R1) rd.part1[slot] = v1;
-        }
-      }
+    if (lane == 0) {
+      if (P::HAS_R0) plb[(i - ib) * nw + warp] = to_dbl(a0[0]);
+      if (P::HAS_R1) plb[(i - ib) * nw + warp] = a1[0];
     }
-    __syncthreads();  // ring slot (i+2)%3 is rebuilt next iteration
-    if constexpr (P::IDENT) {  // plane i-1 is no longer read: refill its stage
+    if constexpr (P::IDENT) {
+      __syncthreads();  // plane i-1 is no longer read: refill its stage
       if (tid == 0 && i - 1 >= qlo && i - 1 + S <= qhi) {
         fence_proxy_async();
         issue(i - 1 + S);
       }
     }
+  }
+  // each plane's warp partials -> one pairwise subtree (the same shape as a
+  // warp butterfly over nw contiguous warps) -> partials[plane * njt + tile]
+  if (P::HAS_R0 || P::HAS_R1) {
+    __syncthreads();
+    for (int t = tid; t < g.IL; t += blockDim.x) {
+      R0 v0[8];
+      double v1[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < nw) {
+          if (P::HAS_R0) v0[k] = from_dbl<R0>(plb[t * nw + k]);
+          if (P::HAS_R1) v1[k] = plb[t * nw + k];
+        }
+#pragma unroll
+      for (int s2 = 1; s2 < 8; s2 <<= 1)
+#pragma unroll
+        for (int k = 0; k + s2 < 8; k += 2 * s2)
+          if (k + s2 < nw) {
+            if (P::HAS_R0) v0[k] = Ar<R0>::add(v0[k], v0[k + s2]);
+            if (P::HAS_R1) v1[k] = __dadd_rn(v1[k], v1[k + s2]);
+          }
+      const int64_t slot = (int64_t)(ib + t) * g.njt + jt;
+      if (P::HAS_R0) rd.part0[slot] = to_dbl(v0[0]);
+      if (P::HAS_R1) rd.part1[slot] = v1[0];
+    }
+    __threadfence();
   }
 
   // max / flags, then the grid ticket; the last CTA folds the partials
@@ -439,9 +470,10 @@ struct PolSpmvp {
     } else {
       T pv[ST25_VEC];
       lds16<T, ST25_VEC>(rs + pe + idx, pv);
+      C bp[ST25_VEC];
+      mul_vec<C, T, ST25_VEC>(beta, pv, bp);
 #pragma unroll
-      for (int e = 0; e < ST25_VEC; ++e)
-        v[e] = ld_c<T, RT>(st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[e]), Ar<C>::mul(beta, ld_c<T, C>(pv[e])))));
+      for (int e = 0; e < ST25_VEC; ++e) v[e] = ld_c<T, RT>(st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[e]), bp[e])));
     }
   }
   __device__ MatvecF<C, RT> fold() const { return MatvecF<C, RT>(); }
