@@ -263,15 +263,38 @@ __device__ __forceinline__ C block_tree(C v, int count, C* sm) {
   return v;
 }
 
-// Exact pairwise sum of L (power of 2) contiguous values by a binary-counter
-// stack (merges equal-size subtrees as soon as they close).
+// Exact pairwise sum of L (power of 2) contiguous values. The loads go out
+// in batches of up to 16 (all in flight at once: the values are L2-resident
+// partials, and a load-add-load chain would cost one L2 latency per value);
+// each batch is a perfect subtree, and a binary-counter stack merges the
+// batch sums as equal-size subtrees close, so the shape is the pairwise tree.
 template <class C, class Load>
 __device__ __forceinline__ C run_pairwise(int64_t L, Load load) {
+  constexpr int B = 16;
+  if (L < B) {
+    C v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k)
+      if (k < L) v[k] = load(k);
+#pragma unroll
+    for (int st = 1; st < B; st <<= 1)
+#pragma unroll
+      for (int k = 0; k + st < B; k += 2 * st)
+        if (k + st < L) v[k] = Ar<C>::add(v[k], v[k + st]);
+    return v[0];
+  }
   C stk[40];
   int sp = 0;
-  for (int64_t j = 0; j < L; ++j) {
-    stk[sp++] = load(j);
-    for (int64_t k = j + 1; (k & 1) == 0; k >>= 1) {
+  for (int64_t j = 0; j < L; j += B) {
+    C v[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) v[k] = load(j + k);
+#pragma unroll
+    for (int st = 1; st < B; st <<= 1)
+#pragma unroll
+      for (int k = 0; k + st < B; k += 2 * st) v[k] = Ar<C>::add(v[k], v[k + st]);
+    stk[sp++] = v[0];
+    for (int64_t q = j / B + 1; (q & 1) == 0; q >>= 1) {
       stk[sp - 2] = Ar<C>::add(stk[sp - 2], stk[sp - 1]);
       --sp;
     }

@@ -106,6 +106,50 @@ __device__ __forceinline__ void seg_run(const Geo& g, Body&& body, C0& w0, doubl
   w1 = R1 ? a1[0] : 0.0;
 }
 
+// seg_run over one input stream whose R segment loads are all issued before
+// any of them is consumed (memory-level parallelism for single-stream
+// reductions); body(seg, v, c, d) gets the segment's G values.
+template <int VEC, bool R0, bool R1, int G, class T, class C0, class Body>
+__device__ __forceinline__ void seg_run_ld(const Geo& g, const T* __restrict__ p, Body&& body, C0& w0, double& w1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  T v[RMAX][G];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r)
+    if (r < g.R) {
+      const int64_t t = (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane;
+      if constexpr (VEC > 1) {
+        ld_vec<T, VEC>(p, t * VEC, v[r]);
+      } else {
+        const Seg s = seg_of<VEC>(t, g.N, g.D);
+#pragma unroll
+        for (int i = 0; i < G; ++i) v[r][i] = i < s.len ? p[s.lo + i] : from_dbl<T>(0.0);
+      }
+    }
+  C0 a0[RMAX];
+  double a1[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r < g.R) {
+      const int64_t t = (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane;
+      C0 c = Ar<C0>::zero();
+      double d = 0.0;
+      body(seg_of<VEC>(t, g.N, g.D), v[r], c, d);
+      if (R0) a0[r] = warp_tree(c, g.L);
+      if (R1) a1[r] = warp_tree(d, g.L);
+    }
+  }
+#pragma unroll
+  for (int st = 1; st < RMAX; st <<= 1)
+#pragma unroll
+    for (int r = 0; r + st < RMAX; r += 2 * st)
+      if (r + st < g.R) {
+        if (R0) a0[r] = Ar<C0>::add(a0[r], a0[r + st]);
+        if (R1) a1[r] = __dadd_rn(a1[r], a1[r + st]);
+      }
+  w0 = R0 ? a0[0] : Ar<C0>::zero();
+  w1 = R1 ? a1[0] : 0.0;
+}
+
 // Elementwise loop over this lane's segments (no reduction).
 template <int VEC, class Body>
 __device__ __forceinline__ void seg_each(const Geo& g, Body&& body) {
@@ -316,9 +360,7 @@ __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int ma
   GADI_G;
   C w0;
   double w1;
-  seg_run<VEC, true, true>(g, [&](const Seg& s, C& c, double& d) {
-    T v[G];
-    load_seg<T, VEC, G>(r, s, v);
+  seg_run_ld<VEC, true, true, G>(g, r, [&](const Seg& s, const T (&v)[G], C& c, double& d) {
     C tc[G];
     double td[G];
 #pragma unroll
@@ -504,26 +546,8 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
   double m = 0.0;
   C w0;
   double w1;
-  auto body = [&](const Seg& s, double& d, const auto& src) {
-    T bv[G], xc[G], rv[G];
-    load_seg<T, VEC, G>(rhs, s, bv);
-    C acc[G];
-#pragma unroll
-    for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
-    if constexpr (std::is_same<std::decay_t<decltype(src)>, ZeroSrc<T>>::value) {
-      if constexpr (VEC > 1) {
-        int fl[VEC];
-        op.template zflags_vec<VEC>(s.lo, fl);
-#pragma unroll
-        for (int i = 0; i < G; ++i) acc[i] = zero_resid(acc[i], fl[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < G; ++i)
-          if (GADI_LIVE(i)) acc[i] = zero_resid(acc[i], op.zflags(s.lo + i));
-      }
-    } else {
-      fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
-    }
+  auto fin = [&](const Seg& s, double& d, const C (&acc)[G]) {
+    T rv[G];
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
@@ -538,9 +562,30 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
     store_seg<T, VEC, G>(r, s, rv);
     d = seg_sum<double, G>(td, s.len);
   };
-  if (x_zero) {
-    const ZeroSrc<T> src{};
-    seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
+  auto body = [&](const Seg& s, double& d, const auto& src) {
+    T bv[G], xc[G];
+    load_seg<T, VEC, G>(rhs, s, bv);
+    C acc[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) acc[i] = ld_c<T, C>(bv[i]);
+    fold_seg<VEC, G>(op, src, s, acc, ResidF<C, T>(), xc);
+    fin(s, d, acc);
+  };
+  if (x_zero) {  // from x = 0: the per-row zflag summaries, the matrix is not read
+    seg_run_ld<VEC, false, true, G>(g, rhs, [&](const Seg& s, const T (&bv)[G], C&, double& d) {
+      C acc[G];
+      if constexpr (VEC > 1) {
+        int fl[VEC];
+        op.template zflags_vec<VEC>(s.lo, fl);
+#pragma unroll
+        for (int i = 0; i < G; ++i) acc[i] = zero_resid(ld_c<T, C>(bv[i]), fl[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i)
+          acc[i] = GADI_LIVE(i) ? zero_resid(ld_c<T, C>(bv[i]), op.zflags(s.lo + i)) : ld_c<T, C>(bv[i]);
+      }
+      fin(s, d, acc);
+    }, w0, w1);
   } else if (VEC > 1 && wband > 0) {
     const SmemSrc<T> src = stage_window<T, VEC>(x, g, wband);
     seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
@@ -576,9 +621,7 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   const float mf = (float)m, yf = MK ? __frcp_rn(mf) : 0.f;
   C w0;
   double w1;
-  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
-    T wv[G];
-    load_seg<T, VEC, G>(w, s, wv);
+  seg_run_ld<VEC, true, false, G>(g, w, [&](const Seg& s, const T (&wv)[G], C& c, double&) {
     C tc[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
