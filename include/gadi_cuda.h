@@ -232,6 +232,38 @@ int gadi_cuda_norm2(int32_t device, int32_t p, const double* x, int64_t n, doubl
 int gadi_cuda_make_rhs(gadi_handle* h, uint64_t seed, double lo, double hi, double* d_xtrue,
                        double* d_b);
 
+/* ---- sharded solves: z-slabs over several devices (the
+ * reference has no distributed path -- this extends gadi_ir_solve,
+ * solver.hpp:97-98, to a slab-partitioned stencil) ----
+ * Rank r of `world` (a power of two dividing n) owns planes
+ * [r n/world, (r+1) n/world) of the n^3 grid: rows [r N/world, (r+1) N/world).
+ * Every dot / norm is a collective whose result is the single-device value
+ * bit for bit (each slab is an aligned subtree of the pairwise sum; the slab
+ * partials are folded in rank order), and every rank takes the same
+ * control-flow decisions. A shard's vectors (b, x0, x, make_rhs) are its
+ * N/world rows; gadi_cuda_dim returns that count. A group must outlive its
+ * handles. */
+typedef struct gadi_group gadi_group;
+/* ranks = threads of this process (one or several devices): gadi_cuda_solve_group */
+int gadi_group_local(int32_t world, gadi_group** out);
+/* one rank per process over NCCL: every process passes the same 128-byte id
+ * (from gadi_nccl_unique_id on one rank, broadcast by the caller) and then
+ * calls gadi_cuda_solve / gadi_cuda_solve_device on its shard collectively */
+int gadi_nccl_unique_id(uint8_t* out128);
+int gadi_group_nccl(int32_t world, int32_t rank, const uint8_t* id128, gadi_group** out);
+int gadi_group_destroy(gadi_group* g);
+/* the shard of `rank` (GADI_PROBLEM_STENCIL7 only) */
+int gadi_cuda_create_shard(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_group* g,
+                           int32_t rank, gadi_handle** out);
+/* first global row and row count of a handle's shard (0, dim when unsharded) */
+int gadi_cuda_shard_range(const gadi_handle* h, int64_t* first_row, int64_t* n_rows);
+/* a local group's sharded solve: one host thread per rank, hs[r] = rank r;
+ * device buffers per rank (d_x0 may be NULL); one report per rank (identical
+ * status, iteration counts and history on every rank) */
+int gadi_cuda_solve_group(gadi_handle* const* hs, int32_t world, const gadi_config* cfg,
+                          const double* const* d_b, const double* const* d_x0, double* const* d_x,
+                          gadi_report* reps);
+
 /* ---- GPR alpha predictor (gpr.hpp:60-87; fit gpr.cpp:109-149,
  * predict_alpha gpr.cpp:151-169) ---- */
 typedef struct {

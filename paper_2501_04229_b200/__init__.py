@@ -35,7 +35,8 @@ __all__ = [
     "Precision", "InnerMethod", "SolveStatus", "InnerStatus", "Accum", "InnerSolverSpec", "GadiConfig",
     "SolveReport", "GadiResult", "SparseMatrix", "Stencil7", "Splitting", "build_convdiff3d",
     "hss_split", "gadi_ir_solve", "CudaGadiSystem", "GadiError", "ContractViolation", "ParameterError",
-    "UnsupportedError", "FitError", "default_xi", "lib", "gpr_fit",
+    "UnsupportedError", "FitError", "default_xi", "lib", "gpr_fit", "ShardGroup", "ShardSystem", "solve_group",
+    "nccl_unique_id",
 ]
 
 
@@ -183,6 +184,16 @@ def lib():
     L.gadi_cuda_launch_count.argtypes = [C.c_void_p]
     L.gadi_cuda_launch_count.restype = C.c_int64
     L.gadi_cuda_nnz.argtypes = [C.c_void_p, _i64p, _i64p]
+    L.gadi_group_local.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
+    L.gadi_nccl_unique_id.argtypes = [C.c_char_p]
+    L.gadi_group_nccl.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.gadi_group_destroy.argtypes = [C.c_void_p]
+    L.gadi_cuda_create_shard.argtypes = [C.POINTER(_Problem), C.POINTER(_DevOpts), C.c_void_p, C.c_int32,
+                                         C.POINTER(C.c_void_p)]
+    L.gadi_cuda_shard_range.argtypes = [C.c_void_p, _i64p, _i64p]
+    L.gadi_cuda_solve_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(_Config),
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+                                        C.POINTER(_Report)]
     _lib = L
     return L
 
@@ -460,6 +471,73 @@ class CudaGadiSystem:
                            rep.inner_iter_totals, rep.inner_stagnations, rep.h_iters, rep.s_iters,
                            rep.solve_ms, rep.h_ms, rep.s_ms, rep.h2d_bytes, rep.d2h_bytes, rep.outer_ms,
                            rep.e2e_ms, rep.launches)
+
+
+class ShardGroup:
+    """A sharded (z-slab) solve's communicator, SURVEY §8(e) (include/gadi_cuda.h).
+
+    ShardGroup.local(world): the ranks are threads of this process (one or
+    several devices; solve them together with solve_group).
+    ShardGroup.nccl(world, rank, uid): one rank per process over NCCL; every
+    process passes the same 128-byte id (nccl_unique_id() on one rank,
+    broadcast by the caller) and solves its shard collectively.
+    """
+
+    def __init__(self, ptr, world):
+        self._g, self.world = ptr, world
+
+    @classmethod
+    def local(cls, world: int) -> "ShardGroup":
+        g = C.c_void_p()
+        _check(lib().gadi_group_local(world, C.byref(g)))
+        return cls(g, world)
+
+    @classmethod
+    def nccl(cls, world: int, rank: int, uid: bytes) -> "ShardGroup":
+        if len(uid) != 128:
+            raise ContractViolation("nccl id must be 128 bytes")
+        g = C.c_void_p()
+        _check(lib().gadi_group_nccl(world, rank, uid, C.byref(g)))
+        return cls(g, world)
+
+    def close(self):
+        if self._g:
+            lib().gadi_group_destroy(self._g)
+            self._g = C.c_void_p()
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().gadi_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ShardSystem(CudaGadiSystem):
+    """One rank's z-slab of a 7-point stencil problem (gadi_cuda_create_shard).
+    Vectors are the shard's rows [first_row, first_row + n)."""
+
+    def __init__(self, A: "Stencil7", group: ShardGroup, rank: int, device: int = 0):
+        L = lib()
+        self._h = C.c_void_p()
+        self._A, self.group, self.rank = A, group, rank
+        desc = A._desc()
+        _check(L.gadi_cuda_create_shard(C.byref(desc), C.byref(_DevOpts(device)), group._g, rank,
+                                        C.byref(self._h)))
+        first, n = C.c_int64(), C.c_int64()
+        _check(L.gadi_cuda_shard_range(self._h, C.byref(first), C.byref(n)))
+        self.first_row, self.n = first.value, n.value
+
+
+def solve_group(shards, cfg: GadiConfig, d_b, d_x, d_x0=None):
+    """A local group's sharded solve (gadi_cuda_solve_group): shards[r] is
+    rank r; d_b / d_x / d_x0 are per-rank device pointers. One report per rank."""
+    w = len(shards)
+    hs = (C.c_void_p * w)(*[s_._h for s_ in shards])
+    arr = lambda ptrs: (C.c_void_p * w)(*[C.c_void_p(p) for p in ptrs])
+    reps = (_Report * w)()
+    _check(lib().gadi_cuda_solve_group(hs, w, C.byref(cfg._c()), arr(d_b), None if d_x0 is None else arr(d_x0),
+                                       arr(d_x), reps))
+    return [sh._report(reps[r]) for r, sh in enumerate(shards)]
 
 
 def gadi_ir_solve(A, b, split: Splitting, cfg: GadiConfig, x0=None, device: int = 0) -> GadiResult:

@@ -1,4 +1,6 @@
 // gadi_api.cu — run_gadi_ir on the device and the C ABI (include/gadi_cuda.h).
+#include <thread>
+
 #include "gadi_host.cuh"
 
 using namespace gadi_host;
@@ -310,14 +312,26 @@ const char* gadi_status_name(int32_t s) {
 const char* gadi_last_error(void) { return g_last_error.c_str(); }
 int32_t gadi_abi_version(void) { return GADI_ABI_VERSION; }
 
-int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_handle** out) {
-  API_BEGIN
-  if (!d || !out) throw Err(GADI_E_CONTRACT, "gadi_cuda_create: null argument");
-  *out = nullptr;
+// One device's part of a problem: the whole problem (grp == nullptr) or the
+// z-slab `rank` of a sharded stencil solve over grp (gadi_dist.cuh).
+static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_group* grp,
+                                int rank) {
+  if (!d) throw Err(GADI_E_CONTRACT, "gadi_cuda_create: null argument");
   std::unique_ptr<gadi_handle> h(new gadi_handle());
   h->device = opts ? opts->device : 0;
   CK(cudaSetDevice(h->device));
   h->kind = d->kind;
+  if (grp) {
+    const int w = grp->world;
+    if (d->kind != GADI_PROBLEM_STENCIL7)
+      throw Err(GADI_E_UNSUPPORTED, "sharded solves: z-slabs of the 7-point stencil only (CSR row blocks: next)");
+    if (w < 1 || w > GADI_MAX_RANKS || (w & (w - 1)) != 0)
+      throw Err(GADI_E_PARAM, "sharded solves: world must be a power of two <= 64");
+    if (rank < 0 || rank >= w) throw Err(GADI_E_PARAM, "sharded solves: rank out of range");
+    if (d->n % w != 0) throw Err(GADI_E_PARAM, "sharded solves: world must divide n");
+    if (grp->nccl_rank >= 0 && grp->nccl_rank != rank)
+      throw Err(GADI_E_PARAM, "sharded solves: an NCCL group holds this process's rank only");
+  }
   if (d->kind == GADI_PROBLEM_STENCIL7) {
     if (d->n < 2) throw Err(GADI_E_CONTRACT, "convdiff3d: n >= 2 required");  // problems.cpp:10
     h->n = d->n;
@@ -325,6 +339,21 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
     h->t1 = d->t1;
     h->t2 = d->t2;
     h->t3 = d->t3;
+    h->i0 = 0;
+    h->i1 = d->n;
+    if (grp) {
+      const int64_t np = d->n / grp->world;
+      h->world = grp->world;
+      h->rank = rank;
+      h->i0 = rank * np;
+      h->i1 = h->i0 + np;
+      h->N = d->n * d->n * np;
+      h->gh = d->n * d->n;
+      if (grp->local)
+        h->comm.reset(new LocalComm(grp->local.get(), rank));
+      else
+        h->comm.reset(new NcclComm(grp->world, rank, grp->id));
+    }
   } else if (d->kind == GADI_PROBLEM_CSR) {
     const int64_t n = d->n_rows;
     if (n < 1 || !d->row_ptr || !d->col_idx || !d->values) throw Err(GADI_E_CONTRACT, "csr: bad arguments");
@@ -374,13 +403,16 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   if (!h->stencil()) device_split(h.get());
   const int64_t N = h->N;
-  h->d_x = dalloc<double>(N);
-  h->d_b = dalloc<double>(N);
-  h->d_s = dalloc<double>(N);
-  h->d_t64 = dalloc<double>(N);
-  CK(cudaMemset(h->d_b, 0, N * 8));
+  h->d_x = hvec<double>(h.get());
+  h->d_b = hvec<double>(h.get());
+  h->d_s = hvec<double>(h.get());
+  h->d_t64 = hvec<double>(h.get());
   h->st = dalloc<DevState>(1);
   CK(cudaMemset(h->st, 0, sizeof(DevState)));
+  if (h->sharded()) {
+    const int one = 1;
+    CK(cudaMemcpy(&h->st->dist, &one, sizeof(int), cudaMemcpyHostToDevice));
+  }
   CK(cudaHostAlloc(&h->h_st, sizeof(DevState), cudaHostAllocDefault));
   std::memset(h->h_st, 0, sizeof(DevState));
   const int64_t maxblk = std::max<int64_t>(N / 64, 1) + 8;
@@ -395,7 +427,14 @@ int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, g
   for (cudaEvent_t* ev : {&h->ev0, &h->ev1, &h->evA, &h->evB, &h->evC}) CK(cudaEventCreate(ev));
   h->ring.resize(4);
   for (auto& ev : h->ring) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  *out = h.release();
+  return h.release();
+}
+
+int gadi_cuda_create(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_handle** out) {
+  API_BEGIN
+  if (!d || !out) throw Err(GADI_E_CONTRACT, "gadi_cuda_create: null argument");
+  *out = nullptr;
+  *out = create_impl(d, opts, nullptr, 0);
   API_END
 }
 
@@ -405,10 +444,11 @@ int gadi_cuda_destroy(gadi_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->eng.reset();
   for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_urp, (void*)h->d_uci,
-                  (void*)h->d_mv, (void*)h->d_nv, (void*)h->d_dpos, (void*)h->d_din, (void*)h->d_x,
-                  (void*)h->d_b, (void*)h->d_s, (void*)h->d_t64, (void*)h->st, (void*)h->d_part0,
-                  (void*)h->d_part1, (void*)h->d_ticket})
+                  (void*)h->d_mv, (void*)h->d_nv, (void*)h->d_dpos, (void*)h->d_din, (void*)h->st,
+                  (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_ticket})
     if (p) cudaFree(p);
+  for (void* p : h->raw) cudaFree(p);  // d_x, d_b, d_s, d_t64 (hvec)
+  h->comm.reset();
   h->sellA.release();
   if (h->h_st) cudaFreeHost(h->h_st);
   if (h->h_done) cudaFreeHost(h->h_done);
@@ -437,6 +477,7 @@ int gadi_cuda_set_rhs(gadi_handle* h, const double* b) {
 
 int gadi_cuda_residual_uf(gadi_handle* h, int32_t u_f, const double* x, double* s_out) {
   API_BEGIN
+  if (h && h->sharded()) throw Err(GADI_E_UNSUPPORTED, "gadi_cuda_residual_uf: not on a shard (use the sharded solve)");
   if (!h || !x || !s_out) throw Err(GADI_E_CONTRACT, "residual_uf: null argument");
   if (u_f < 0 || u_f > 2) throw Err(GADI_E_PARAM, "unknown precision");
   CK(cudaSetDevice(h->device));
@@ -449,6 +490,7 @@ int gadi_cuda_residual_uf(gadi_handle* h, int32_t u_f, const double* x, double* 
 
 int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_out) {
   API_BEGIN
+  if (h && h->sharded()) throw Err(GADI_E_UNSUPPORTED, "gadi_cuda_true_residual_norm: not on a shard (use the sharded solve)");
   if (!h || !x || !norm_out) throw Err(GADI_E_CONTRACT, "true_residual_norm: null argument");
   CK(cudaSetDevice(h->device));
   CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
@@ -461,6 +503,7 @@ int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_o
 int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r, const gadi_inner_spec* spec,
                       int32_t accum) {
   API_BEGIN
+  if (h && h->sharded()) throw Err(GADI_E_UNSUPPORTED, "gadi_cuda_prepare: not on a shard (use the sharded solve)");
   if (!h || !spec) throw Err(GADI_E_CONTRACT, "prepare: null argument");
   if (u_r < 0 || u_r > 2) throw Err(GADI_E_PARAM, "unknown precision");
   CK(cudaSetDevice(h->device));
@@ -566,6 +609,7 @@ int gadi_cuda_history(const gadi_handle* h, double* out, int32_t cap) {
 
 int gadi_cuda_apply(gadi_handle* h, int32_t which, const double* x, double* y) {
   API_BEGIN
+  if (h && h->sharded()) throw Err(GADI_E_UNSUPPORTED, "gadi_cuda_apply: not on a shard (use the sharded solve)");
   if (!h || !x || !y) throw Err(GADI_E_CONTRACT, "apply: null argument");
   CK(cudaSetDevice(h->device));
   CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
@@ -648,11 +692,103 @@ int gadi_cuda_make_rhs(gadi_handle* h, uint64_t seed, double lo, double hi, doub
   API_BEGIN
   if (!h || !d_xtrue || !d_b) throw Err(GADI_E_CONTRACT, "make_rhs: null argument");
   CK(cudaSetDevice(h->device));
-  k_uniform<<<ew_grid(h->N), 256, 0, h->stream>>>(d_xtrue, seed, lo, hi, h->N);
+  // x_true by global row (a shard draws its slab of the same sequence), then
+  // b = A x_true with the neighbours' x_true planes (a collective on shards)
+  k_uniform<<<ew_grid(h->N), 256, 0, h->stream>>>(h->d_t64, seed, lo, hi, h->N, h->e_off());
   CKL();
   ++h->launches;
-  OuterA::apply(h, d_xtrue, d_b);
+  halo(h, h->d_t64);
+  OuterA::apply(h, h->d_t64, d_b);
+  CK(cudaMemcpyAsync(d_xtrue, h->d_t64, h->N * 8, cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+// ------------------------------------------------------------ sharded solves
+int gadi_group_local(int32_t world, gadi_group** out) {
+  API_BEGIN
+  if (!out) throw Err(GADI_E_CONTRACT, "group: null argument");
+  if (world < 1 || world > GADI_MAX_RANKS || (world & (world - 1)) != 0)
+    throw Err(GADI_E_PARAM, "group: world must be a power of two <= 64");
+  gadi_group* g = new gadi_group();
+  g->world = world;
+  g->local.reset(new LocalGroup(world));
+  *out = g;
+  API_END
+}
+
+int gadi_nccl_unique_id(uint8_t* out128) {
+  API_BEGIN
+  if (!out128) throw Err(GADI_E_CONTRACT, "nccl id: null argument");
+  NcclApi& a = NcclApi::get();
+  if (a.get_unique_id(out128) != 0) throw Err(GADI_E_NCCL, "ncclGetUniqueId failed");
+  API_END
+}
+
+int gadi_group_nccl(int32_t world, int32_t rank, const uint8_t* id128, gadi_group** out) {
+  API_BEGIN
+  if (!out || !id128) throw Err(GADI_E_CONTRACT, "group: null argument");
+  if (world < 1 || world > GADI_MAX_RANKS || (world & (world - 1)) != 0)
+    throw Err(GADI_E_PARAM, "group: world must be a power of two <= 64");
+  if (rank < 0 || rank >= world) throw Err(GADI_E_PARAM, "group: rank out of range");
+  NcclApi::get();  // fails loudly without libnccl
+  gadi_group* g = new gadi_group();
+  g->world = world;
+  g->nccl_rank = rank;
+  std::memcpy(g->id.b, id128, sizeof(g->id.b));
+  *out = g;
+  API_END
+}
+
+int gadi_group_destroy(gadi_group* g) {
+  delete g;
+  return GADI_OK;
+}
+
+int gadi_cuda_create_shard(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_group* g, int32_t rank,
+                           gadi_handle** out) {
+  API_BEGIN
+  if (!d || !g || !out) throw Err(GADI_E_CONTRACT, "create_shard: null argument");
+  *out = nullptr;
+  *out = create_impl(d, opts, g, rank);
+  API_END
+}
+
+int gadi_cuda_shard_range(const gadi_handle* h, int64_t* first_row, int64_t* n_rows) {
+  if (!h || !first_row || !n_rows) return GADI_E_CONTRACT;
+  *first_row = h->e_off();
+  *n_rows = h->N;
+  return GADI_OK;
+}
+
+int gadi_cuda_solve_group(gadi_handle* const* hs, int32_t world, const gadi_config* cfg, const double* const* d_b,
+                          const double* const* d_x0, double* const* d_x, gadi_report* reps) {
+  API_BEGIN
+  if (!hs || !cfg || !d_b || !d_x || !reps || world < 1) throw Err(GADI_E_CONTRACT, "solve_group: null argument");
+  LocalGroup* lg = nullptr;
+  for (int r = 0; r < world; ++r) {
+    auto* lc = hs[r] ? dynamic_cast<LocalComm*>(hs[r]->comm.get()) : nullptr;
+    if (!lc || lc->rank != r || lc->world != world || (lg && lc->g != lg))
+      throw Err(GADI_E_CONTRACT, "solve_group: handles must be ranks 0..world-1 of one local group");
+    lg = lc->g;
+  }
+  std::vector<int> rc(world, GADI_OK);
+  std::vector<std::string> msg(world);
+  std::vector<std::thread> th;
+  for (int r = 0; r < world; ++r)
+    th.emplace_back([&, r] {
+      rc[r] = gadi_cuda_solve_device(hs[r], cfg, d_b[r], d_x0 ? d_x0[r] : nullptr, d_x[r], &reps[r]);
+      if (rc[r] != GADI_OK) {
+        msg[r] = gadi_last_error();
+        lg->abort();  // release the ranks waiting at a collective
+      }
+    });
+  for (auto& t : th) t.join();
+  for (int r = 0; r < world; ++r)
+    if (rc[r] != GADI_OK && msg[r].find("aborted by another rank") == std::string::npos)
+      throw Err(rc[r], "rank " + std::to_string(r) + ": " + msg[r]);
+  for (int r = 0; r < world; ++r)
+    if (rc[r] != GADI_OK) throw Err(rc[r], msg[r]);
   API_END
 }
 

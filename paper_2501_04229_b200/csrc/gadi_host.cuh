@@ -25,6 +25,7 @@
 #include "../../include/gadi_cuda.h"
 #include "gadi_kernels.cuh"
 #include "gadi_st25.cuh"
+#include "gadi_dist.cuh"
 #include "gadi_csr.cuh"
 
 using namespace gadi;
@@ -131,7 +132,12 @@ inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
 // grid of n^3 points stored as `tsize`-byte values with `nin` staged inputs.
 // ok = false when the shape does not fit (then the generic kernels run).
 inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_chunks = 512,
-                      bool ident = false, int ring_tsize = 0) {
+                      bool ident = false, int ring_tsize = 0, int64_t i0 = 0, int64_t i1 = -1) {
+  if (i1 < 0) i1 = n;
+  const int64_t nloc = i1 - i0;
+  if (nloc < 1 || !is_pow2(nloc)) return false;
+  g.i0 = (int)i0;
+  g.i1 = (int)i1;
   if (ring_tsize == 0) ring_tsize = tsize;
   if (const char* e = std::getenv("GADI_ST25_CHUNKS")) target_chunks = std::max(32, std::atoi(e));  // tuning knob
   const int vec = 16 / tsize;
@@ -153,10 +159,10 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   g.lgTJ = ilog2(TJ);
   g.njt = (int)(n / TJ);
   int64_t IL = 32;
-  while (IL > 4 && g.njt * (n / IL) < 2048) IL /= 2;
-  IL = std::min<int64_t>(IL, n);
+  while (IL > 4 && g.njt * (nloc / IL) < 2048) IL /= 2;
+  IL = std::min<int64_t>(IL, nloc);
   g.IL = (int)IL;
-  g.nblk = (int)(g.njt * (n / IL));
+  g.nblk = (int)(g.njt * (nloc / IL));
   // operand-ring kernels: raw stages + a 4-plane operand ring; identity-
   // operand kernels fold from the stages directly and need 4 of them
   g.stages = 4;
@@ -336,8 +342,17 @@ struct gadi_handle {
   std::unique_ptr<EngineBase> eng;
   double stop_norm = 1.0;
   std::vector<double> history;
+  // sharded solves (gadi_dist.cuh): this rank's z-slab [i0, i1) of the n
+  // planes; every slab vector has gh = n^2 ghost entries on each side
+  int world = 1, rank = 0;
+  int64_t i0 = 0, i1 = 0, gh = 0;
+  std::unique_ptr<gadi_host::Comm> comm;
+  uint64_t dist_seq = 0;
+  std::vector<void*> raw;  // ghosted allocations (freed at destroy)
 
   bool stencil() const { return kind == GADI_PROBLEM_STENCIL7; }
+  bool sharded() const { return comm != nullptr; }
+  int64_t e_off() const { return i0 * n * n; }  // global index of local entry 0
 };
 
 namespace gadi_host {
@@ -416,11 +431,48 @@ inline void read_state(gadi_handle* h) {
 
 inline Red red_of(gadi_handle* h) { return Red{h->d_part0, h->d_part1, h->d_ticket}; }
 
+// A slab vector of the handle: N entries with h->gh ghost entries on each
+// side (zero-filled), the interior pointer returned.
+template <class T>
+T* hvec(gadi_handle* h, int64_t n_extra = 0) {
+  T* p = dalloc<T>(h->N + 2 * h->gh + n_extra);
+  CK(cudaMemset(p, 0, (h->N + 2 * h->gh + n_extra) * sizeof(T)));
+  h->raw.push_back(p);
+  return p + h->gh;
+}
+
+// Sharded solves: complete a reduction whose kernel parked its record
+// (finish_red) -- all-gather the records, fold them in rank order and apply
+// the epilogue on every rank. A no-op on one device.
+template <class C0, class Epi>
+inline void coll(gadi_handle* h, const Epi& e) {
+  if (!h->sharded()) return;
+  const int half = (int)(h->dist_seq++ & 1);
+  h->comm->allgather4(h->st->dist_loc[half], h->st->dist_all[half], h->stream);
+  k_dist_finish<Epi, C0><<<1, 1, 0, h->stream>>>(e, h->st, h->world, half);
+  CKL();
+}
+// flag / max words only (kernels without a grid reduction)
+inline void coll_flags(gadi_handle* h, int* flags) {
+  if (!h->sharded()) return;
+  k_dist_pack<<<1, 1, 0, h->stream>>>(h->st, flags);
+  coll<double>(h, EpiNone{flags});
+}
+// the ghost planes of a slab vector before a stencil pass reads them
+template <class T>
+inline void halo(gadi_handle* h, const T* interior) {
+  if (!h->sharded()) return;
+  const int64_t plane = h->n * h->n * (int64_t)sizeof(T);
+  h->comm->halo(reinterpret_cast<char*>(const_cast<T*>(interior)), plane, h->i1 - h->i0, h->stream);
+}
+
 // ------------------------------------------------------------ outer kernels on A
 struct OuterA {
   // s = b - A x in u_f; s == nullptr computes the norm only.
   static void resid(gadi_handle* h, const double* x, double* s, int uf, bool scaling) {
     CK(cudaMemsetAsync(&h->st->maxbits, 0, sizeof(unsigned long long), h->stream));
+    halo(h, x);
+    const int64_t eo = h->e_off();  // stencil kernels index by global row
     const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
     const Geo g = make_geo(h->N, al ? 2 : 1);
     const Window win = h->stencil() ? Window{} : window_for(g, 2, sizeof(double), h->max_band, al);
@@ -441,10 +493,11 @@ struct OuterA {
       else LV(VecTag<P_DOUBLE>{});
     };
     St25Geo g25;
-    if (h->stencil() && make_st25(h->n, 8, 1, g25, 1024, true)) {
+    if (h->stencil() && make_st25(h->n, 8, 1, g25, 1024, true, 0, h->i0, h->i1)) {
       auto L = [&](auto pt) {
         constexpr int PF = decltype(pt)::v;
-        PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x, h->d_b, s, scaling ? 1 : 0};
+        PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x - eo, h->d_b - eo,
+                          s ? s - eo : nullptr, scaling ? 1 : 0};
         launch_st25(pol, g25, h->stream, red_of(h), h->st);
       };
       if (uf == GADI_HALF) L(VecTag<P_HALF>{});
@@ -452,6 +505,7 @@ struct OuterA {
       else L(VecTag<P_DOUBLE>{});
     } else if (h->stencil()) {
       Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
+      op.i_off = h->i0;
       go(op);
     } else {
       Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
@@ -460,6 +514,7 @@ struct OuterA {
     }
     CKL();
     ++h->launches;
+    coll<double>(h, EpiResidA{scaling ? 1 : 0});
   }
   static void apply(gadi_handle* h, const double* x, double* y) {
     auto go = [&](auto op) {
@@ -468,6 +523,7 @@ struct OuterA {
     };
     if (h->stencil()) {
       Stencil7<double> op{h->n, h->n * h->n, h->N, {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, lg_of(h->n)};
+      op.i_off = h->i0;
       go(op);
     } else {
       Sell<double> op{h->N, h->sellA.lgSR, h->sellA.soff, h->sellA.len, h->sellA.col,
@@ -532,10 +588,11 @@ struct Engine final : EngineBase {
   St25Geo g25i;       // GMRES residual: identity operand, folded from the stages
   Window win;         // sparse operators: operand window in shared memory
 
-  T* vec() {
-    T* v = dalloc<T>(h->N);
+  T* vec() {  // a slab vector (ghost planes when sharded)
+    T* v = dalloc<T>(h->N + 2 * h->gh);
+    if (h->gh) CK(cudaMemset(v, 0, (h->N + 2 * h->gh) * sizeof(T)));
     owned.push_back(v);
-    return v;
+    return v + h->gh;
   }
 
   Engine(gadi_handle* hh, const gadi_inner_spec& sp, double a, double om, int ur, int acc) : h(hh) {
@@ -552,9 +609,11 @@ struct Engine final : EngineBase {
     if constexpr (SPARSE) win = window_for(geo, VA, sizeof(T), h->max_band, aligned);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       constexpr int rsz = sizeof(typename RingOf<T, C>::type);
-      st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz) && make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz) &&
-             make_st25(h->n, sizeof(T), 1, g25i, 512, true);
+      st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz, h->i0, h->i1) &&
+             make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz, h->i0, h->i1) &&
+             make_st25(h->n, sizeof(T), 1, g25i, 512, true, 0, h->i0, h->i1);
     }
+    if (h->sharded() && !st25) throw Err(GADI_E_UNSUPPORTED, "sharded solve: the slab shape needs the st25 kernels");
     m_restart = std::max(1, spec.restart);
     rhat = vec();
     z = vec();
@@ -601,6 +660,7 @@ struct Engine final : EngineBase {
       opH.nn = opS.nn = h->n * h->n;
       opH.N = opS.N = h->N;
       opH.lg = opS.lg = lg_of(h->n);
+      opH.i_off = opS.i_off = h->i0;
       auto zf = [&](double v) {  // zflag of the u_r-rounded coefficient (gadi_ops.cuh)
         const double r = hround(v, u_r);
         return (uint8_t)((std::signbit(r) ? 1 : 0) | (std::isfinite(r) ? 0 : 2));
@@ -652,8 +712,9 @@ struct Engine final : EngineBase {
   bool spmvp25(const Op& o, const T* r, const T* p_in, T* p_out, int first) {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
+      const int64_t eo = h->e_off();  // the st25 kernels index by global row
       PolSpmvp<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]},
-                         r, p_in, p_out, q, Ar_beta(), first};
+                         r - eo, p_in - eo, p_out - eo, q - eo, Ar_beta(), first};
       launch_st25(pol, g25, h->stream, red_of(h), h->st);
       return true;
     } else {
@@ -663,7 +724,9 @@ struct Engine final : EngineBase {
   bool gmmatvec25(const Op& o, const T* wprev, double inv, T* vj, T* w) {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
-      PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev, inv, vj, V, w};
+      const int64_t eo = h->e_off();
+      PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev - eo, inv, vj - eo,
+                            V - eo, w - eo};
       launch_st25(pol, g25m, h->stream, red_of(h), h->st);
       return true;
     } else {
@@ -673,7 +736,8 @@ struct Engine final : EngineBase {
   bool gmresid25(const Op& o, const T* x, const T* rhs) {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
-      PolGmResid<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, x, rhs, gr};
+      const int64_t eo = h->e_off();
+      PolGmResid<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, x - eo, rhs - eo, gr - eo};
       launch_st25(pol, g25i, h->stream, red_of(h), h->st);
       return true;
     } else {
@@ -703,15 +767,23 @@ struct Engine final : EngineBase {
     });
     CKL();
     ++h->launches;
+    coll<C>(h, EpiCgInit{spec.max_inner_iters, target});
     const int kAhead = (int)h->ring.size();
     for (int it = 0; it < spec.max_inner_iters; ++it) {
       if (it >= kAhead) {
         CK(cudaEventSynchronize(h->ring[it % kAhead]));
-        if (*(volatile int*)h->h_done) break;
+        const int hd = *(volatile int*)h->h_done;
+        // sharded: stop where the decision was made at or before the synced
+        // iteration, so every rank queues the same collectives
+        if (h->sharded() ? (hd && hd - 2 <= it - kAhead) : hd != 0) break;
       }
       T* p_in = (it & 1) ? pA : pB;
       T* p_out = (it & 1) ? pB : pA;
       const int first = it == 0;
+      if (h->sharded()) {  // the stencil pass reads r and p_old on the neighbours' boundary planes
+        halo(h, r);
+        if (!first) halo(h, p_in);
+      }
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
         if constexpr (SPARSE) {  // p-update as its own pass: a gathered operand is not re-formed per nonzero
@@ -723,7 +795,9 @@ struct Engine final : EngineBase {
         } else if (!spmvp25(o, r, p_in, p_out, first)) {
           k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
         }
+        coll<C>(h, EpiCgPap{});
         k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st);
+        coll<C>(h, EpiCgUpdate{});
       });
       CKL();
       h->launches += 2;
@@ -760,13 +834,16 @@ struct Engine final : EngineBase {
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
+        if (!x_zero) halo(h, x);
         if (x_zero || !gmresid25(o, x, rhs)) {
           auto kern = k_gm_resid<Op, T, C, V_>;
           const size_t sm = x_zero ? 0 : win.bytes;
           smem_attr(kern, sm);
           kern<<<geo.nblk, nt, sm, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st, x_zero ? 0 : win.band);
         }
+        coll<C>(h, EpiRedD{});
         k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
+        coll<C>(h, EpiNorm2{&h->st->red_c});
       });
       CKL();
       h->launches += 2;
@@ -804,19 +881,25 @@ struct Engine final : EngineBase {
             smem_attr(kern, win.bytes);
             kern<<<geo.nblk, nt, win.bytes, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st, win.band);
             ++h->launches;
-          } else if (!gmmatvec25(o, wprev, inv, vj, w)) {
-            k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
+          } else {
+            halo(h, wprev);
+            if (!gmmatvec25(o, wprev, inv, vj, w))
+              k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
           }
+          coll<C>(h, EpiHcol{0});
           for (int i = 0; i <= j; ++i) {
             T* vi = V + (int64_t)i * N;
             if (i < j) {
               k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + N, i, geo, rd, h->st);
+              coll<C>(h, EpiHcol{i + 1});
             } else {
               CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
               k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
+              coll_flags(h, nullptr);  // max|w| over all ranks
             }
           }
           k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
+          coll<C>(h, EpiNorm2{&h->st->hcol[j + 1]});
         });
         CKL();
         h->launches += j + 3;
@@ -877,6 +960,7 @@ struct Engine final : EngineBase {
       });
       CKL();
       ++h->launches;
+      coll_flags(h, &h->st->flags);
       x_zero = false;
       read_state(h);
       if (h->h_st->flags & 1) {
@@ -910,6 +994,7 @@ struct Engine final : EngineBase {
     else k_scale_round<T, 1><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
     CKL();
     ++h->launches;
+    coll<double>(h, EpiRhat{});
   }
   void scale_pz(double phat) override {
     V2([&](auto vt) {
@@ -935,6 +1020,7 @@ struct Engine final : EngineBase {
     else LV(VecTag<P_DOUBLE>{});
     CKL();
     ++h->launches;
+    coll_flags(h, &h->st->xbad);
   }
   void to_inner(const double* src, void* dst) override {
     constexpr int PT = prec_of<T>();

@@ -26,6 +26,7 @@
 namespace gadi {
 
 constexpr int RMAX = 8;  // segments per lane (unrolled)
+#define GADI_MAX_RANKS 64
 
 struct Geo {
   int64_t N;
@@ -60,19 +61,96 @@ struct DevState {
   double res_ss, res_max, rhat_ss;
   int res_e, xbad;
   int* hdone;  // mapped host flag raised when a CG solve finishes
+  // sharded solves (gadi_dist.cuh): this rank's subtree sums + flag/max
+  // words, parked by a reduction's last block; all ranks' copies, gathered
+  // Both are double-buffered by collective parity (dist_par, toggled by
+  // k_dist_finish): a peer may still be pulling record c while this rank's
+  // next reduction writes record c+1.
+  int dist, dist_par;
+  double dist_loc[2][4];
+  double dist_all[2][4 * GADI_MAX_RANKS];
 };
 
 enum : int { INNER_CONVERGED = 0, INNER_STAGNATED = 1, INNER_OVERFLOW = 2 };
 
-__device__ __forceinline__ void cg_finish(DevState* st, int status, int iters) {
+// host_it: the host loop iteration whose kernels decided (-1: the init pass).
+// The mapped flag carries host_it + 2, so a sharded solve's ranks can all stop
+// queueing at the same iteration (Engine::cg).
+__device__ __forceinline__ void cg_finish(DevState* st, int status, int iters, int host_it) {
   st->cg_done = 1;
   st->cg_status = status;
   st->cg_iters = iters;
   if (st->hdone) {
-    *(volatile int*)st->hdone = 1;
+    *(volatile int*)st->hdone = host_it + 2;
     __threadfence_system();
   }
 }
+
+// ------------------------------------------------------------ epilogues
+// A reduction's scalar epilogue (the recurrences / stop tests that follow a
+// dot or norm in the reference) is an object with finish(t0, t1, st) and
+// flag_dst(st). On one device the last block applies it directly. In a
+// sharded solve (st->dist) the last block parks the rank's subtree sums and
+// its flag / max words in st->dist_loc; the host all-gathers them and
+// k_dist_finish folds the ranks' values in rank order -- the slabs are
+// aligned power-of-two blocks of the pairwise tree, so this is the
+// single-device value bit for bit -- and applies the same epilogue.
+template <class Epi, class C0>
+__device__ __forceinline__ void finish_red(const Epi& epi, DevState* st, C0 t0, double t1) {
+  if (st->dist) {
+    int* f = epi.flag_dst(st);
+    double* rec = st->dist_loc[st->dist_par];
+    rec[0] = to_dbl(t0);
+    rec[1] = t1;
+    rec[2] = f ? (double)*(volatile int*)f : 0.0;
+    rec[3] = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
+  } else {
+    epi.finish(t0, t1, st);
+  }
+}
+
+// the flag / max words alone (kernels without a grid reduction)
+static __global__ void k_dist_pack(DevState* st, int* flags) {
+  double* rec = st->dist_loc[st->dist_par];
+  rec[0] = 0.0;
+  rec[1] = 0.0;
+  rec[2] = flags ? (double)*flags : 0.0;
+  rec[3] = __longlong_as_double((long long)st->maxbits);
+}
+
+template <class Epi, class C0>
+__global__ void k_dist_finish(const Epi epi, DevState* st, int world, int half) {
+  C0 v0[GADI_MAX_RANKS];
+  double v1[GADI_MAX_RANKS];
+  int fl = 0;
+  unsigned long long mb = 0;
+  const double* all = st->dist_all[half];
+  for (int r = 0; r < world; ++r) {
+    v0[r] = from_dbl<C0>(all[4 * r]);
+    v1[r] = all[4 * r + 1];
+    fl |= (int)all[4 * r + 2];
+    const unsigned long long b = (unsigned long long)__double_as_longlong(all[4 * r + 3]);
+    mb = b > mb ? b : mb;
+  }
+  for (int s = 1; s < world; s <<= 1)  // world is a power of two
+    for (int k = 0; k + s < world; k += 2 * s) {
+      v0[k] = Ar<C0>::add(v0[k], v0[k + s]);
+      v1[k] = __dadd_rn(v1[k], v1[k + s]);
+    }
+  st->dist_par = half ^ 1;
+  if (epi.skip(st)) return;  // the kernel returned early (CG done): nothing was reduced
+  if (int* f = epi.flag_dst(st)) *f = fl;
+  st->maxbits = mb;
+  epi.finish(v0[0], v1[0], st);
+}
+
+struct EpiNone {  // flags / max only
+  int* flags = nullptr;
+  template <class C0>
+  __device__ void finish(C0, double, DevState*) const {}
+  __device__ int* flag_dst(DevState*) const { return flags; }
+  __device__ bool skip(DevState*) const { return false; }
+};
 
 // ------------------------------------------------------------ segment loop
 // Runs body(seg, c, d) on this lane's R segments and returns the warp's
@@ -352,6 +430,73 @@ struct MatvecAF {  // b = A x in binary64 (problems.cpp:44)
 #define GADI_LIVE(i) (VEC > 1 || (i) < s.len)
 
 // ================================================================== CG
+struct EpiCgInit {  // inner_solver.cpp:51-57
+  int max_inner;
+  double target;
+  template <class C>
+  __device__ void finish(C rs, double ss, DevState* st) const {
+    st->cg_rs = to_dbl(rs);
+    st->cg_it = 0;
+    st->cg_flags = 0;
+    st->cg_xvalid = 0;
+    st->cg_max = max_inner;
+    st->cg_target = target;
+    st->cg_done = 0;
+    if (max_inner <= 0) cg_finish(st, INNER_STAGNATED, 0, -1);
+    else if (sqrt(ss) <= target) cg_finish(st, INNER_CONVERGED, 0, -1);
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+struct EpiCgPap {  // alpha = rs / pap, or `break` (inner_solver.cpp:62-65)
+  template <class C>
+  __device__ void finish(C pap, double, DevState* st) const {
+    const double pd = to_dbl(pap);
+    st->cg_pap = pd;
+    if (pd == 0.0 || !isfinite(pd)) {
+      // `break` -> Stagnated / Overflow with iters = max (:64, :79-81)
+      cg_finish(st, (st->cg_flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max, st->cg_it);
+    } else {
+      st->cg_a = to_dbl(div_c<C>(from_dbl<C>(st->cg_rs), pap));
+    }
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return *(volatile int*)&st->cg_done != 0; }
+};
+struct EpiCgUpdate {  // beta, the overflow / max-iteration / residual stop tests (inner_solver.cpp:66-77)
+  template <class C>
+  __device__ void finish(C rsn, double ss, DevState* st) const {
+    const int it = st->cg_it;
+    const double rn = to_dbl(rsn);
+    const int flags = *(volatile int*)&st->cg_flags;
+    st->cg_xvalid = 1;
+    if (!isfinite(rn) || (flags & 1)) {
+      cg_finish(st, INNER_OVERFLOW, it + 1, it);
+    } else {
+      st->cg_beta = to_dbl(div_c<C>(rsn, from_dbl<C>(st->cg_rs)));
+      st->cg_rs = rn;
+      st->cg_it = it + 1;
+      if (it + 1 >= st->cg_max) cg_finish(st, (flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max, it);
+      else if (sqrt(ss) <= st->cg_target) cg_finish(st, INNER_CONVERGED, it + 1, it);
+    }
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->cg_flags; }
+  __device__ bool skip(DevState* st) const { return *(volatile int*)&st->cg_done != 0; }
+};
+struct EpiRedD {  // ||r||_2 of a GMRES restart residual (+ flags, max)
+  template <class C>
+  __device__ void finish(C, double ss, DevState* st) const { st->red_d = ss; }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+struct EpiHcol {  // an Arnoldi coefficient h(i, j)
+  int i;
+  template <class C>
+  __device__ void finish(C h, double, DevState* st) const { st->hcol[i] = to_dbl(h); }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+
 // r = rhs (in place), rs = dot(r, r) and the initial stop test
 // (inner_solver.cpp:51-57). x and p are produced by the first iteration.
 template <class T, class C, int VEC>
@@ -375,17 +520,7 @@ __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int ma
   }, w0, w1);
   C rs;
   double ss;
-  if (grid_finish(w0, w1, g, rd, rs, ss)) {
-    st->cg_rs = to_dbl(rs);
-    st->cg_it = 0;
-    st->cg_flags = 0;
-    st->cg_xvalid = 0;
-    st->cg_max = max_inner;
-    st->cg_target = target;
-    st->cg_done = 0;
-    if (max_inner <= 0) cg_finish(st, INNER_STAGNATED, 0);
-    else if (sqrt(ss) <= target) cg_finish(st, INNER_CONVERGED, 0);
-  }
+  if (grid_finish(w0, w1, g, rd, rs, ss)) finish_red(EpiCgInit{max_inner, target}, st, rs, ss);
 }
 
 // p_out = r + beta p_in (or r on the first iteration; inner_solver.cpp:53,76),
@@ -429,16 +564,7 @@ __global__ void __launch_bounds__(256) k_cg_spmvp(Op op, const T* __restrict__ r
   }
   C pap;
   double dummy;
-  if (grid_finish(w0, w1, g, rd, pap, dummy)) {
-    const double pd = to_dbl(pap);
-    st->cg_pap = pd;
-    if (pd == 0.0 || !isfinite(pd)) {
-      // `break` -> Stagnated / Overflow with iters = max (:64, :79-81)
-      cg_finish(st, (st->cg_flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
-    } else {
-      st->cg_a = to_dbl(div_c<C>(from_dbl<C>(st->cg_rs), pap));
-    }
-  }
+  if (grid_finish(w0, w1, g, rd, pap, dummy)) finish_red(EpiCgPap{}, st, pap, dummy);
 }
 
 // p_out = r + beta p_in, or r on the first iteration (inner_solver.cpp:53,76);
@@ -502,21 +628,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
   or_flags(&st->cg_flags, bad);
   C rsn;
   double ss;
-  if (grid_finish(w0, w1, g, rd, rsn, ss)) {
-    const int it = st->cg_it;
-    const double rn = to_dbl(rsn);
-    const int flags = *(volatile int*)&st->cg_flags;
-    st->cg_xvalid = 1;
-    if (!isfinite(rn) || (flags & 1)) {
-      cg_finish(st, INNER_OVERFLOW, it + 1);
-    } else {
-      st->cg_beta = to_dbl(div_c<C>(rsn, from_dbl<C>(st->cg_rs)));
-      st->cg_rs = rn;
-      st->cg_it = it + 1;
-      if (it + 1 >= st->cg_max) cg_finish(st, (flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
-      else if (sqrt(ss) <= st->cg_target) cg_finish(st, INNER_CONVERGED, it + 1);
-    }
-  }
+  if (grid_finish(w0, w1, g, rd, rsn, ss)) finish_red(EpiCgUpdate{}, st, rsn, ss);
 }
 
 // ================================================================ GMRES
@@ -597,8 +709,24 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
   or_flags(&st->flags, bad);
   C dc;
   double ss;
-  if (grid_finish(w0, w1, g, rd, dc, ss)) st->red_d = ss;
+  if (grid_finish(w0, w1, g, rd, dc, ss)) finish_red(EpiRedD{}, st, dc, ss);
 }
+
+struct EpiNorm2 {  // m * sqrt(sum) in the inner format (kernels.cpp:79-81), m = max|w| from maxbits
+  double* dst;
+  template <class C>
+  __device__ void finish(C sum, double, DevState* st) const {
+    const double m = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
+    if (m == 0.0 || !isfinite(m)) {
+      *dst = m;
+    } else {
+      const C sq = Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(sum)));
+      *dst = to_dbl(Ar<C>::mul(from_dbl<C>(m), sq));
+    }
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
 
 // norm2 in the inner format (kernels.cpp:71-82): m = max|w| (from maxbits),
 // q = w/m, pairwise sum of q*q, m * sqrt(sum); written to *dst.
@@ -641,14 +769,7 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   }, w0, w1);
   C sum;
   double dummy;
-  if (grid_finish(w0, w1, g, rd, sum, dummy)) {
-    if (m == 0.0 || !isfinite(m)) {
-      *dst = m;
-    } else {
-      const C sq = Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(sum)));
-      *dst = to_dbl(Ar<C>::mul(mc, sq));
-    }
-  }
+  if (grid_finish(w0, w1, g, rd, sum, dummy)) finish_red(EpiNorm2{dst}, st, sum, dummy);
 }
 
 // dst = round(a * src) with a in binary64 (scale, kernels.cpp:166-171).
@@ -708,7 +829,7 @@ __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ 
   }
   C h;
   double dummy;
-  if (grid_finish(w0, w1, g, rd, h, dummy)) st->hcol[0] = to_dbl(h);
+  if (grid_finish(w0, w1, g, rd, h, dummy)) finish_red(EpiHcol{0}, st, h, dummy);
 }
 
 // Modified Gram-Schmidt step i (inner_solver.cpp:121-125): w -= h_i v_i, then
@@ -749,7 +870,7 @@ __global__ void __launch_bounds__(256) k_gm_mgs(T* __restrict__ w, const T* __re
   } else {
     C h;
     double dummy;
-    if (grid_finish(w0, w1, g, rd, h, dummy)) st->hcol[i + 1] = to_dbl(h);
+    if (grid_finish(w0, w1, g, rd, h, dummy)) finish_red(EpiHcol{i + 1}, st, h, dummy);
   }
 }
 
@@ -783,6 +904,22 @@ __global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero
 }
 
 // ============================================================ outer loop
+struct EpiResidA {  // ||s||, max|s| and the scaling exponent (solver.cpp:48-53)
+  int scaling;
+  __device__ void finish(double, double ss, DevState* st) const {
+    const double mx = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
+    st->res_ss = ss;
+    st->res_max = mx;
+    st->res_e = (scaling && mx != 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+struct EpiRhat {  // ||rhat||_2
+  __device__ void finish(double, double ss, DevState* st) const { st->rhat_ss = ss; }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
 // s = b - A x in u_f (residual_uf, solver.cpp:190-192); max|s|, ||s||_2 and
 // the scaling exponent e = ilogb(max|s|) (solver.cpp:48-53). s may be null
 // (norm only: true_residual_norm, solver.cpp:194-197).
@@ -816,10 +953,7 @@ __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict
   double dummy, ss;
   if (grid_finish(w0, w1, g, rd, dummy, ss)) {
     __threadfence();
-    const double mx = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
-    st->res_ss = ss;
-    st->res_max = mx;
-    st->res_e = (scaling && mx != 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
+    finish_red(EpiResidA{scaling}, st, dummy, ss);
   }
 }
 
@@ -845,7 +979,7 @@ __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ 
     d = seg_sum<double, G>(td, s.len);
   }, w0, w1);
   double dummy, ss;
-  if (grid_finish(w0, w1, g, rd, dummy, ss)) st->rhat_ss = ss;
+  if (grid_finish(w0, w1, g, rd, dummy, ss)) finish_red(EpiRhat{}, st, dummy, ss);
 }
 
 // x = round_u(x + round_u(2^e y)) (solver.cpp:163-166 with axpy kernels.cpp:147-164).
@@ -895,9 +1029,10 @@ __device__ __forceinline__ double uniform01(uint64_t seed, uint64_t i, double lo
   const double u = __dmul_rn((double)(splitmix64(seed, i) >> 11), 0x1p-53);
   return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u));
 }
-static __global__ void k_uniform(double* __restrict__ x, uint64_t seed, double lo, double hi, int64_t n) {
+static __global__ void k_uniform(double* __restrict__ x, uint64_t seed, double lo, double hi, int64_t n,
+                                 int64_t off = 0) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) x[i] = uniform01(seed, (uint64_t)i, lo, hi);
+  if (i < n) x[i] = uniform01(seed, (uint64_t)(i + off), lo, hi);
 }
 
 // y = Op x with the given fold, one element per thread (tests / rhs).

@@ -114,6 +114,7 @@ struct Stencil7 {
   V c[7];
   int lg;  // log2(n) when n is a power of two (always on the aligned path), else -1
   uint8_t zc[7];  // zflag of each coefficient (set by the engine; see zflags)
+  int64_t i_off;  // first plane of a z-slab (sharded solves): local row e is global row e + i_off*n^2
 
   // Fold for the VEC consecutive elements e0..e0+VEC-1 of one grid row
   // (aligned path: e0 % VEC == 0 and n % VEC == 0; VEC == 1 is any element).
@@ -124,12 +125,12 @@ struct Stencil7 {
     if (lg >= 0) {  // shifts, not 64-bit division, on the hot path
       k0 = e0 & (n - 1);
       j = (e0 >> lg) & (n - 1);
-      i = e0 >> (2 * lg);
+      i = (e0 >> (2 * lg)) + i_off;
     } else {
       k0 = e0 % n;
       const int64_t r = e0 / n;
       j = r % n;
-      i = r / n;
+      i = r / n + i_off;
     }
     X nb[VEC];
     x.template vec<VEC>(e0, cc);
@@ -181,12 +182,12 @@ struct Stencil7 {
     if (lg >= 0) {
       k = e & (n - 1);
       j = (e >> lg) & (n - 1);
-      i = e >> (2 * lg);
+      i = (e >> (2 * lg)) + i_off;
     } else {
       k = e % n;
       const int64_t r = e / n;
       j = r % n;
-      i = r / n;
+      i = r / n + i_off;
     }
     int f = zc[3];
     if (i > 0) f |= zc[0];
@@ -204,12 +205,12 @@ struct Stencil7 {
     if (lg >= 0) {
       k0 = e0 & (n - 1);
       j = (e0 >> lg) & (n - 1);
-      i = e0 >> (2 * lg);
+      i = (e0 >> (2 * lg)) + i_off;
     } else {
       k0 = e0 % n;
       const int64_t r = e0 / n;
       j = r % n;
-      i = r / n;
+      i = r / n + i_off;
     }
     int b = zc[3];
     if (i > 0) b |= zc[0];

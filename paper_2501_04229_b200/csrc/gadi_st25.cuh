@@ -144,7 +144,8 @@ struct St25Geo {
   int TR, lgTR;   // 16-byte chunks per row
   int CPT;        // chunks per thread per plane (power of two)
   int njt;        // tiles per plane = n / TJ
-  int nblk;       // CTAs = njt * n / IL
+  int i0, i1;     // the planes this device owns (a z-slab of a sharded solve; 0, n on one device)
+  int nblk;       // CTAs = njt * (i1 - i0) / IL
   int threads;
   int stages;
   int64_t nn;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int jt = blockIdx.x % g.njt, ic = blockIdx.x / g.njt;
-  const int j0 = jt << g.lgTJ, ib = ic * g.IL, ie = ib + g.IL;
+  const int j0 = jt << g.lgTJ, ib = g.i0 + ic * g.IL, ie = ib + g.IL;
   const int rlo = max(j0 - 1, 0), rhi = min(j0 + g.TJ, n - 1);
   const uint32_t bytes_in = (uint32_t)((rhi - rlo + 1) * n * sizeof(T));
   const int soff = (rlo - (j0 - 1)) * n;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
             if (P::HAS_R0) v0[k] = Ar<R0>::add(v0[k], v0[k + s2]);
             if (P::HAS_R1) v1[k] = __dadd_rn(v1[k], v1[k + s2]);
           }
-      const int64_t slot = (int64_t)(ib + t) * g.njt + jt;
+      const int64_t slot = (int64_t)(ib - g.i0 + t) * g.njt + jt;
       if (P::HAS_R0) rd.part0[slot] = to_dbl(v0[0]);
       if (P::HAS_R1) rd.part1[slot] = v1[0];
     }
@@ -402,7 +403,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int64_t P_ = (int64_t)n * g.njt;  // partials (power of two)
+  const int64_t P_ = (int64_t)(g.i1 - g.i0) * g.njt;  // partials (power of two)
   const int B = blockDim.x;
   R0 t0 = Ar<R0>::zero();
   double t1 = 0.0;
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   if (tid == 0) {
     *rd.ticket = 0u;
     __threadfence();
-    pol.finish(t0, t1, st);
+    finish_red(pol, st, t0, t1);
   }
 }
 
@@ -495,13 +496,8 @@ struct PolSpmvp {
     st_vec<T, ST25_VEC>(p_out, e0, pv);
     c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
   }
-  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
-  __device__ void finish(C pap, double, DevState* st) const {
-    const double pd = to_dbl(pap);
-    st->cg_pap = pd;
-    if (pd == 0.0 || !isfinite(pd)) cg_finish(st, (st->cg_flags & 2) ? INNER_OVERFLOW : INNER_STAGNATED, st->cg_max);
-    else st->cg_a = to_dbl(div_c<C>(from_dbl<C>(st->cg_rs), pap));
-  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ void finish(C pap, double t1, DevState* st) const { EpiCgPap{}.finish(pap, t1, st); }
 };
 
 // Arnoldi step: v_j = round(inv * w_prev) (stored), w = S v_j, h_0j = dot(w, v_0)  (= k_gm_matvec)
@@ -558,8 +554,8 @@ struct PolGmMatvec {
     st_vec<T, ST25_VEC>(w, e0, wv);
     c = seg_sum<C, ST25_VEC>(tc, ST25_VEC);
   }
-  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
-  __device__ void finish(C h, double, DevState* st) const { st->hcol[0] = to_dbl(h); }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ void finish(C h, double t1, DevState* st) const { EpiHcol{0}.finish(h, t1, st); }
 };
 
 // GMRES restart residual r = rhs - S x (x != 0), max|r|, ||r||, finiteness (= k_gm_resid)
@@ -603,7 +599,7 @@ struct PolGmResid {
     d = seg_sum<double, ST25_VEC>(td, ST25_VEC);
   }
   __device__ int* flag_dst(DevState* st) const { return &st->flags; }
-  __device__ void finish(C, double ss, DevState* st) const { st->red_d = ss; }
+  __device__ void finish(C t0, double ss, DevState* st) const { EpiRedD{}.finish(t0, ss, st); }
 };
 
 // Outer residual s = b - A x in u_f (binary64 carried), max|s|, ||s||, e (= k_resid_A)
@@ -638,13 +634,8 @@ struct PolResidA {
     if (s) st_vec<double, 2>(s, e0, acc);
     d = seg_sum<double, 2>(td, 2);
   }
-  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
-  __device__ void finish(double, double ss, DevState* st) const {
-    const double mx = __longlong_as_double((long long)*(volatile unsigned long long*)&st->maxbits);
-    st->res_ss = ss;
-    st->res_max = mx;
-    st->res_e = (scaling && mx != 0.0 && isfinite(mx)) ? ilogb(mx) : 0;
-  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ void finish(double t0, double ss, DevState* st) const { EpiResidA{scaling}.finish(t0, ss, st); }
 };
 
 #undef ST25_VEC
