@@ -257,7 +257,13 @@ def main():
     cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": 1.0, "inner": "cg(H)/gmres(S)",
                 "max_inner": wl["max_inner"], "tol_epsilon": wl["eps"], "xi": 1e-20,
                 "l2": "inputs larger than L2 (x, b: 8N bytes each)",
-                "parallelism": f"replicas{world}" if world > 1 else "single"}
+                "parallelism": "single"}
+    # stencil workloads shard into z-slabs over the ranks (NCCL, strong
+    # scaling: the same n^3 problem on every N); the band CSR has no row-block
+    # sharding yet and runs one full replica per GPU (weak scaling)
+    sharded = world > 1 and wl.get("kind") != "band"
+    if world > 1:
+        cfg_json["parallelism"] = f"zslab{world}" if sharded else f"replicas{world}"
     if band:
         cfg_json.update(k_off=wl["k_off"], band=wl["band"], matrix_seed=wl["mseed"])
     else:
@@ -287,11 +293,19 @@ def main():
         S = g.build_band_csr(wl["N"], wl["k_off"], wl["band"], wl["mseed"])
     else:
         S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
-    sysx = g.CudaGadiSystem(S, device=local)
-    N = S.n_rows
+    grp = None
+    if sharded:  # one NCCL communicator for the solver's collectives (gadi_group_nccl)
+        obj = [g.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        grp = g.ShardGroup.nccl(world, rank, obj[0])
+        sysx = g.ShardSystem(S, grp, rank, device=local)
+    else:
+        sysx = g.CudaGadiSystem(S, device=local)
+    N = sysx.n  # this rank's rows
     xt = torch.empty(N, dtype=torch.float64, device="cuda")
     b = torch.empty_like(xt)
-    sysx.make_rhs(wl["seed"] + rank, wl["lo"], wl["hi"], xt.data_ptr(), b.data_ptr())
+    seed = wl["seed"] if (sharded or world == 1) else wl["seed"] + rank
+    sysx.make_rhs(seed, wl["lo"], wl["hi"], xt.data_ptr(), b.data_ptr())  # collective on shards
     torch.cuda.synchronize()
     b_h = b.cpu().pin_memory()
     x_h = torch.empty(N, dtype=torch.float64).pin_memory()
@@ -325,7 +339,10 @@ def main():
     h_it = sum(r.h_iters for r in reps)
     ok = all(r.status == g.SolveStatus.Converged for r in reps)
     x = torch.from_numpy(x_np).cuda()
-    ferr = (torch.linalg.norm(x - xt) / torch.linalg.norm(xt)).item()
+    ss = torch.stack([torch.sum((x - xt) ** 2), torch.sum(xt ** 2)])
+    if sharded:
+        dist.all_reduce(ss)
+    ferr = (ss[0].sqrt() / ss[1].sqrt()).item()
     if dist:
         t = torch.tensor([solve_s, e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -344,7 +361,8 @@ def main():
             traffic = json.load(f).get("cg_iteration_dram_bytes")
     out = {
         "metric": metric, "value": solve_s, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": solve_s * 1e3, "higher_is_better": False, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": solve_s * 1e3, "higher_is_better": False,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64 outer / " + ("f16 storage, f32 arithmetic" if wl["u_r"] == 0 else "f32")
         + " inner", "data": "synthetic (seeded splitmix64 x_true, b = A x_true)", "config": cfg_json,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(reps[0].h2d_bytes),
@@ -352,8 +370,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": ("inner CG iteration (p-update, SELL spmv + p.q, axpys + dots)"
                                                 if band else "inner CG iteration (spmv+p-update, axpys+dots)"),
                      "achieved": cg_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic,
-                     "algorithmic_bytes_per_iter": bytes_it},
+                     "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic if world == 1 else None,
+                     "algorithmic_bytes_per_iter": bytes_it, "per": "GPU (rank 0's slab)" if sharded else "GPU"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "solve": {"converged": ok, "outer_iters": reps[0].outer_iters, "final_rres": reps[0].final_rres,
@@ -366,6 +384,8 @@ def main():
     if rank == 0:
         print(json.dumps(out), flush=True)
     sysx.close()
+    if grp is not None:
+        grp.close()
     if dist:
         dist.destroy_process_group()
 

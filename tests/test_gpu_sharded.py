@@ -105,3 +105,28 @@ def test_shard_contract_errors():
         sh.residual_uf(np.zeros(sh.n))  # whole-vector API calls are not collective
     sh.close()
     grp.close()
+
+
+def test_nccl_transport_world1():
+    """The NCCL transport (libnccl loaded at run time, ncclAllGather of the
+    reduction records) on a one-rank communicator: the same bits as the
+    unsharded solve. Multi-rank NCCL runs under torchrun (bench.py --gpus N)."""
+    S = g.build_convdiff3d(16, r=0.3)
+    full = g.CudaGadiSystem(S)
+    xt = torch.empty(S.n_rows, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(xt)
+    full.make_rhs(1, -1.0, 1.0, xt.data_ptr(), b.data_ptr())
+    cfg = g.GadiConfig(alpha=0.3, xi=1e-20, u_r=g.Precision.Half, accum=g.Accum.Fp32,
+                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30))
+    x1 = torch.empty_like(xt)
+    rep1 = full.solve_device(b.data_ptr(), x1.data_ptr(), cfg)
+    grp = g.ShardGroup.nccl(1, 0, g.nccl_unique_id())
+    sh = g.ShardSystem(S, grp, 0)
+    x2 = torch.empty_like(xt)
+    rep2 = sh.solve_device(b.data_ptr(), x2.data_ptr(), cfg)
+    torch.cuda.synchronize()
+    assert rep2.outer_iters == rep1.outer_iters and rep2.status == rep1.status
+    assert np.array_equal(bits(x2), bits(x1))
+    sh.close()
+    grp.close()
+    full.close()
