@@ -218,69 +218,6 @@ constexpr int prec_of() {
   return std::is_same<T, __half>::value ? GADI_HALF : std::is_same<T, float>::value ? GADI_SINGLE : GADI_DOUBLE;
 }
 
-// ---------------------------------------------------------------- the problem
-struct HostCsr {
-  std::vector<int64_t> rp, ci;
-};
-
-// hss_split (splitting.cpp:12-20) on the host for the CSR path: union pattern
-// of A and A^T, M = (A + A^T)/2, N = (A - A^T)/2 with explicit zeros (the
-// duplicate summation of from_triplets, sparse.cpp:36-58,166-178), plus the
-// diagonal in the pattern (shift_diagonal, sparse.cpp:180-183). diag_in
-// records whether the diagonal was already in M's own pattern.
-inline void hss_split_host(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, HostCsr& P,
-                    std::vector<double>& Mv, std::vector<double>& Nv, std::vector<uint8_t>& diag_in) {
-  const int64_t nnz = rp[n];
-  std::vector<int64_t> trp(n + 1, 0), tci(nnz), next(n);
-  std::vector<double> tv(nnz);
-  for (int64_t k = 0; k < nnz; ++k) ++trp[ci[k] + 1];
-  for (int64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
-  for (int64_t j = 0; j < n; ++j) next[j] = trp[j];
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-      const int64_t q = next[ci[k]]++;
-      tci[q] = i;
-      tv[q] = v[k];
-    }
-  P.rp.assign(n + 1, 0);
-  P.ci.clear();
-  Mv.clear();
-  Nv.clear();
-  diag_in.clear();
-  P.ci.reserve(nnz + n);
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t a = rp[i], ae = rp[i + 1], t = trp[i], te = trp[i + 1];
-    bool diag_done = false;
-    while (a < ae || t < te || !diag_done) {
-      const int64_t ca = a < ae ? ci[a] : INT64_MAX, ct = t < te ? tci[t] : INT64_MAX;
-      int64_t col = std::min(ca, ct);
-      if (!diag_done && i <= col) col = i;
-      const bool hA = ca == col, hT = ct == col;
-      double m = 0.0, nv = 0.0;
-      if (hA && hT) {
-        m = 0.5 * v[a] + 0.5 * tv[t];
-        nv = 0.5 * v[a] + -0.5 * tv[t];
-      } else if (hA) {
-        m = 0.5 * v[a];
-        nv = 0.5 * v[a];
-      } else if (hT) {
-        m = 0.5 * tv[t];
-        nv = -0.5 * tv[t];
-      }
-      if (col == i) {
-        diag_done = true;
-        diag_in.push_back(hA || hT);
-      }
-      P.ci.push_back(col);
-      Mv.push_back(m);
-      Nv.push_back(nv);
-      if (hA) ++a;
-      if (hT) ++t;
-    }
-    P.rp[i + 1] = (int64_t)P.ci.size();
-  }
-}
-
 }  // namespace gadi_host
 
 // ==================================================================== handle
