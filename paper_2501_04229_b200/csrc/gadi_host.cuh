@@ -152,7 +152,9 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   int64_t TJ = std::max<int64_t>(1, target_chunks / TR);
   TJ = std::min<int64_t>(TJ, n);
   const int64_t chunks = TJ * TR;
-  g.threads = (int)std::min<int64_t>(256, chunks);
+  int64_t max_threads = 256;
+  if (const char* e = std::getenv("GADI_ST25_THREADS")) max_threads = std::atoi(e);  // tuning knob
+  g.threads = (int)std::min<int64_t>(std::min<int64_t>(max_threads, 32 * ST25_MAXW), chunks);
   g.CPT = (int)(chunks / g.threads);
   if (g.CPT > ST25_CPT_MAX || g.threads < 32) return false;
   g.TJ = (int)TJ;
@@ -170,11 +172,11 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   auto bytes = [&]() {
     return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)4 * pe * ring_tsize);
   };
-  // stages in [2 (4 for identity operands), 4]: the most CTAs per SM (228 KB
-  // of shared memory, ~4 KB static + 1 KB reserved per CTA), then the most stages
-  auto ctas = [&]() { return (int)((228 * 1024) / (bytes() + 5 * 1024)); };
+  // stages in [2 (3 for identity operands), 4]: the most CTAs per SM (228 KB
+  // of shared memory, ~5 KB static + 1 KB reserved per CTA), then the most stages
+  auto ctas = [&]() { return (int)((228 * 1024) / (bytes() + 6 * 1024)); };
   int best = g.stages, bc = ctas();
-  for (int st = g.stages - 1; st >= (ident ? 4 : 2); --st) {
+  for (int st = g.stages - 1; st >= (ident ? 3 : 2); --st) {
     g.stages = st;
     if (ctas() > bc) {
       bc = ctas();

@@ -393,6 +393,17 @@ __device__ __forceinline__ SmemSrc<T> stage_window(const T* __restrict__ x, cons
   return SmemSrc<T>{w, lo};
 }
 
+// acc + a * b for binary16 a, b in binary32 arithmetic, one instruction
+// (FHFMA, sm_100): the product of two binary16 values is exact in binary32
+// (11 + 11 <= 24 significand bits, exponents in range), so the single
+// rounding of the fused op IS the reference's round(acc + round(a * b)) --
+// the same bits as __fadd_rn(acc, __fmul_rn(a, b)), signed zeros included.
+__device__ __forceinline__ float fhfma(__half a, __half b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(__half_as_ushort(a)), "h"(__half_as_ushort(b)), "f"(c));
+  return d;
+}
+
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
   // PACKED: binary32 folds may pair the products (FMUL2, fold_vec in
@@ -400,16 +411,24 @@ struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
   // mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 (a single rounding) despite
   // .rn and -fmad=false, which would break the reference's two-rounding fold;
   // FMUL2 + scalar FADD is never contracted (checked in the SASS).
-  static constexpr bool PACKED = std::is_same<C, float>::value, NEG = false;
+  // EXACT_H: binary16 operands in binary32 arithmetic. The coefficients are
+  // u_r = binary16 values too (rounded_copy, inner_solver.cpp:41-45), so each
+  // product is exact and the fold is one FHFMA per entry (see fhfma).
+  static constexpr bool EXACT_H = std::is_same<C, float>::value && std::is_same<T, __half>::value;
+  static constexpr bool PACKED = std::is_same<C, float>::value && !EXACT_H, NEG = false;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
-    return Ar<C>::add(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
+    if constexpr (EXACT_H) return fhfma(__float2half_rn(coef), xv, a);
+    else return Ar<C>::add(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <class C, class T>
 struct ResidF {  // acc - coef * x (kernels.cpp:63-66)
-  static constexpr bool PACKED = std::is_same<C, float>::value, NEG = true;
+  // EXACT_H: acc - c x = round(acc + (-c) x), -c exact (see MatvecF)
+  static constexpr bool EXACT_H = std::is_same<C, float>::value && std::is_same<T, __half>::value;
+  static constexpr bool PACKED = std::is_same<C, float>::value && !EXACT_H, NEG = true;
   __device__ __forceinline__ C operator()(C a, C coef, T xv) const {
-    return Ar<C>::sub(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
+    if constexpr (EXACT_H) return fhfma(__float2half_rn(-coef), xv, a);
+    else return Ar<C>::sub(a, Ar<C>::mul(coef, ld_c<T, C>(xv)));
   }
 };
 template <int P>

@@ -137,6 +137,92 @@ __device__ __forceinline__ void mul_vec(C a, const X (&x)[VEC], C (&out)[VEC]) {
   }
 }
 
+// ---------------------------------------------- binary16 lanes, packed
+// The binary16-storage / binary32-arithmetic operator passes keep 8 values
+// per 16-byte chunk as 4 packed 32-bit registers and never unpack them:
+// FHFMA / FHADD (sm_100) read either half of a register directly. Every
+// product on these paths multiplies two binary16 values, exact in binary32,
+// so a fused op rounds exactly once where the reference rounds the sum (see
+// fhfma in gadi_kernels.cuh): the bits are the reference's.
+template <int SA, int SB>  // SA / SB: which half (0 low, 1 high) of a / b
+__device__ __forceinline__ float fhf(uint32_t a, uint32_t b, float c) {
+  float d;
+  if constexpr (SA == 0 && SB == 0)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bl, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else if constexpr (SA == 0 && SB == 1)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bh, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else if constexpr (SA == 1 && SB == 0)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bl, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bh, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+// a.half(S) + c in binary32, one rounding (FHADD)
+template <int S>
+__device__ __forceinline__ float fhadd(uint32_t a, float c) {
+  float d;
+  if constexpr (S == 0)
+    asm("{.reg .f16 al, ah; mov.b32 {al, ah}, %1; add.rn.f32.f16 %0, al, %2;}" : "=f"(d) : "r"(a), "f"(c));
+  else
+    asm("{.reg .f16 al, ah; mov.b32 {al, ah}, %1; add.rn.f32.f16 %0, ah, %2;}" : "=f"(d) : "r"(a), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {  // two RN roundings (F2FP)
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ uint32_t u4_at(const uint4& u, int k) {
+  return k == 0 ? u.x : k == 1 ? u.y : k == 2 ? u.z : u.w;
+}
+__device__ __forceinline__ uint4 lds_u4(const void* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void sts_u4(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// acc[e] += c * x[e + SH] over one chunk, c in the low half of `c`;
+// SH = -1 / +1 take the k-1 / k+1 neighbours: x[-1] = edge (its low half),
+// x[8] = edge. A missing edge neighbour passes the coefficient's neutral
+// operand (nh_of), whose product is -0: acc + -0 == acc for every acc.
+template <int SH>
+__device__ __forceinline__ void fold8h(float (&a)[8], uint32_t c, const uint4& x, uint32_t edge) {
+  const uint32_t r[4] = {x.x, x.y, x.z, x.w};
+  if constexpr (SH == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[2 * k] = fhf<0, 0>(c, r[k], a[2 * k]);
+      a[2 * k + 1] = fhf<0, 1>(c, r[k], a[2 * k + 1]);
+    }
+  } else if constexpr (SH < 0) {
+    a[0] = fhf<0, 0>(c, edge, a[0]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[2 * k + 1] = fhf<0, 0>(c, r[k], a[2 * k + 1]);
+      if (k < 3) a[2 * k + 2] = fhf<0, 1>(c, r[k], a[2 * k + 2]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[2 * k] = fhf<0, 1>(c, r[k], a[2 * k]);
+      if (k < 3) a[2 * k + 1] = fhf<0, 0>(c, r[k + 1], a[2 * k + 1]);
+    }
+    a[7] = fhf<0, 0>(c, edge, a[7]);
+  }
+}
+// the operand whose product with coefficient c is -0 (sign(c) XOR sign(-0))
+__device__ __forceinline__ uint32_t nh_of(uint32_t c) { return (c & 0x8000u) ^ 0x8000u; }
+// pairwise sum of the 8 exact products a[e] * b[e] (kernels.cpp:33-39): each
+// first-level node RN(a0 b0 + a1 b1) is one FHFMA onto the exact product
+// a1 b1 (an FHFMA onto -0, which returns it unchanged)
+__device__ __forceinline__ float dot8h(const uint4& a, const uint4& b) {
+  const uint32_t x[4] = {a.x, a.y, a.z, a.w}, y[4] = {b.x, b.y, b.z, b.w};
+  float s[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s[k] = fhf<0, 0>(x[k], y[k], fhf<1, 1>(x[k], y[k], -0.0f));
+  return __fadd_rn(__fadd_rn(s[0], s[1]), __fadd_rn(s[2], s[3]));
+}
+
 struct St25Geo {
   int n, lg;      // points per direction (power of two), log2 n
   int TJ, lgTJ;   // rows per tile
@@ -154,16 +240,20 @@ struct St25Geo {
 
 constexpr int ST25_CPT_MAX = 4;
 constexpr int ST25_IL_MAX = 32;  // planes per CTA (make_st25)
+constexpr int ST25_MAXW = 16;    // warps per CTA
 
 // ------------------------------------------------------------ the kernel
 template <class P, int CPT>
-__global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd, DevState* st) {
+__global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd, DevState* st) {
   using T = typename P::T;
   using Acc = typename P::Acc;
   using R0 = typename P::R0;
   using RT = typename P::RT;  // operand ring element: C when widening binary16 is free, else T
   static_assert(!P::IDENT || std::is_same<RT, T>::value, "identity operands are folded from the stages");
   constexpr int VEC = 16 / sizeof(T);
+  // packed binary16 path (fold8h / dot8h): binary16 operands, binary32
+  // arithmetic, exact products
+  constexpr bool FASTH = P::FASTH;
   if (pol_in.skip(st)) return;
   P pol = pol_in;
   pol.prepare(st);  // device-resident scalars (e.g. CG beta) the host never sees
@@ -182,7 +272,7 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   // per-(plane, warp) partial sums, folded over the warps once after the
   // plane loop (no block barrier per plane for the reductions)
   static_assert(!(P::HAS_R0 && P::HAS_R1), "one reduced quantity per policy");
-  __shared__ double plb[ST25_IL_MAX * 8];  // R0 values are held exactly in binary64
+  __shared__ double plb[ST25_IL_MAX * ST25_MAXW];  // R0 values are held exactly in binary64
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int jt = blockIdx.x % g.njt, ic = blockIdx.x / g.njt;
@@ -218,20 +308,41 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
     const int nch = (rhi - rlo + 1) << g.lgTR;
     for (int c = tid; c < nch; c += blockDim.x) {
       const int idx = soff + c * VEC;
-      RT v[VEC];
-      pol.make(rs, pe, idx, v);
-      sts_vec<RT, VEC>(o + idx, v);
+      if constexpr (FASTH) {
+        sts_u4(o + idx, pol.make_h(rs, pe, idx));
+      } else {
+        RT v[VEC];
+        pol.make(rs, pe, idx, v);
+        sts_vec<RT, VEC>(o + idx, v);
+      }
     }
   };
 
   // IDENT policies (the operand is input 0 as stored: residuals) fold
-  // straight from the staged planes: S >= 4 stages hold planes i-1, i, i+1
-  // while i+2.. are in flight, and no operand ring is built.
+  // straight from the staged planes, and no operand ring is built.
   auto stage_of = [&](int q) { return raw + (size_t)((q - qlo) % S) * P::NIN * pe; };
   auto wait_q = [&](int q) { mbar_wait(&bar[(q - qlo) % S], (uint32_t)(((q - qlo) / S) & 1)); };
+  // IDENT: each thread keeps its own chunks of planes i-1 and i+1 in
+  // registers, so only plane i must stay staged while it is folded: stage
+  // i is refilled right after its fold, and S-2 planes stay in flight.
+  RT xprv[CPT][VEC], xnxt[CPT][VEC];
+  auto own_sidx = [&](int rr) {
+    const int c = ((warp * CPT + rr) << 5) + lane;
+    return ((c >> g.lgTR) + 1) * n + (c & (g.TR - 1)) * VEC;
+  };
   if constexpr (P::IDENT) {
-    if (ib - 1 >= 0) wait_q(ib - 1);
+    if (ib - 1 >= 0) {
+      wait_q(ib - 1);
+      const RT* sp = stage_of(ib - 1);
+#pragma unroll
+      for (int rr = 0; rr < CPT; ++rr) lds_vec<RT, VEC>(sp + own_sidx(rr), xprv[rr]);
+    }
     wait_q(ib);
+    __syncthreads();  // stage ib-1 is consumed
+    if (tid == 0 && ib - 1 >= qlo && ib - 1 + S <= qhi) {
+      fence_proxy_async();
+      issue(ib - 1 + S);
+    }
   } else {
     if (ib - 1 >= 0) build(ib - 1);
     build(ib);
@@ -271,10 +382,15 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
     }
     const RT *om, *oc, *op;
     if constexpr (P::IDENT) {
-      if (i + 1 <= n - 1) wait_q(i + 1);
-      om = i > 0 ? stage_of(i - 1) : nullptr;
+      if (i + 1 <= n - 1) {
+        wait_q(i + 1);
+        const RT* sp = stage_of(i + 1);
+#pragma unroll
+        for (int rr = 0; rr < CPT; ++rr) lds_vec<RT, VEC>(sp + own_sidx(rr), xnxt[rr]);
+      }
+      om = i > 0 ? stage_of(i) : nullptr;  // non-null marks presence; the values are xprv / xnxt
       oc = stage_of(i);
-      op = i < n - 1 ? stage_of(i + 1) : nullptr;
+      op = i < n - 1 ? stage_of(i) : nullptr;
     } else {
       if (i + 1 <= n - 1) build(i + 1);
       __syncthreads();
@@ -296,6 +412,26 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
         const int j = j0 + jl;
         const int sidx = (jl + 1) * n + k0;
         const int64_t e0 = (int64_t)i * g.nn + (int64_t)j * n + k0;
+        if constexpr (FASTH) {
+          float acc[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) acc[v] = 0.0f;  // matvec folds start from +0 (kernels.cpp:46)
+          const uint32_t* ch = pol.ch;  // coefficients, binary16 in the low halves
+          const unsigned short* ocu = reinterpret_cast<const unsigned short*>(oc);
+          const uint4 ccu = lds_u4(oc + sidx);
+          // the seven neighbours in stored-column order; absent i / j
+          // neighbours are skipped, absent k neighbours fold the neutral -0 product
+          if (om) fold8h<0>(acc, ch[0], lds_u4(om + sidx), 0u);
+          if (j > 0) fold8h<0>(acc, ch[1], lds_u4(oc + sidx - n), 0u);
+          fold8h<-1>(acc, ch[2], ccu, k0 > 0 ? (uint32_t)ocu[sidx - 1] : nh_of(ch[2]));
+          fold8h<0>(acc, ch[3], ccu, 0u);
+          fold8h<1>(acc, ch[4], ccu, k0 + VEC < n ? (uint32_t)ocu[sidx + VEC] : nh_of(ch[4]));
+          if (j < n - 1) fold8h<0>(acc, ch[5], lds_u4(oc + sidx + n), 0u);
+          if (op) fold8h<0>(acc, ch[6], lds_u4(op + sidx), 0u);
+          R0 c0 = pol.epi_h(e0, acc, ccu);
+          a0[rr] = warp_tree(c0, 32);
+          continue;
+        }
         Acc acc[VEC];
         if constexpr (P::IDENT) {
 #pragma unroll
@@ -310,8 +446,11 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
         // the seven neighbours in stored-column order; an absent neighbour is
         // skipped, never folded as a zero (fold_vec restores acc there)
         if (om) {
-          lds_vec<RT, VEC>(om + sidx, nb);
-          fold_vec(f, acc, c7[0], nb, false, false);
+          if constexpr (P::IDENT) fold_vec(f, acc, c7[0], xprv[rr], false, false);
+          else {
+            lds_vec<RT, VEC>(om + sidx, nb);
+            fold_vec(f, acc, c7[0], nb, false, false);
+          }
         }
         if (j > 0) {
           lds_vec<RT, VEC>(oc + sidx - n, nb);
@@ -334,8 +473,15 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
           fold_vec(f, acc, c7[5], nb, false, false);
         }
         if (op) {
-          lds_vec<RT, VEC>(op + sidx, nb);
-          fold_vec(f, acc, c7[6], nb, false, false);
+          if constexpr (P::IDENT) fold_vec(f, acc, c7[6], xnxt[rr], false, false);
+          else {
+            lds_vec<RT, VEC>(op + sidx, nb);
+            fold_vec(f, acc, c7[6], nb, false, false);
+          }
+        }
+        if constexpr (P::IDENT) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) xprv[rr][v] = cc[v];
         }
         R0 c0 = Ar<R0>::zero();
         double d0 = 0.0;
@@ -357,10 +503,10 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
       if (P::HAS_R1) plb[(i - ib) * nw + warp] = a1[0];
     }
     if constexpr (P::IDENT) {
-      __syncthreads();  // plane i-1 is no longer read: refill its stage
-      if (tid == 0 && i - 1 >= qlo && i - 1 + S <= qhi) {
+      __syncthreads();  // plane i is no longer read (plane i+1 folds it from xprv): refill its stage
+      if (tid == 0 && i + S <= qhi) {
         fence_proxy_async();
-        issue(i - 1 + S);
+        issue(i + S);
       }
     }
   }
@@ -369,18 +515,18 @@ __global__ void __launch_bounds__(256) k_st25(const P pol_in, St25Geo g, Red rd,
   if (P::HAS_R0 || P::HAS_R1) {
     __syncthreads();
     for (int t = tid; t < g.IL; t += blockDim.x) {
-      R0 v0[8];
-      double v1[8];
+      R0 v0[ST25_MAXW];
+      double v1[ST25_MAXW];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < ST25_MAXW; ++k)
         if (k < nw) {
           if (P::HAS_R0) v0[k] = from_dbl<R0>(plb[t * nw + k]);
           if (P::HAS_R1) v1[k] = plb[t * nw + k];
         }
 #pragma unroll
-      for (int s2 = 1; s2 < 8; s2 <<= 1)
+      for (int s2 = 1; s2 < ST25_MAXW; s2 <<= 1)
 #pragma unroll
-        for (int k = 0; k + s2 < 8; k += 2 * s2)
+        for (int k = 0; k + s2 < ST25_MAXW; k += 2 * s2)
           if (k + s2 < nw) {
             if (P::HAS_R0) v0[k] = Ar<R0>::add(v0[k], v0[k + s2]);
             if (P::HAS_R1) v1[k] = __dadd_rn(v1[k], v1[k + s2]);
@@ -451,6 +597,7 @@ struct PolSpmvp {
   using RT = typename RingOf<T, C>::type;
   static constexpr int NIN = 2;
   static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
+  static constexpr bool FASTH = std::is_same<T, __half>::value && std::is_same<C, float>::value;
   C c7[7];
   const T* r;
   const T* p_in;
@@ -458,8 +605,35 @@ struct PolSpmvp {
   T* q;
   C beta;
   int first;
+  uint32_t ch[7];  // FASTH: c7 as binary16 (exact: the coefficients are u_r values)
   __device__ bool skip(DevState* st) const { return *(volatile int*)&st->cg_done; }
-  __device__ void prepare(DevState* st) { beta = from_dbl<C>(st->cg_beta); }
+  __device__ void prepare(DevState* st) {
+    beta = from_dbl<C>(st->cg_beta);
+    if constexpr (FASTH)
+      for (int k = 0; k < 7; ++k) ch[k] = __half_as_ushort(__float2half_rn(c7[k]));
+  }
+  // FASTH: p = r + beta p as FMUL2 products + FHADD sums, one F2FP per pair
+  __device__ uint4 make_h(const T* rs, int pe, int idx) const {
+    const uint4 rv = lds_u4(rs + idx);
+    if (first) return rv;
+    const uint4 pv = lds_u4(rs + pe + idx);
+    const float2 b2 = make_float2(beta, beta);
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t pk = u4_at(pv, k), rk = u4_at(rv, k);
+      const float2 bp = __fmul2_rn(b2, __half22float2(*reinterpret_cast<const __half2*>(&pk)));
+      o[k] = pack_h2(fhadd<0>(rk, bp.x), fhadd<1>(rk, bp.y));
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& pc) const {
+    const uint4 qv = make_uint4(pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), pack_h2(acc[4], acc[5]),
+                                pack_h2(acc[6], acc[7]));
+    *reinterpret_cast<uint4*>(q + e0) = qv;
+    *reinterpret_cast<uint4*>(p_out + e0) = pc;
+    return dot8h(pc, qv);
+  }
   __device__ int nin() const { return first ? 1 : 2; }
   __device__ const T* in(int k) const { return k == 0 ? r : p_in; }
   __device__ void make(const T* rs, int pe, int idx, RT (&v)[ST25_VEC]) const {
@@ -509,14 +683,41 @@ struct PolGmMatvec {
   using RT = typename RingOf<T, C>::type;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = true, HAS_R1 = false, HAS_MAX = false, HAS_FLAG = false, IDENT = false;
+  static constexpr bool FASTH = std::is_same<T, __half>::value && std::is_same<C, float>::value;
   C c7[7];
   const T* wprev;
   double inv;
   T* vj;
   const T* v0;
   T* w;
+  uint32_t ch[7];
   __device__ bool skip(DevState*) const { return false; }
-  __device__ void prepare(DevState*) {}
+  __device__ void prepare(DevState*) {
+    if constexpr (FASTH)
+      for (int k = 0; k < 7; ++k) ch[k] = __half_as_ushort(__float2half_rn(c7[k]));
+  }
+  // FASTH: v = round(inv * w) with the product in binary64 (scale, kernels.cpp:166-171)
+  __device__ uint4 make_h(const T* rs, int, int idx) const {
+    const uint4 wv = lds_u4(rs + idx);
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t wk = u4_at(wv, k);
+      const float2 wf = __half22float2(*reinterpret_cast<const __half2*>(&wk));
+      const __half2 v = __halves2half2(__double2half(__dmul_rn(inv, (double)wf.x)),
+                                       __double2half(__dmul_rn(inv, (double)wf.y)));
+      o[k] = *reinterpret_cast<const uint32_t*>(&v);
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& vc) const {
+    const uint4 wq = make_uint4(pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), pack_h2(acc[4], acc[5]),
+                                pack_h2(acc[6], acc[7]));
+    *reinterpret_cast<uint4*>(vj + e0) = vc;
+    *reinterpret_cast<uint4*>(w + e0) = wq;
+    const uint4 v0u = vj == v0 ? vc : __ldg(reinterpret_cast<const uint4*>(v0 + e0));
+    return dot8h(wq, v0u);
+  }
   __device__ int nin() const { return 1; }
   __device__ const T* in(int) const { return wprev; }
   __device__ void make(const T* rs, int, int idx, RT (&v)[ST25_VEC]) const {
@@ -567,6 +768,7 @@ struct PolGmResid {
   using RT = TS;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = true, IDENT = true;
+  static constexpr bool FASTH = false;
   C c7[7];
   const T* x;
   const T* rhs;
@@ -611,6 +813,7 @@ struct PolResidA {
   using RT = double;
   static constexpr int NIN = 1;
   static constexpr bool HAS_R0 = false, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false, IDENT = true;
+  static constexpr bool FASTH = false;
   double c7[7];
   const double* x;
   const double* b;
