@@ -129,7 +129,16 @@ __device__ __forceinline__ bool finite_t(T v) {
 // VEC * sizeof(T) == 16 on the aligned path (one 128-bit access).
 template <class T, int VEC>
 __device__ __forceinline__ void ld_vec(const T* __restrict__ p, int64_t e0, T (&v)[VEC]) {
-  if constexpr (VEC * sizeof(T) == 16) {
+  if constexpr (VEC * sizeof(T) > 16 && VEC * sizeof(T) % 16 == 0) {  // several 128-bit accesses
+    constexpr int per = 16 / sizeof(T);
+#pragma unroll
+    for (int b = 0; b < VEC / per; ++b) {
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(p + e0) + b);
+      const T* t = reinterpret_cast<const T*>(&u);
+#pragma unroll
+      for (int i = 0; i < per; ++i) v[b * per + i] = t[i];
+    }
+  } else if constexpr (VEC * sizeof(T) == 16) {
     uint4 u = __ldg(reinterpret_cast<const uint4*>(p + e0));
     const T* t = reinterpret_cast<const T*>(&u);
 #pragma unroll
@@ -151,7 +160,17 @@ __device__ __forceinline__ void ld_vec(const T* __restrict__ p, int64_t e0, T (&
 }
 template <class T, int VEC>
 __device__ __forceinline__ void st_vec(T* __restrict__ p, int64_t e0, const T (&v)[VEC]) {
-  if constexpr (VEC * sizeof(T) == 16) {
+  if constexpr (VEC * sizeof(T) > 16 && VEC * sizeof(T) % 16 == 0) {
+    constexpr int per = 16 / sizeof(T);
+#pragma unroll
+    for (int b = 0; b < VEC / per; ++b) {
+      uint4 u;
+      T* t = reinterpret_cast<T*>(&u);
+#pragma unroll
+      for (int i = 0; i < per; ++i) t[i] = v[b * per + i];
+      reinterpret_cast<uint4*>(p + e0)[b] = u;
+    }
+  } else if constexpr (VEC * sizeof(T) == 16) {
     uint4 u;
     T* t = reinterpret_cast<T*>(&u);
 #pragma unroll

@@ -529,10 +529,15 @@ __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int ma
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-      const C cv = ld_c<T, C>(v[i]);
-      tc[i] = Ar<C>::mul(cv, cv);
-      const double dv = to_dbl(v[i]);
-      td[i] = __dmul_rn(dv, dv);
+      if constexpr (MatvecF<C, T>::EXACT_H) {  // the square of a binary16 value is exact in binary32
+        tc[i] = fhfma(v[i], v[i], -0.0f);
+        td[i] = (double)tc[i];
+      } else {
+        const C cv = ld_c<T, C>(v[i]);
+        tc[i] = Ar<C>::mul(cv, cv);
+        const double dv = to_dbl(v[i]);
+        td[i] = __dmul_rn(dv, dv);
+      }
     }
     c = seg_sum<C, G>(tc, s.len);
     d = seg_sum<double, G>(td, s.len);
@@ -633,11 +638,19 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
       const C x0 = first ? Ar<C>::zero() : ld_c<T, C>(xv[i]);
       xv[i] = st_t<T, C>(Ar<C>::add(x0, Ar<C>::mul(a, ld_c<T, C>(pv[i]))));
       rv[i] = st_t<T, C>(Ar<C>::add(ld_c<T, C>(rv[i]), Ar<C>::mul(na, ld_c<T, C>(qv[i]))));
-      const C rc = ld_c<T, C>(rv[i]);
-      tc[i] = Ar<C>::mul(rc, rc);
-      const double dv = to_dbl(rv[i]);
-      td[i] = __dmul_rn(dv, dv);
-      if (GADI_LIVE(i)) bad |= (finite_t(rv[i]) ? 0 : 1) | (finite_t(xv[i]) ? 0 : 2);
+      if constexpr (MatvecF<C, T>::EXACT_H) {  // exact binary16 squares; finiteness from the bits
+        tc[i] = fhfma(rv[i], rv[i], -0.0f);
+        td[i] = (double)tc[i];
+        if (GADI_LIVE(i))
+          bad |= ((__half_as_ushort(rv[i]) & 0x7c00u) == 0x7c00u ? 1 : 0) |
+                 ((__half_as_ushort(xv[i]) & 0x7c00u) == 0x7c00u ? 2 : 0);
+      } else {
+        const C rc = ld_c<T, C>(rv[i]);
+        tc[i] = Ar<C>::mul(rc, rc);
+        const double dv = to_dbl(rv[i]);
+        td[i] = __dmul_rn(dv, dv);
+        if (GADI_LIVE(i)) bad |= (finite_t(rv[i]) ? 0 : 1) | (finite_t(xv[i]) ? 0 : 2);
+      }
     }
     store_seg<T, VEC, G>(x, s, xv);
     store_seg<T, VEC, G>(r, s, rv);
@@ -673,8 +686,10 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
                                                   const T* __restrict__ rhs, T* __restrict__ r, Geo g, Red rd,
                                                   DevState* st, int64_t wband = 0) {
   GADI_G;
+  constexpr bool EH = MatvecF<C, T>::EXACT_H;
   int bad = 0;
   double m = 0.0;
+  unsigned mh = 0;  // EH: max |r| as binary16 magnitude bits (order preserving; NaN excluded)
   C w0;
   double w1;
   auto fin = [&](const Seg& s, double& d, const C (&acc)[G]) {
@@ -683,11 +698,20 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       rv[i] = st_t<T, C>(acc[i]);
-      const double dv = to_dbl(rv[i]);
-      td[i] = __dmul_rn(dv, dv);
-      if (GADI_LIVE(i)) {
-        bad |= finite_t(rv[i]) ? 0 : 1;
-        m = (dv == dv) ? fmax(m, fabs(dv)) : m;
+      if constexpr (EH) {  // no binary64 work but the exact square's widening
+        td[i] = (double)fhfma(rv[i], rv[i], -0.0f);
+        const unsigned mag = __half_as_ushort(rv[i]) & 0x7fffu;
+        if (GADI_LIVE(i)) {
+          bad |= mag >= 0x7c00u ? 1 : 0;
+          mh = (mag <= 0x7c00u && mag > mh) ? mag : mh;
+        }
+      } else {
+        const double dv = to_dbl(rv[i]);
+        td[i] = __dmul_rn(dv, dv);
+        if (GADI_LIVE(i)) {
+          bad |= finite_t(rv[i]) ? 0 : 1;
+          m = (dv == dv) ? fmax(m, fabs(dv)) : m;
+        }
       }
     }
     store_seg<T, VEC, G>(r, s, rv);
@@ -724,6 +748,7 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
     const PlainSrc<T> src{x};
     seg_run<VEC, false, true>(g, [&](const Seg& s, C&, double& d) { body(s, d, src); }, w0, w1);
   }
+  if constexpr (EH) m = (double)__half2float(__ushort_as_half((unsigned short)mh));
   block_max_abs(&st->maxbits, m);
   or_flags(&st->flags, bad);
   C dc;
