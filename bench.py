@@ -20,8 +20,10 @@ e2e    = the same solve through the C ABI gadi_cuda_solve with HOST buffers
          (pinned b in, x out; copies inside the timed region).
 roofline = the inner CG sweep (SpMV + axpys + dots, SURVEY §8(d) B_CG =
          11 N s_r bytes per iteration) against MEASURED_PEAKS.json hbm_gbs.
-Multi-GPU (torchrun): each rank solves its own full-size replica (weak
-scaling); the z-slab partition is not wired into this driver yet.
+Multi-GPU (torchrun, one rank per GPU): the workload is partitioned over the
+ranks -- z-slabs of the stencil grid, contiguous row blocks of the band CSR
+ -- with halo exchanges and rank-ordered reduction records over
+one NCCL communicator (strong scaling: the same problem at every N).
 """
 import argparse
 import json
@@ -258,12 +260,11 @@ def main():
                 "max_inner": wl["max_inner"], "tol_epsilon": wl["eps"], "xi": 1e-20,
                 "l2": "inputs larger than L2 (x, b: 8N bytes each)",
                 "parallelism": "single"}
-    # stencil workloads shard into z-slabs over the ranks (NCCL, strong
-    # scaling: the same n^3 problem on every N); the band CSR has no row-block
-    # sharding yet and runs one full replica per GPU (weak scaling)
-    sharded = world > 1 and wl.get("kind") != "band"
+    # the stencil shards into z-slabs, the band CSR into row blocks (NCCL,
+    # strong scaling: the same problem at every N)
+    sharded = world > 1
     if world > 1:
-        cfg_json["parallelism"] = f"zslab{world}" if sharded else f"replicas{world}"
+        cfg_json["parallelism"] = f"rowblock{world}" if band else f"zslab{world}"
     if band:
         cfg_json.update(k_off=wl["k_off"], band=wl["band"], matrix_seed=wl["mseed"])
     else:
@@ -371,7 +372,7 @@ def main():
                                                 if band else "inner CG iteration (spmv+p-update, axpys+dots)"),
                      "achieved": cg_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic if world == 1 else None,
-                     "algorithmic_bytes_per_iter": bytes_it, "per": "GPU (rank 0's slab)" if sharded else "GPU"},
+                     "algorithmic_bytes_per_iter": bytes_it, "per": "GPU (rank 0's shard)" if sharded else "GPU"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "solve": {"converged": ok, "outer_iters": reps[0].outer_iters, "final_rres": reps[0].final_rres,

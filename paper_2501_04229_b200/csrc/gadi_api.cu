@@ -52,9 +52,60 @@ void device_split(gadi_handle* h) {
   CK(cudaStreamSynchronize(s));
   for (void* p : {(void*)cnt, (void*)c64, (void*)trp, (void*)next, (void*)tci, (void*)tv}) cudaFree(p);
   h->launches += 7;
-  // SELL image of A for the binary64 residual (2 rows per lane: 16-byte loads)
-  build_sell_layout(s, N, ilog2(64), h->d_rpA, h->d_ciA, h->sellA, h->max_band < 32768);
-  h->sellA.val = fill_sell_values<double, P_DOUBLE>(s, N, h->sellA, h->d_rpA, h->d_vA, nullptr, nullptr, 0.0);
+}
+
+// SELL image of A for the binary64 residual (2 rows per lane: 16-byte loads)
+void build_sell_A(gadi_handle* h) {
+  build_sell_layout(h->stream, h->N, ilog2(64), h->d_rpA, h->d_ciA, h->sellA, h->max_band < 32768);
+  h->sellA.val = fill_sell_values<double, P_DOUBLE>(h->stream, h->N, h->sellA, h->d_rpA, h->d_vA, nullptr, nullptr,
+                                                    0.0);
+}
+
+// A CSR row block (sharded solves): the split ran on the window [lo, hi)^2
+// around the block; keep rows [a, b) of A and of the union pattern, columns
+// renumbered relative to row a (the block's first row: negative columns and
+// columns >= b - a address the ghost entries of the shard vectors).
+void crop_rows(gadi_handle* h, int64_t a, int64_t b) {
+  cudaStream_t s = h->stream;
+  const int64_t m = b - a;
+  auto crop = [&](int64_t*& rp, int32_t*& ci, std::vector<double**> vals, int64_t& nnz, int64_t* first) {
+    int64_t pa = 0, pb = 0;
+    CK(cudaMemcpy(&pa, rp + a, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&pb, rp + b, 8, cudaMemcpyDeviceToHost));
+    int64_t* nrp = dalloc<int64_t>(m + 1);
+    k_sub_i64<<<ew_grid(m + 1), 256, 0, s>>>(rp + a, nrp, m + 1, pa);
+    int32_t* nci = dalloc<int32_t>(pb - pa);
+    k_sub_i32<<<ew_grid(pb - pa), 256, 0, s>>>(ci + pa, nci, pb - pa, (int32_t)a);
+    CKL();
+    for (double** v : vals) {
+      double* nv = dalloc<double>(pb - pa);
+      CK(cudaMemcpyAsync(nv, *v + pa, (pb - pa) * 8, cudaMemcpyDeviceToDevice, s));
+      CK(cudaStreamSynchronize(s));
+      cudaFree(*v);
+      *v = nv;
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaFree(rp);
+    cudaFree(ci);
+    rp = nrp;
+    ci = nci;
+    nnz = pb - pa;
+    *first = pa;
+  };
+  int64_t pa = 0, ua = 0;
+  crop(h->d_rpA, h->d_ciA, {&h->d_vA}, h->nnzA, &pa);
+  crop(h->d_urp, h->d_uci, {&h->d_mv, &h->d_nv}, h->nnzHS, &ua);
+  int64_t* ndp = dalloc<int64_t>(m);
+  k_sub_i64<<<ew_grid(m), 256, 0, s>>>(h->d_dpos + a, ndp, m, ua);
+  uint8_t* ndi = dalloc<uint8_t>(m);
+  CK(cudaMemcpyAsync(ndi, h->d_din + a, m, cudaMemcpyDeviceToDevice, s));
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  cudaFree(h->d_dpos);
+  cudaFree(h->d_din);
+  h->d_dpos = ndp;
+  h->d_din = ndi;
+  h->N = m;
 }
 
 EngineBase* make_engine(gadi_handle* h, const gadi_inner_spec& sp, double a, double om, int ur, int acc) {
@@ -321,17 +372,33 @@ static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_op
   h->device = opts ? opts->device : 0;
   CK(cudaSetDevice(h->device));
   h->kind = d->kind;
+  // sharded CSR / band problems: rank's row block [r0, r1) of N/world rows;
+  // the split runs on the window [lo, hi) = the block +- the band
+  int64_t r0 = 0, r1 = 0, lo = 0, hi = 0;
   if (grp) {
     const int w = grp->world;
-    if (d->kind != GADI_PROBLEM_STENCIL7)
-      throw Err(GADI_E_UNSUPPORTED, "sharded solves: z-slabs of the 7-point stencil only (CSR row blocks: next)");
     if (w < 1 || w > GADI_MAX_RANKS || (w & (w - 1)) != 0)
       throw Err(GADI_E_PARAM, "sharded solves: world must be a power of two <= 64");
     if (rank < 0 || rank >= w) throw Err(GADI_E_PARAM, "sharded solves: rank out of range");
-    if (d->n % w != 0) throw Err(GADI_E_PARAM, "sharded solves: world must divide n");
+    if (d->kind == GADI_PROBLEM_STENCIL7 && d->n % w != 0)
+      throw Err(GADI_E_PARAM, "sharded solves: world must divide n");
+    if (d->kind != GADI_PROBLEM_STENCIL7 && (d->n_rows < w || d->n_rows % w != 0))
+      throw Err(GADI_E_PARAM, "sharded solves: world must divide n_rows");
     if (grp->nccl_rank >= 0 && grp->nccl_rank != rank)
       throw Err(GADI_E_PARAM, "sharded solves: an NCCL group holds this process's rank only");
+    h->world = w;
+    h->rank = rank;
+    if (d->kind != GADI_PROBLEM_STENCIL7) {
+      const int64_t m = d->n_rows / w;
+      r0 = rank * m;
+      r1 = r0 + m;
+    }
   }
+  auto set_window = [&](int64_t N, int64_t band) {
+    if (band > r1 - r0) throw Err(GADI_E_UNSUPPORTED, "sharded solves: the band exceeds a row block (fewer ranks)");
+    lo = std::max<int64_t>(0, r0 - band);
+    hi = std::min<int64_t>(N, r1 + band);
+  };
   if (d->kind == GADI_PROBLEM_STENCIL7) {
     if (d->n < 2) throw Err(GADI_E_CONTRACT, "convdiff3d: n >= 2 required");  // problems.cpp:10
     h->n = d->n;
@@ -372,36 +439,88 @@ static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_op
     for (int64_t i = 0; i < n; ++i)
       for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
         h->max_band = std::max<int64_t>(h->max_band, std::llabs(d->col_idx[k] - i));
-    h->N = n;
-    h->nnzA = d->nnz;
-    std::vector<int32_t> ci32(d->col_idx, d->col_idx + d->nnz);
-    h->d_rpA = dalloc<int64_t>(n + 1);
-    h->d_ciA = dalloc<int32_t>(d->nnz);
-    h->d_vA = dalloc<double>(d->nnz);
-    CK(cudaMemcpy(h->d_rpA, rp, (n + 1) * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_ciA, ci32.data(), d->nnz * 4, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_vA, d->values, d->nnz * 8, cudaMemcpyHostToDevice));
+    std::vector<int64_t> rpw;
+    std::vector<int32_t> ci32;
+    std::vector<double> vw;
+    if (grp) {  // the window [lo, hi)^2 around this rank's row block, columns shifted by -lo
+      set_window(n, h->max_band);
+      rpw.push_back(0);
+      for (int64_t i = lo; i < hi; ++i) {
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+          if (d->col_idx[k] >= lo && d->col_idx[k] < hi) {
+            ci32.push_back((int32_t)(d->col_idx[k] - lo));
+            vw.push_back(d->values[k]);
+          }
+        rpw.push_back((int64_t)ci32.size());
+      }
+    } else {
+      rpw.assign(rp, rp + n + 1);
+      ci32.assign(d->col_idx, d->col_idx + d->nnz);
+      vw.assign(d->values, d->values + d->nnz);
+    }
+    h->N = (int64_t)rpw.size() - 1;
+    h->nnzA = (int64_t)ci32.size();
+    h->d_rpA = dalloc<int64_t>(h->N + 1);
+    h->d_ciA = dalloc<int32_t>(h->nnzA);
+    h->d_vA = dalloc<double>(h->nnzA);
+    CK(cudaMemcpy(h->d_rpA, rpw.data(), (h->N + 1) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_ciA, ci32.data(), h->nnzA * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_vA, vw.data(), h->nnzA * 8, cudaMemcpyHostToDevice));
   } else if (d->kind == GADI_PROBLEM_BAND) {
     // BASELINE configs[3] generated on the device (bit for bit orc_band_csr)
     const int64_t n = d->n_rows;
     if (n < 2 || d->k_off < 1 || d->k_off > 31 || d->band < d->k_off || n - 1 < d->k_off)
       throw Err(GADI_E_CONTRACT, "band: need 1 <= k_off <= 31, band >= k_off, n_rows > k_off");
     if (n >= (int64_t(1) << 31)) throw Err(GADI_E_UNSUPPORTED, "band: n_rows must be < 2^31");
-    h->N = n;
     h->max_band = d->band;
-    h->nnzA = n * (int64_t)(d->k_off + 1);
-    h->d_rpA = dalloc<int64_t>(n + 1);
-    h->d_ciA = dalloc<int32_t>(h->nnzA);
-    h->d_vA = dalloc<double>(h->nnzA);
-    k_iota_scaled<<<ew_grid(n + 1), 256>>>(h->d_rpA, n + 1, d->k_off + 1);
-    k_band_gen<<<ew_grid(n), 256>>>(n, d->k_off, d->band, d->seed, h->d_ciA, h->d_vA);
+    if (grp) set_window(n, d->band);
+    else hi = n;
+    const int64_t rows = hi - lo, gnnz = rows * (int64_t)(d->k_off + 1);
+    h->d_rpA = dalloc<int64_t>(rows + 1);
+    h->d_ciA = dalloc<int32_t>(gnnz);
+    h->d_vA = dalloc<double>(gnnz);
+    k_iota_scaled<<<ew_grid(rows + 1), 256>>>(h->d_rpA, rows + 1, d->k_off + 1);
+    k_band_gen<<<ew_grid(rows), 256>>>(n, d->k_off, d->band, d->seed, h->d_ciA, h->d_vA, lo, rows);
     CKL();
     CK(cudaDeviceSynchronize());
+    h->N = rows;
+    h->nnzA = gnnz;
+    if (grp) {  // rows [lo, hi) restricted to the columns [lo, hi), shifted by -lo
+      int64_t* cnt = dalloc<int64_t>(rows + 1);
+      CK(cudaMemset(cnt + rows, 0, 8));
+      k_window_count<<<ew_grid(rows), 256>>>(h->d_rpA, h->d_ciA, rows, lo, hi, cnt);
+      CKL();
+      int64_t* nrp = dalloc<int64_t>(rows + 1);
+      scan_i64(nullptr, cnt, nrp, rows + 1);
+      CK(cudaMemcpy(&h->nnzA, nrp + rows, 8, cudaMemcpyDeviceToHost));
+      int32_t* nci = dalloc<int32_t>(h->nnzA);
+      double* nv = dalloc<double>(h->nnzA);
+      k_window_fill<<<ew_grid(rows), 256>>>(h->d_rpA, h->d_ciA, h->d_vA, rows, lo, hi, nrp, nci, nv);
+      CKL();
+      CK(cudaDeviceSynchronize());
+      for (void* p : {(void*)cnt, (void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA}) cudaFree(p);
+      h->d_rpA = nrp;
+      h->d_ciA = nci;
+      h->d_vA = nv;
+    }
   } else {
     throw Err(GADI_E_CONTRACT, "unknown problem kind");
   }
   CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  if (!h->stencil()) device_split(h.get());
+  if (!h->stencil()) {
+    device_split(h.get());
+    if (grp) {
+      crop_rows(h.get(), r0 - lo, r1 - lo);
+      h->row0 = r0;
+      h->gh = (h->max_band + 7) & ~int64_t(7);  // >= the band; a multiple of 8 keeps 16-byte windows aligned
+      if (h->gh > h->N) throw Err(GADI_E_UNSUPPORTED, "sharded solves: the band exceeds a row block (fewer ranks)");
+      if (grp->local)
+        h->comm.reset(new LocalComm(grp->local.get(), rank));
+      else
+        h->comm.reset(new NcclComm(grp->world, rank, grp->id));
+    }
+    build_sell_A(h.get());
+  }
   const int64_t N = h->N;
   h->d_x = hvec<double>(h.get());
   h->d_b = hvec<double>(h.get());

@@ -113,10 +113,13 @@ __global__ void k_sell_zflags(int64_t N, int lgSR, const int64_t* __restrict__ s
 
 // ------------------------------------------------------------ generator
 #define GADI_VALSALT 0x5851F42D4C957F2Dull
+// rows [row0, row0 + rows) of the N x N matrix (global columns), row i - row0
+// at (i - row0) * (k_off + 1): a row block generates its own rows (+ the band)
 static __global__ void k_band_gen(int64_t N, int k_off, int64_t band, uint64_t seed, int32_t* __restrict__ ci,
-                           double* __restrict__ v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N) return;
+                                  double* __restrict__ v, int64_t row0, int64_t rows) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows) return;
+  const int64_t i = row0 + t;
   int64_t cols[32];
   int cnt = 0;
   for (uint64_t draw = 0; cnt < k_off && draw < (1u << 20); ++draw) {
@@ -138,7 +141,7 @@ static __global__ void k_band_gen(int64_t N, int k_off, int64_t band, uint64_t s
     }
     cols[b + 1] = key;
   }
-  const int64_t base = i * (int64_t)(k_off + 1);
+  const int64_t base = t * (int64_t)(k_off + 1);
   double sum = 0.0;
   int64_t dpos = -1, w = base;
   int slot = 0;
@@ -167,6 +170,43 @@ static __global__ void k_iota_scaled(int64_t* __restrict__ rp, int64_t n, int64_
 static __global__ void k_i32_to_i64(const int* __restrict__ a, int64_t* __restrict__ b, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = a[i];
+}
+
+// ------------------------------------------------------------ row blocks
+// The square window [lo, hi)^2 of a CSR holding rows [lo, hi) with global
+// columns (a sharded row block's rows plus the band on each side): per-row
+// counts of the columns inside, then the entries with columns shifted by -lo.
+static __global__ void k_window_count(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t rows,
+                                      int64_t lo, int64_t hi, int64_t* __restrict__ cnt) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int64_t c = 0;
+  for (int64_t k = rp[r]; k < rp[r + 1]; ++k) c += (ci[k] >= lo && ci[k] < hi) ? 1 : 0;
+  cnt[r] = c;
+}
+static __global__ void k_window_fill(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                     const double* __restrict__ v, int64_t rows, int64_t lo, int64_t hi,
+                                     const int64_t* __restrict__ nrp, int32_t* __restrict__ nci,
+                                     double* __restrict__ nv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int64_t w = nrp[r];
+  for (int64_t k = rp[r]; k < rp[r + 1]; ++k)
+    if (ci[k] >= lo && ci[k] < hi) {
+      nci[w] = (int32_t)(ci[k] - lo);
+      nv[w] = v[k];
+      ++w;
+    }
+}
+// out[i] = in[i] - d (row pointers / entry positions of a cropped row range)
+static __global__ void k_sub_i64(const int64_t* __restrict__ in, int64_t* __restrict__ out, int64_t n, int64_t d) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i] - d;
+}
+// out[k] = in[k] - d (column indices relative to a cropped row range's first row)
+static __global__ void k_sub_i32(const int32_t* __restrict__ in, int32_t* __restrict__ out, int64_t n, int32_t d) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = in[k] - d;
 }
 
 // ------------------------------------------------------------ transpose

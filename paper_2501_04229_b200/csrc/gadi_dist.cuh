@@ -11,8 +11,9 @@
 //    k_dist_finish folds them in rank order -- bit for bit the single-device
 //    value -- and applies the reduction's epilogue identically on all ranks,
 //    so every rank takes the same control-flow decisions;
-//  * halo: a vector's first / last interior planes into the neighbours'
-//    ghost planes before a stencil pass reads them.
+//  * halo: a vector's first / last owned entries (one plane of a z-slab,
+//    the band of a CSR row block) into the neighbours' ghost entries before
+//    an operator pass reads them.
 //
 // Two transports implement them: LocalComm (ranks are threads of one
 // process, on one or several devices: device copies ordered by CUDA events,
@@ -39,9 +40,11 @@ struct Comm {
   virtual ~Comm() = default;
   // dst[4*r + k] = rank r's src[k], k < 4 (device pointers, stream ordered)
   virtual void allgather4(const double* src, double* dst, cudaStream_t s) = 0;
-  // ghost planes of a slab vector: interior - plane <- rank-1's last plane,
-  // interior + nplanes*plane <- rank+1's first plane (plane = bytes per plane)
-  virtual void halo(char* interior, int64_t plane, int64_t nplanes, cudaStream_t s) = 0;
+  // ghost entries of a shard vector (len bytes of owned entries, `ghost`
+  // bytes of ghosts on each side, ghost <= len): interior - ghost <- rank-1's
+  // last ghost bytes, interior + len <- rank+1's first ghost bytes. Stencil
+  // slabs exchange one plane; CSR row blocks the band of x entries.
+  virtual void halo(char* interior, int64_t ghost, int64_t len, cudaStream_t s) = 0;
 };
 
 // ------------------------------------------------------------ local group
@@ -111,18 +114,17 @@ struct LocalComm final : Comm {
     }
     g->barrier();  // every rank has read the slots before they are republished
   }
-  void halo(char* interior, int64_t plane, int64_t nplanes, cudaStream_t s) override {
+  void halo(char* interior, int64_t ghost, int64_t len, cudaStream_t s) override {
     publish(interior, s);
     if (rank > 0) {
       const LocalGroup::Slot sl = g->slots[rank - 1];
       cudaStreamWaitEvent(s, sl.ev, 0);
-      cudaMemcpyAsync(interior - plane, static_cast<const char*>(sl.p) + (nplanes - 1) * plane, plane,
-                      cudaMemcpyDefault, s);
+      cudaMemcpyAsync(interior - ghost, static_cast<const char*>(sl.p) + len - ghost, ghost, cudaMemcpyDefault, s);
     }
     if (rank + 1 < world) {
       const LocalGroup::Slot sl = g->slots[rank + 1];
       cudaStreamWaitEvent(s, sl.ev, 0);
-      cudaMemcpyAsync(interior + nplanes * plane, sl.p, plane, cudaMemcpyDefault, s);
+      cudaMemcpyAsync(interior + len, sl.p, ghost, cudaMemcpyDefault, s);
     }
     g->barrier();
   }
@@ -200,16 +202,16 @@ struct NcclComm final : Comm {
   void allgather4(const double* src, double* dst, cudaStream_t s) override {
     check(NcclApi::get().all_gather(src, dst, 4, kDouble, comm, s), "ncclAllGather");
   }
-  void halo(char* interior, int64_t plane, int64_t nplanes, cudaStream_t s) override {
+  void halo(char* interior, int64_t ghost, int64_t len, cudaStream_t s) override {
     NcclApi& a = NcclApi::get();
     check(a.group_start(), "ncclGroupStart");
     if (rank > 0) {
-      check(a.send(interior, (size_t)plane, kChar, rank - 1, comm, s), "ncclSend");
-      check(a.recv(interior - plane, (size_t)plane, kChar, rank - 1, comm, s), "ncclRecv");
+      check(a.send(interior, (size_t)ghost, kChar, rank - 1, comm, s), "ncclSend");
+      check(a.recv(interior - ghost, (size_t)ghost, kChar, rank - 1, comm, s), "ncclRecv");
     }
     if (rank + 1 < world) {
-      check(a.send(interior + (nplanes - 1) * plane, (size_t)plane, kChar, rank + 1, comm, s), "ncclSend");
-      check(a.recv(interior + nplanes * plane, (size_t)plane, kChar, rank + 1, comm, s), "ncclRecv");
+      check(a.send(interior + len - ghost, (size_t)ghost, kChar, rank + 1, comm, s), "ncclSend");
+      check(a.recv(interior + len, (size_t)ghost, kChar, rank + 1, comm, s), "ncclRecv");
     }
     check(a.group_end(), "ncclGroupEnd");
   }

@@ -282,7 +282,8 @@ struct gadi_handle {
   double stop_norm = 1.0;
   std::vector<double> history;
   // sharded solves (gadi_dist.cuh): this rank's z-slab [i0, i1) of the n
-  // planes; every slab vector has gh = n^2 ghost entries on each side
+  // planes (every slab vector has gh = n^2 ghost entries on each side), or
+  // its CSR row block [row0, row0 + N) (gh = the band)
   int world = 1, rank = 0;
   int64_t i0 = 0, i1 = 0, gh = 0;
   std::unique_ptr<gadi_host::Comm> comm;
@@ -291,7 +292,8 @@ struct gadi_handle {
 
   bool stencil() const { return kind == GADI_PROBLEM_STENCIL7; }
   bool sharded() const { return comm != nullptr; }
-  int64_t e_off() const { return i0 * n * n; }  // global index of local entry 0
+  int64_t row0 = 0;  // CSR row block: first owned row
+  int64_t e_off() const { return stencil() ? i0 * n * n : row0; }  // global index of local entry 0
 };
 
 namespace gadi_host {
@@ -397,12 +399,13 @@ inline void coll_flags(gadi_handle* h, int* flags) {
   k_dist_pack<<<1, 1, 0, h->stream>>>(h->st, flags);
   coll<double>(h, EpiNone{flags});
 }
-// the ghost planes of a slab vector before a stencil pass reads them
+// the ghost entries of a shard vector (a plane of a z-slab, the band of a
+// CSR row block) before an operator pass reads them
 template <class T>
 inline void halo(gadi_handle* h, const T* interior) {
   if (!h->sharded()) return;
-  const int64_t plane = h->n * h->n * (int64_t)sizeof(T);
-  h->comm->halo(reinterpret_cast<char*>(const_cast<T*>(interior)), plane, h->i1 - h->i0, h->stream);
+  h->comm->halo(reinterpret_cast<char*>(const_cast<T*>(interior)), h->gh * (int64_t)sizeof(T),
+                h->N * (int64_t)sizeof(T), h->stream);
 }
 
 // ------------------------------------------------------------ outer kernels on A
@@ -413,7 +416,8 @@ struct OuterA {
     halo(h, x);
     const int64_t eo = h->e_off();  // stencil kernels index by global row
     const bool al = aligned_for(h->N, h->n, h->stencil(), 2);
-    const Geo g = make_geo(h->N, al ? 2 : 1);
+    Geo g = make_geo(h->N, al ? 2 : 1);
+    g.gh = h->gh;
     const Window win = h->stencil() ? Window{} : window_for(g, 2, sizeof(double), h->max_band, al);
     auto go = [&](auto op) {
       auto L = [&](auto pt, auto vt) {
@@ -514,6 +518,7 @@ struct Engine final : EngineBase {
   static constexpr bool SPARSE = !std::is_same<Op, Stencil7<C>>::value;
   // CG / GMRES work vectors
   T *pA = nullptr, *pB = nullptr, *q = nullptr, *wA = nullptr, *wB = nullptr, *gr = nullptr, *V = nullptr;
+  int64_t ldv = 0;  // basis stride
   using OV = typename Op::value_type;
   OV* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
   OV* dS = nullptr;
@@ -545,6 +550,7 @@ struct Engine final : EngineBase {
     const int64_t N = h->N;
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
+    geo.gh = h->gh;
     if constexpr (SPARSE) win = window_for(geo, VA, sizeof(T), h->max_band, aligned);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       constexpr int rsz = sizeof(typename RingOf<T, C>::type);
@@ -552,7 +558,8 @@ struct Engine final : EngineBase {
              make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz, h->i0, h->i1) &&
              make_st25(h->n, sizeof(T), 1, g25i, 512, true, 0, h->i0, h->i1);
     }
-    if (h->sharded() && !st25) throw Err(GADI_E_UNSUPPORTED, "sharded solve: the slab shape needs the st25 kernels");
+    if (h->sharded() && !SPARSE && !st25)
+      throw Err(GADI_E_UNSUPPORTED, "sharded solve: the slab shape needs the st25 kernels");
     m_restart = std::max(1, spec.restart);
     rhat = vec();
     z = vec();
@@ -564,13 +571,18 @@ struct Engine final : EngineBase {
     wA = vec();
     wB = vec();
     gr = vec();
-    V = dalloc<T>((int64_t)(m_restart + 1) * N);
-    owned.push_back(V);
+    // basis: m+1 vectors of ldv = N + 2 gh entries (a sharded sparse matvec
+    // reads its operand v_j, a basis vector, at the ghost entries)
+    ldv = N + 2 * h->gh;
+    T* vb = dalloc<T>((int64_t)(m_restart + 1) * ldv);
+    if (h->gh) CK(cudaMemset(vb, 0, (int64_t)(m_restart + 1) * ldv * sizeof(T)));
+    owned.push_back(vb);
+    V = vb + h->gh;
     build_ops();
   }
 
   ~Engine() override {
-    for (T* v : owned) cudaFree(v);
+    for (T* v : owned) cudaFree(v);  // allocation bases
     if (dH) cudaFree(dH);
     if (dS) cudaFree(dS);
     sHS.release();
@@ -719,7 +731,7 @@ struct Engine final : EngineBase {
       T* p_in = (it & 1) ? pA : pB;
       T* p_out = (it & 1) ? pB : pA;
       const int first = it == 0;
-      if (h->sharded()) {  // the stencil pass reads r and p_old on the neighbours' boundary planes
+      if (h->sharded() && !SPARSE) {  // the stencil pass reads r and p_old on the neighbours' boundary planes
         halo(h, r);
         if (!first) halo(h, p_in);
       }
@@ -727,6 +739,7 @@ struct Engine final : EngineBase {
         constexpr int V_ = decltype(vt)::v;
         if constexpr (SPARSE) {  // p-update as its own pass: a gathered operand is not re-formed per nonzero
           k_cg_pupd<T, C, V_><<<geo.nblk, nt, 0, s>>>(r, p_in, p_out, first, geo, h->st);
+          halo(h, p_out);  // a row block's SpMV reads p at the band beyond its rows
           auto kern = k_cg_spmvp<Op, T, C, V_, false>;
           smem_attr(kern, win.bytes);
           kern<<<geo.nblk, nt, win.bytes, s>>>(o, r, p_out, p_out, q, first, geo, rd, h->st, win.band);
@@ -810,12 +823,13 @@ struct Engine final : EngineBase {
       double inv = 1.0 / beta;  // v_0 = r / beta (scale with a binary64 factor)
       const T* wprev = gr;
       for (; j < m && total < spec.max_inner_iters; ++j, ++total) {
-        T* vj = V + (int64_t)j * N;
+        T* vj = V + (int64_t)j * ldv;
         T* w = (j & 1) ? wB : wA;
         V2([&](auto vt) {
           constexpr int V_ = decltype(vt)::v;
           if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
             k_scale<T, V_><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
+            halo(h, vj);  // a row block's matvec reads v_j at the band beyond its rows
             auto kern = k_gm_matvec<Op, T, C, V_, false>;
             smem_attr(kern, win.bytes);
             kern<<<geo.nblk, nt, win.bytes, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st, win.band);
@@ -827,9 +841,9 @@ struct Engine final : EngineBase {
           }
           coll<C>(h, EpiHcol{0});
           for (int i = 0; i <= j; ++i) {
-            T* vi = V + (int64_t)i * N;
+            T* vi = V + (int64_t)i * ldv;
             if (i < j) {
-              k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + N, i, geo, rd, h->st);
+              k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + ldv, i, geo, rd, h->st);
               coll<C>(h, EpiHcol{i + 1});
             } else {
               CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
@@ -895,7 +909,7 @@ struct Engine final : EngineBase {
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, x_zero ? 1 : 0, V, N, j, geo, h->st);
+        k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, x_zero ? 1 : 0, V, ldv, j, geo, h->st);
       });
       CKL();
       ++h->launches;

@@ -35,6 +35,7 @@ struct Geo {
   int W;     // warps per block
   int R;     // segments per lane
   int nblk;  // blocks; nblk * W * R * L == 2^D
+  int64_t gh = 0;  // ghost entries on each side of the operand (a sharded CSR row block)
   __host__ __device__ int threads() const { return L * W; }
 };
 
@@ -377,10 +378,10 @@ __device__ __forceinline__ SmemSrc<T> stage_window(const T* __restrict__ x, cons
   extern __shared__ __align__(16) unsigned char gadi_wsm[];
   T* w = reinterpret_cast<T*>(gadi_wsm);
   const int64_t BR = block_rows<VEC>(g), r0 = (int64_t)blockIdx.x * BR;
-  int64_t lo = r0 - band;
-  lo = lo < 0 ? 0 : (lo & ~(int64_t)(VEC - 1));
+  int64_t lo = r0 - band;  // ghosts (g.gh, a multiple of 8) are part of the operand
+  lo = lo < -g.gh ? -g.gh : (lo & ~(int64_t)(VEC - 1));
   int64_t hi = r0 + BR + band;
-  hi = hi > g.N ? g.N : hi;
+  hi = hi > g.N + g.gh ? g.N + g.gh : hi;
   const int64_t len = hi - lo;
   for (int64_t i = (int64_t)threadIdx.x * VEC; i < len; i += (int64_t)blockDim.x * VEC) {
     if (VEC * sizeof(T) == 16 && i + VEC <= len) {

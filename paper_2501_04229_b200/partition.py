@@ -102,3 +102,78 @@ def exchange_halos(slab: Slab, lo_plane, hi_plane, group=None):
     for r in reqs:
         r.wait()
     return below, above
+
+
+# ------------------------------------------------------------ CSR row blocks
+@dataclass(frozen=True)
+class RowBlock:
+    """Rank r's contiguous rows [row_lo, row_hi) of an N-row banded CSR
+     and the window [win_lo, win_hi) = the block +- the band
+    whose rows (restricted to window columns) determine the block's rows of
+    H = aI + (A+A^T)/2 and S = aI + (A-A^T)/2 (splitting.cpp:12-20): a row's
+    transpose entries come from rows within the band."""
+    rank: int
+    world: int
+    N: int
+    band: int
+    row_lo: int
+    row_hi: int
+    win_lo: int
+    win_hi: int
+
+    @property
+    def rows(self) -> int:
+        return self.row_hi - self.row_lo
+
+
+def row_block_plan(N: int, world: int, rank: int, band: int) -> RowBlock:
+    """N / world rows per rank (world a power of two dividing N: every
+    rank's block is an aligned node of the pairwise-sum tree); the band may
+    not exceed a block (the halo comes from the two neighbours only)."""
+    if world < 1 or not 0 <= rank < world or not is_pow2(world):
+        raise ValueError("bad rank/world (world: a power of two)")
+    if N % world:
+        raise ValueError(f"row-block partition needs world ({world}) to divide N ({N})")
+    m = N // world
+    if band > m:
+        raise ValueError(f"band {band} exceeds a row block of {m} rows: use fewer ranks")
+    lo, hi = rank * m, (rank + 1) * m
+    return RowBlock(rank, world, N, band, lo, hi, max(0, lo - band), min(N, hi + band))
+
+
+def window_csr(rp, ci, v, lo: int, hi: int):
+    """Rows [lo, hi) of a CSR restricted to the columns [lo, hi), columns
+    shifted by -lo (what a rank splits; gadi_api.cu create_impl)."""
+    import numpy as np
+
+    out_rp, out_ci, out_v = [0], [], []
+    for i in range(lo, hi):
+        for k in range(rp[i], rp[i + 1]):
+            if lo <= ci[k] < hi:
+                out_ci.append(ci[k] - lo)
+                out_v.append(v[k])
+        out_rp.append(len(out_ci))
+    return np.array(out_rp, np.int64), np.array(out_ci, np.int64), np.array(out_v, np.float64)
+
+
+def exchange_band(blk: RowBlock, x_local, group=None):
+    """The band of operand entries each SpMV needs beyond the block: my first
+    / last `band` entries to rank-1 / rank+1, theirs back. Returns the
+    operand over [row_lo - band, row_hi + band) clipped to [0, N)."""
+    import torch
+    import torch.distributed as dist
+
+    b = blk.band
+    reqs = []
+    below = above = None
+    if blk.rank > 0 and b:
+        below = torch.empty(b, dtype=x_local.dtype)
+        reqs.append(dist.irecv(below, blk.rank - 1, group=group))
+        reqs.append(dist.isend(x_local[:b].contiguous(), blk.rank - 1, group=group))
+    if blk.rank + 1 < blk.world and b:
+        above = torch.empty(b, dtype=x_local.dtype)
+        reqs.append(dist.irecv(above, blk.rank + 1, group=group))
+        reqs.append(dist.isend(x_local[-b:].contiguous(), blk.rank + 1, group=group))
+    for r in reqs:
+        r.wait()
+    return torch.cat([t for t in (below, x_local, above) if t is not None])

@@ -134,3 +134,88 @@ def test_gloo_slab_protocol(orc, world):
     for r in range(world):
         assert out[r]["matvec_ok"]
         assert out[r]["max"] == float(world)
+
+
+# ------------------------------------------------------------ CSR row blocks
+def test_row_block_plan():
+    from paper_2501_04229_b200.partition import row_block_plan
+
+    b = row_block_plan(1 << 12, 4, 1, 300)
+    assert (b.row_lo, b.row_hi, b.win_lo, b.win_hi) == (1024, 2048, 724, 2348)
+    assert row_block_plan(1 << 12, 4, 0, 300).win_lo == 0
+    assert row_block_plan(1 << 12, 4, 3, 300).win_hi == 1 << 12
+    with pytest.raises(ValueError):
+        row_block_plan(1000, 3, 0, 10)   # world not a power of two
+    with pytest.raises(ValueError):
+        row_block_plan(1002, 4, 0, 10)   # world does not divide N
+    with pytest.raises(ValueError):
+        row_block_plan(1024, 4, 0, 300)  # band wider than a block
+
+
+def _rb_worker(rank, world, port, N, band, q):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import CSR, Oracle
+    from paper_2501_04229_b200.partition import allreduce_pairwise, exchange_band, row_block_plan, window_csr
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = Oracle()
+        A = orc.band(N, 8, band, 7)
+        x, _ = orc.make_rhs(A, 5, -1.0, 1.0)
+        blk = row_block_plan(N, world, rank, band)
+        lo, hi = blk.row_lo, blk.row_hi
+        res = {}
+        # 1. the split of the window, cropped to the block == the global split's block rows
+        wrp, wci, wv = window_csr(A.rp, A.ci, A.v, blk.win_lo, blk.win_hi)
+        Hw, Sw = orc.regularize(CSR(blk.win_hi - blk.win_lo, wrp, wci, wv), 0.7)
+        Hg, Sg = orc.regularize(A, 0.7)
+        a, b = lo - blk.win_lo, hi - blk.win_lo
+        ok = True
+        for Mw, Mg in ((Hw, Hg), (Sw, Sg)):
+            sl_w = slice(Mw.rp[a], Mw.rp[b])
+            sl_g = slice(Mg.rp[lo], Mg.rp[hi])
+            ok &= np.array_equal(Mw.ci[sl_w] + blk.win_lo, Mg.ci[sl_g])
+            ok &= np.array_equal(Mw.v[sl_w].view(np.int64), Mg.v[sl_g].view(np.int64))
+            ok &= np.array_equal(Mw.rp[a:b + 1] - Mw.rp[a], Mg.rp[lo:hi + 1] - Mg.rp[lo])
+        res["split_ok"] = bool(ok)
+        # 2. band exchange + the block's rows of A x == the global matvec's rows
+        xo = exchange_band(blk, torch.from_numpy(x[lo:hi].copy())).numpy()
+        off = max(0, lo - band)
+        y = np.empty(hi - lo)
+        for i in range(lo, hi):
+            acc = 0.0
+            for k in range(A.rp[i], A.rp[i + 1]):
+                acc = acc + A.v[k] * xo[A.ci[k] - off]
+            y[i - lo] = acc
+        res["matvec_ok"] = bool(np.array_equal(y.view(np.int64), orc.matvec(A, x, 2)[lo:hi].view(np.int64)))
+        # 3. block partials folded in rank order == the global pairwise dot
+        res["dot"] = allreduce_pairwise(orc.dot(x[lo:hi], x[lo:hi], 1), lambda u, v: orc.round(u + v, 1))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_row_block_protocol(orc):
+    import torch.multiprocessing as mp
+
+    world, N, band = 2, 512, 60
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_rb_worker, args=(r, world, port, N, band, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A = orc.band(N, 8, band, 7)
+    x, _ = orc.make_rhs(A, 5, -1.0, 1.0)
+    want = orc.dot(x, x, 1)
+    for r in range(world):
+        assert out[r]["split_ok"] and out[r]["matvec_ok"]
+        assert np.array([out[r]["dot"]]).view(np.int64)[0] == np.array([want]).view(np.int64)[0]
