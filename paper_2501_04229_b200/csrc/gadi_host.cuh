@@ -132,7 +132,8 @@ inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
 // grid of n^3 points stored as `tsize`-byte values with `nin` staged inputs.
 // ok = false when the shape does not fit (then the generic kernels run).
 inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_chunks = 512,
-                      bool ident = false, int ring_tsize = 0, int64_t i0 = 0, int64_t i1 = -1) {
+                      bool ident = false, int ring_tsize = 0, int64_t i0 = 0, int64_t i1 = -1,
+                      int ring_planes = 4) {
   if (i1 < 0) i1 = n;
   const int64_t nloc = i1 - i0;
   if (nloc < 1 || !is_pow2(nloc)) return false;
@@ -170,7 +171,7 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
   g.stages = 4;
   const int64_t pe = (TJ + 2) * n;
   auto bytes = [&]() {
-    return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)4 * pe * ring_tsize);
+    return 128 + (size_t)g.stages * nin * pe * tsize + (ident ? 0 : (size_t)ring_planes * pe * ring_tsize);
   };
   // stages in [2 (3 for identity operands), 4]: the most CTAs per SM (228 KB
   // of shared memory, ~5 KB static + 1 KB reserved per CTA), then the most stages
@@ -205,6 +206,66 @@ inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Re
     case 1: return launch_st25_cpt<P, 1>(pol, g, s, rd, st);
     case 2: return launch_st25_cpt<P, 2>(pol, g, s, rd, st);
     default: return launch_st25_cpt<P, 4>(pol, g, s, rd, st);
+  }
+}
+
+// k_st25h geometry: the k_st25 tiling with a padded 3-plane operand ring;
+// stages chosen for the most CTAs per SM, then the most stages
+inline bool make_st25h(int64_t n, int nin, St25Geo& g, int64_t i0, int64_t i1) {
+  if (!make_st25(n, 2, nin, g, 512, false, 2, i0, i1, 3)) return false;
+  if (g.TR < 32) return false;  // a warp's 32 chunks lie in one grid row
+  const size_t pe = (size_t)(g.TJ + 2) * n, pr = (size_t)st25h_plane(g.TJ, (int)n);
+  auto bytes = [&](int st) { return 128 + (size_t)st * nin * pe * 2 + 3 * pr * 2; };
+  auto ctas = [&](int st) { return (int)((228 * 1024) / (bytes(st) + 4 * 1024)); };
+  int best = 2;
+  for (int st = 3; st <= 4; ++st)
+    if (ctas(st) >= ctas(best)) best = st;
+  if (const char* e = std::getenv("GADI_ST25_STAGES")) best = std::max(2, std::atoi(e));  // tuning knob
+  g.stages = best;
+  g.smem = bytes(best);
+  return g.smem <= 200 * 1024;
+}
+
+template <class P, int CPT, int MINB>
+inline void launch_st25h_cpt(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_st25h<P, CPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  // persistent CTAs: as many as are resident at once (cached per shape)
+  static size_t c_smem = 0;
+  static int c_threads = 0, c_res = 0;
+  if (c_smem != g.smem || c_threads != g.threads) {
+    int dev = 0, sms = 0, per = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_st25h<P, CPT, MINB>, g.threads, g.smem));
+    c_smem = g.smem;
+    c_threads = g.threads;
+    c_res = std::max(1, per) * sms;
+    if (const char* e = std::getenv("GADI_ST25H_GRID")) c_res = std::max(1, std::atoi(e));  // tuning knob
+  }
+  const int grid = std::min(g.nblk, c_res);
+  k_st25h<P, CPT, MINB><<<grid, g.threads, g.smem, s>>>(pol, g, rd, st);
+}
+template <class P>
+inline void launch_st25h(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  static const int minb = [] {  // tuning knob: register budget (CTAs per SM)
+    const char* e = std::getenv("GADI_ST25H_MINB");
+    return e ? std::atoi(e) : 2;
+  }();
+  if (minb == 2) {
+    switch (g.CPT) {
+      case 1: return launch_st25h_cpt<P, 1, 2>(pol, g, s, rd, st);
+      case 2: return launch_st25h_cpt<P, 2, 2>(pol, g, s, rd, st);
+      default: return launch_st25h_cpt<P, 4, 2>(pol, g, s, rd, st);
+    }
+  }
+  switch (g.CPT) {
+    case 1: return launch_st25h_cpt<P, 1, 3>(pol, g, s, rd, st);
+    case 2: return launch_st25h_cpt<P, 2, 3>(pol, g, s, rd, st);
+    default: return launch_st25h_cpt<P, 4, 3>(pol, g, s, rd, st);
   }
 }
 
@@ -530,6 +591,8 @@ struct Engine final : EngineBase {
   St25Geo g25;        // CG p-update + SpMV: two staged inputs + operand ring
   St25Geo g25m;       // Arnoldi matvec: one staged input + operand ring
   St25Geo g25i;       // GMRES residual: identity operand, folded from the stages
+  bool st25h = false;  // binary16 operator passes with register-resident operands (k_st25h)
+  St25Geo g25h, g25mh;  // their geometries (3-plane operand ring)
   Window win;         // sparse operators: operand window in shared memory
 
   T* vec() {  // a slab vector (ghost planes when sharded)
@@ -557,6 +620,11 @@ struct Engine final : EngineBase {
       st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz, h->i0, h->i1) &&
              make_st25(h->n, sizeof(T), 1, g25m, 512, false, rsz, h->i0, h->i1) &&
              make_st25(h->n, sizeof(T), 1, g25i, 512, true, 0, h->i0, h->i1);
+      if constexpr (PolSpmvp<T, C>::FASTH) {
+        const char* e = std::getenv("GADI_ST25H");
+        st25h = st25 && !(e && e[0] == '0') &&
+                make_st25h(h->n, 2, g25h, h->i0, h->i1) && make_st25h(h->n, 1, g25mh, h->i0, h->i1);
+      }
     }
     if (h->sharded() && !SPARSE && !st25)
       throw Err(GADI_E_UNSUPPORTED, "sharded solve: the slab shape needs the st25 kernels");
@@ -579,6 +647,10 @@ struct Engine final : EngineBase {
     owned.push_back(vb);
     V = vb + h->gh;
     build_ops();
+    if constexpr (std::is_same<Op, Stencil7<C>>::value && PolSpmvp<T, C>::FASTH) {
+      for (int k = 0; k < 7; ++k)  // k_st25h folds neutral operands at the boundary: finite coefficients only
+        if (!std::isfinite((double)opH.c[k]) || !std::isfinite((double)opS.c[k])) st25h = false;
+    }
   }
 
   ~Engine() override {
@@ -666,6 +738,11 @@ struct Engine final : EngineBase {
       const int64_t eo = h->e_off();  // the st25 kernels index by global row
       PolSpmvp<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]},
                          r - eo, p_in - eo, p_out - eo, q - eo, Ar_beta(), first};
+      if constexpr (PolSpmvp<T, C>::FASTH)
+        if (st25h) {
+          launch_st25h(pol, g25h, h->stream, red_of(h), h->st);
+          return true;
+        }
       launch_st25(pol, g25, h->stream, red_of(h), h->st);
       return true;
     } else {
@@ -678,6 +755,11 @@ struct Engine final : EngineBase {
       const int64_t eo = h->e_off();
       PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev - eo, inv, vj - eo,
                             V - eo, w - eo};
+      if constexpr (PolGmMatvec<T, C>::FASTH)
+        if (st25h) {
+          launch_st25h(pol, g25mh, h->stream, red_of(h), h->st);
+          return true;
+        }
       launch_st25(pol, g25m, h->stream, red_of(h), h->st);
       return true;
     } else {

@@ -242,6 +242,93 @@ constexpr int ST25_CPT_MAX = 4;
 constexpr int ST25_IL_MAX = 32;  // planes per CTA (make_st25)
 constexpr int ST25_MAXW = 16;    // warps per CTA
 
+// After a tile's plane loop: each plane's warp partials -> one pairwise
+// subtree per (plane, tile) -> partials[plane * njt + tile].
+template <class P, class PL>
+__device__ __forceinline__ void st25_partials(const St25Geo& g, const Red& rd, const PL* plb, int nw, int ib,
+                                              int jt) {
+  using R0 = typename P::R0;
+  if (P::HAS_R0 || P::HAS_R1) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < g.IL; t += blockDim.x) {
+      R0 v0[ST25_MAXW];
+      double v1[ST25_MAXW];
+#pragma unroll
+      for (int k = 0; k < ST25_MAXW; ++k)
+        if (k < nw) {
+          if (P::HAS_R0) v0[k] = from_dbl<R0>(plb[t * nw + k]);
+          if (P::HAS_R1) v1[k] = plb[t * nw + k];
+        }
+#pragma unroll
+      for (int s2 = 1; s2 < ST25_MAXW; s2 <<= 1)
+#pragma unroll
+        for (int k = 0; k + s2 < ST25_MAXW; k += 2 * s2)
+          if (k + s2 < nw) {
+            if (P::HAS_R0) v0[k] = Ar<R0>::add(v0[k], v0[k + s2]);
+            if (P::HAS_R1) v1[k] = __dadd_rn(v1[k], v1[k + s2]);
+          }
+      const int64_t slot = (int64_t)(ib - g.i0 + t) * g.njt + jt;
+      if (P::HAS_R0) rd.part0[slot] = to_dbl(v0[0]);
+      if (P::HAS_R1) rd.part1[slot] = v1[0];
+    }
+  }
+}
+
+// After all of a CTA's tiles: max / flags, then the grid ticket over the
+// `nctas` CTAs; the last CTA folds the partials.
+template <class P>
+__device__ __forceinline__ void st25_ticket(const P& pol, const St25Geo& g, const Red& rd, DevState* st,
+                                            double mloc, int flag, unsigned nctas) {
+  using R0 = typename P::R0;
+  __shared__ __align__(8) unsigned char redb0[32 * sizeof(double)];
+  __shared__ double redb1[32];
+  __shared__ int s_last;
+  R0* red0 = reinterpret_cast<R0*>(redb0);
+  const int tid = threadIdx.x;
+  if (P::HAS_R0 || P::HAS_R1) __threadfence();
+  if (P::HAS_MAX) block_max_abs(&st->maxbits, mloc);
+  if (P::HAS_FLAG) or_flags(pol.flag_dst(st), flag);
+  if (tid == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(rd.ticket, 1u);
+    s_last = (t == nctas - 1u);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int64_t P_ = (int64_t)(g.i1 - g.i0) * g.njt;  // partials (power of two)
+  const int B = blockDim.x;
+  R0 t0 = Ar<R0>::zero();
+  double t1 = 0.0;
+  int cnt;
+  if (P_ <= B) {
+    if (P::HAS_R0) t0 = tid < P_ ? from_dbl<R0>(__ldcg(rd.part0 + tid)) : Ar<R0>::zero();
+    if (P::HAS_R1) t1 = tid < P_ ? __ldcg(rd.part1 + tid) : 0.0;
+    cnt = (int)P_;
+  } else {
+    const int64_t Lr = P_ / B;
+    const double* p0 = rd.part0 + (int64_t)tid * Lr;
+    const double* p1 = rd.part1 + (int64_t)tid * Lr;
+    if (P::HAS_R0) t0 = run_pairwise<R0>(Lr, [&](int64_t j) { return from_dbl<R0>(__ldcg(p0 + j)); });
+    if (P::HAS_R1) t1 = run_pairwise<double>(Lr, [&](int64_t j) { return __ldcg(p1 + j); });
+    cnt = B;
+  }
+  if (P::HAS_R0) t0 = block_tree(t0, cnt, red0);
+  if (P::HAS_R1) t1 = block_tree(t1, cnt, redb1);
+  if (tid == 0) {
+    *rd.ticket = 0u;
+    __threadfence();
+    finish_red(pol, st, t0, t1);
+  }
+}
+
+template <class P, class PL>
+__device__ __forceinline__ void st25_finish(const P& pol, const St25Geo& g, const Red& rd, DevState* st,
+                                            const PL* plb, int nw, int ib, int jt, double mloc, int flag) {
+  st25_partials<P>(g, rd, plb, nw, ib, jt);
+  st25_ticket(pol, g, rd, st, mloc, flag, (unsigned)g.nblk);
+}
+
 // ------------------------------------------------------------ the kernel
 template <class P, int CPT>
 __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd, DevState* st) {
@@ -265,10 +352,6 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
   const int pe = (g.TJ + 2) * n;  // elements of one staged plane (rows j0-1 .. j0+TJ)
   T* raw = reinterpret_cast<T*>(smem + 128);
   RT* opr = reinterpret_cast<RT*>(raw + (size_t)S * P::NIN * pe);
-  __shared__ __align__(8) unsigned char redb0[32 * sizeof(double)];
-  __shared__ double redb1[32];
-  __shared__ int s_last;
-  R0* red0 = reinterpret_cast<R0*>(redb0);
   // per-(plane, warp) partial sums, folded over the warps once after the
   // plane loop (no block barrier per plane for the reductions)
   static_assert(!(P::HAS_R0 && P::HAS_R1), "one reduced quantity per policy");
@@ -510,69 +593,248 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
       }
     }
   }
-  // each plane's warp partials -> one pairwise subtree (the same shape as a
-  // warp butterfly over nw contiguous warps) -> partials[plane * njt + tile]
-  if (P::HAS_R0 || P::HAS_R1) {
-    __syncthreads();
-    for (int t = tid; t < g.IL; t += blockDim.x) {
-      R0 v0[ST25_MAXW];
-      double v1[ST25_MAXW];
-#pragma unroll
-      for (int k = 0; k < ST25_MAXW; ++k)
-        if (k < nw) {
-          if (P::HAS_R0) v0[k] = from_dbl<R0>(plb[t * nw + k]);
-          if (P::HAS_R1) v1[k] = plb[t * nw + k];
-        }
-#pragma unroll
-      for (int s2 = 1; s2 < ST25_MAXW; s2 <<= 1)
-#pragma unroll
-        for (int k = 0; k + s2 < ST25_MAXW; k += 2 * s2)
-          if (k + s2 < nw) {
-            if (P::HAS_R0) v0[k] = Ar<R0>::add(v0[k], v0[k + s2]);
-            if (P::HAS_R1) v1[k] = __dadd_rn(v1[k], v1[k + s2]);
-          }
-      const int64_t slot = (int64_t)(ib - g.i0 + t) * g.njt + jt;
-      if (P::HAS_R0) rd.part0[slot] = to_dbl(v0[0]);
-      if (P::HAS_R1) rd.part1[slot] = v1[0];
-    }
-    __threadfence();
-  }
+  st25_finish(pol, g, rd, st, plb, nw, ib, jt, mloc, flag);
+}
 
-  // max / flags, then the grid ticket; the last CTA folds the partials
-  if (P::HAS_MAX) block_max_abs(&st->maxbits, mloc);
-  if (P::HAS_FLAG) or_flags(pol.flag_dst(st), flag);
+// ------------------------------------------------ binary16 operator passes
+// k_st25h: the FASTH operator passes (binary16 storage, binary32 arithmetic:
+// CG p-update + SpMV, Arnoldi matvec) with the operand of each thread's own
+// chunks kept in registers for planes i-1, i, i+1 (rotated by unrolling the
+// plane loop by three). Only plane i's operand lives in shared memory (a
+// 3-slot ring; the j +- 1 rows and the k edges of the fold read it), so a
+// chunk's fold costs two 16-byte and two 2-byte shared loads. Ring rows are
+// padded by 8 entries that hold the neutral k-edge operands, and off-grid
+// halo rows hold the neutral j-edge operands: an absent neighbour folds a
+// product of -0, which leaves every accumulator unchanged (the reference
+// skips it), so the fold has no per-lane branches. The i-edges are
+// warp-uniform branches. The j-halo rows of each plane are built by all
+// warps evenly. Same arithmetic, same stored-column order, same reduction
+// tree as k_st25. Requires finite binary16 coefficients (the host checks).
+__device__ __forceinline__ uint4 splat4(uint32_t h16) {
+  const uint32_t w = (h16 & 0xffffu) | (h16 << 16);
+  return make_uint4(w, w, w, w);
+}
+// ring plane size in entries: TJ+2 rows of n entries, each after an 8-entry
+// lead pad, plus one trailing pad
+__host__ __device__ inline int st25h_plane(int TJ, int n) { return (TJ + 2) * (n + 8) + 8; }
+
+// pairwise sums over the 32 lanes of CPT per-lane values at once (each a
+// perfect butterfly subtree, the shape of warp_tree), then over the CPT
+// contiguous 32-chunk blocks; the result is valid in lane 0
+template <int CPT>
+__device__ __forceinline__ float warp_tree_multi(float (&v)[CPT], int lane) {
+  if constexpr (CPT == 2) {
+    const bool odd = lane & 1;
+    float s = odd ? v[1] : v[0];
+    const float o = __shfl_xor_sync(0xffffffffu, odd ? v[0] : v[1], 1);
+    s = __fadd_rn(s, o);  // even lanes: v[0] pairs, odd lanes: v[1] pairs
+#pragma unroll
+    for (int m = 2; m < 32; m <<= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, m));
+    const float b = __shfl_sync(0xffffffffu, s, 1);
+    return __fadd_rn(s, b);
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < CPT; ++rr) v[rr] = warp_tree(v[rr], 32);
+#pragma unroll
+    for (int s2 = 1; s2 < CPT; s2 <<= 1)
+#pragma unroll
+      for (int rr = 0; rr + s2 < CPT; rr += 2 * s2) v[rr] = __fadd_rn(v[rr], v[rr + s2]);
+    return v[0];
+  }
+}
+
+template <class P, int CPT, int MINB>
+__global__ void __launch_bounds__(MINB == 2 ? 512 : 256, MINB == 2 ? 1 : MINB)
+    k_st25h(const P pol_in, St25Geo g, Red rd, DevState* st) {
+  using T = typename P::T;
+  static_assert(P::FASTH && std::is_same<T, __half>::value, "binary16 storage only");
+  constexpr int VEC = 8;
+  if (pol_in.skip(st)) return;
+  P pol = pol_in;
+  pol.prepare(st);
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  const int S = g.stages;
+  const int nin = pol.nin();
+  const int n = g.n, rs = n + 8;
+  const int pe = (g.TJ + 2) * n;
+  const int pr = st25h_plane(g.TJ, n);
+  T* raw = reinterpret_cast<T*>(smem + 128);
+  T* ring = raw + (size_t)S * P::NIN * pe;  // 3 operand planes of pr entries
+  __shared__ float plb[ST25_IL_MAX * ST25_MAXW];  // binary32 partials (R0 = float)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+  // Persistent CTAs: tiles blockIdx.x, +gridDim.x, ... The TMA stream runs
+  // across tile boundaries (thread 0 issues the planes of all of this CTA's
+  // tiles in consumption order), so the pipeline never drains.
+  int iss_t = blockIdx.x, iss_q = 0, iss_qhi = -1, iss_s = 0;
+  uint32_t iss_bytes = 0;
+  int64_t iss_src = 0;
+  T* iss_dst = raw;
+  auto iss_tile = [&]() {  // geometry of tile iss_t (thread 0)
+    const int jt = iss_t % g.njt, ic = iss_t / g.njt;
+    const int j0 = jt << g.lgTJ, ib = g.i0 + ic * g.IL;
+    const int rlo = max(j0 - 1, 0), rhi = min(j0 + g.TJ, n - 1);
+    iss_q = max(ib - 1, 0);
+    iss_qhi = min(ib + g.IL, n - 1);
+    iss_bytes = (uint32_t)((rhi - rlo + 1) * n * sizeof(T));
+    iss_src = (int64_t)rlo * n;
+    iss_dst = raw + (rlo - (j0 - 1)) * n;
+  };
+  auto issue_next = [&]() {
+    if (iss_t >= g.nblk) return;
+    mbar_expect_tx(&bar[iss_s], (uint32_t)nin * iss_bytes);
+    for (int k = 0; k < nin; ++k)
+      bulk_g2s(iss_dst + ((size_t)iss_s * P::NIN + k) * pe, pol.in(k) + (int64_t)iss_q * g.nn + iss_src, iss_bytes,
+               &bar[iss_s]);
+    iss_s = iss_s + 1 == S ? 0 : iss_s + 1;
+    if (++iss_q > iss_qhi) {
+      iss_t += gridDim.x;
+      if (iss_t < g.nblk) iss_tile();
+    }
+  };
+  const uint32_t* ch = pol.ch;
   if (tid == 0) {
-    __threadfence();
-    const unsigned t = atomicAdd(rd.ticket, 1u);
-    s_last = (t == (unsigned)g.nblk - 1u);
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  {  // the k-edge pads of every ring row hold the neutral operands
+    const unsigned short ne2 = (unsigned short)nh_of(ch[2]), ne4 = (unsigned short)nh_of(ch[4]);
+    unsigned short* ru = reinterpret_cast<unsigned short*>(ring);
+    for (int t = tid; t < 3 * (g.TJ + 3); t += blockDim.x) {
+      const int sl = t / (g.TJ + 3), r = t % (g.TJ + 3);
+      ru[sl * pr + r * rs + 0] = ne4;  // after the end of row r-1
+      ru[sl * pr + r * rs + 7] = ne2;  // before the start of row r
+    }
   }
   __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int64_t P_ = (int64_t)(g.i1 - g.i0) * g.njt;  // partials (power of two)
-  const int B = blockDim.x;
-  R0 t0 = Ar<R0>::zero();
-  double t1 = 0.0;
-  int cnt;
-  if (P_ <= B) {
-    if (P::HAS_R0) t0 = tid < P_ ? from_dbl<R0>(__ldcg(rd.part0 + tid)) : Ar<R0>::zero();
-    if (P::HAS_R1) t1 = tid < P_ ? __ldcg(rd.part1 + tid) : 0.0;
-    cnt = (int)P_;
-  } else {
-    const int64_t Lr = P_ / B;
-    const double* p0 = rd.part0 + (int64_t)tid * Lr;
-    const double* p1 = rd.part1 + (int64_t)tid * Lr;
-    if (P::HAS_R0) t0 = run_pairwise<R0>(Lr, [&](int64_t j) { return from_dbl<R0>(__ldcg(p0 + j)); });
-    if (P::HAS_R1) t1 = run_pairwise<double>(Lr, [&](int64_t j) { return __ldcg(p1 + j); });
-    cnt = B;
-  }
-  if (P::HAS_R0) t0 = block_tree(t0, cnt, red0);
-  if (P::HAS_R1) t1 = block_tree(t1, cnt, redb1);
   if (tid == 0) {
-    *rd.ticket = 0u;
-    __threadfence();
-    finish_red(pol, st, t0, t1);
+    iss_tile();
+    for (int s = 0; s < S; ++s) issue_next();
   }
+  int cs = 0;
+  uint32_t cph = 0;  // consumption: stage, parity
+  auto consume = [&]() -> const T* {
+    mbar_wait(&bar[cs], cph);
+    const T* r = raw + (size_t)cs * P::NIN * pe;
+    if (++cs == S) {
+      cs = 0;
+      cph ^= 1u;
+    }
+    return r;
+  };
+  // own chunks: fixed positions within every tile
+  int sidx[CPT], ridx[CPT], ebase[CPT];
+#pragma unroll
+  for (int rr = 0; rr < CPT; ++rr) {
+    const int c = ((warp * CPT + rr) << 5) + lane;
+    const int jl = c >> g.lgTR, k0 = (c & (g.TR - 1)) * VEC;
+    sidx[rr] = (jl + 1) * n + k0;
+    ridx[rr] = (jl + 1) * rs + 8 + k0;
+    ebase[rr] = jl * n + k0;
+  }
+  const int nhalo = 2 * g.TR, hpw = (nhalo + nw - 1) / nw;  // halo chunks spread evenly over the warps
+  const uint4 n1 = splat4(nh_of(ch[1])), n5 = splat4(nh_of(ch[5]));
+
+  for (int tile = blockIdx.x; tile < g.nblk; tile += gridDim.x) {
+    const int jt = tile % g.njt, ic = tile / g.njt;
+    const int j0 = jt << g.lgTJ, ib = g.i0 + ic * g.IL, ie = ib + g.IL;
+    const bool hrow0 = j0 > 0, hrow1 = j0 + g.TJ < n;
+    // off-grid halo rows hold the neutral j-edge operands (the previous
+    // tile's folds are complete: st25_partials ends with a barrier)
+    for (int t = tid; t < 3 * g.TR; t += blockDim.x) {
+      const int sl = t / g.TR, k0 = (t % g.TR) * VEC;
+      if (!hrow0) sts_u4(ring + sl * pr + 8 + k0, n1);
+      if (!hrow1) sts_u4(ring + sl * pr + (g.TJ + 1) * rs + 8 + k0, n5);
+    }
+    int64_t e0[CPT];
+#pragma unroll
+    for (int rr = 0; rr < CPT; ++rr) e0[rr] = (int64_t)ib * g.nn + (int64_t)j0 * n + ebase[rr];
+
+    // the operand of plane q: own chunks -> registers (and the ring slot),
+    // halo chunks -> the ring slot
+    auto build = [&](const T* rsg, T* slot, uint4 (&xo)[CPT], bool to_ring) {
+#pragma unroll
+      for (int rr = 0; rr < CPT; ++rr) {
+        xo[rr] = pol.make_h(rsg, pe, sidx[rr]);
+        if (to_ring) sts_u4(slot + ridx[rr], xo[rr]);
+      }
+      if (to_ring)
+        for (int x = lane; x < hpw; x += 32) {
+          const int hc = warp * hpw + x;
+          if (hc < nhalo) {
+            const bool top = hc < g.TR;
+            if (top ? hrow0 : hrow1) {
+              const int k0 = (hc & (g.TR - 1)) * VEC;
+              const int row = top ? 0 : g.TJ + 1;
+              sts_u4(slot + row * rs + 8 + k0, pol.make_h(rsg, pe, row * n + k0));
+            }
+          }
+        }
+    };
+
+    uint4 xa[CPT], xb[CPT], xq[CPT];
+    if (ib - 1 >= 0) build(consume(), nullptr, xa, false);
+    build(consume(), ring, xb, true);
+    __syncthreads();  // stages of planes ib-1, ib consumed; plane ib in the ring
+    if (tid == 0) {
+      fence_proxy_async();
+      issue_next();
+      if (ib - 1 >= 0) issue_next();
+    }
+
+    // one plane: build plane i+1 into xp (ring slot sp), fold plane i from
+    // xm / xc / xp and ring slot sc
+    auto plane = [&](int i, const uint4 (&xm)[CPT], const uint4 (&xc)[CPT], uint4 (&xp)[CPT], int sc, int sp) {
+      uint4 pf[CPT];  // per-point global operands of the epilogue (Arnoldi: v_0), a build + barrier ahead
+#pragma unroll
+      for (int rr = 0; rr < CPT; ++rr) pf[rr] = pol.pref(e0[rr]);
+      const bool hasp = i + 1 <= n - 1, hasm = i > 0;
+      if (hasp) build(consume(), ring + (size_t)sp * pr, xp, true);
+      // plane i+1 is in the ring and its stage consumed. Slot (i+2)%3, written
+      // next, was last read by the fold of plane i-1, before this barrier.
+      __syncthreads();
+      if (tid == 0 && hasp) {
+        fence_proxy_async();
+        issue_next();
+      }
+      const T* oc = ring + (size_t)sc * pr;
+      const unsigned short* ocu = reinterpret_cast<const unsigned short*>(oc);
+      float a0[CPT];
+#pragma unroll
+      for (int rr = 0; rr < CPT; ++rr) {
+        float acc[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc[v] = 0.0f;  // matvec folds start from +0 (kernels.cpp:46)
+        const int ri = ridx[rr];
+        const uint4 vjm = lds_u4(oc + ri - rs), vjp = lds_u4(oc + ri + rs);
+        const uint32_t em = ocu[ri - 1], ep = ocu[ri + VEC];
+        // stored-column order (problems.cpp:28-34): i-1, j-1, k-1, centre, k+1, j+1, i+1
+        if (hasm) fold8h<0>(acc, ch[0], xm[rr], 0u);
+        fold8h<0>(acc, ch[1], vjm, 0u);
+        fold8h<-1>(acc, ch[2], xc[rr], em);
+        fold8h<0>(acc, ch[3], xc[rr], 0u);
+        fold8h<1>(acc, ch[4], xc[rr], ep);
+        fold8h<0>(acc, ch[5], vjp, 0u);
+        if (hasp) fold8h<0>(acc, ch[6], xp[rr], 0u);
+        a0[rr] = pol.epi_h(e0[rr], acc, xc[rr], pf[rr]);
+        e0[rr] += g.nn;
+      }
+      const float t = warp_tree_multi<CPT>(a0, lane);
+      if (lane == 0) plb[(i - ib) * nw + warp] = t;
+    };
+    int i = ib;
+    for (; i + 3 <= ie; i += 3) {  // ring slots: plane ib in 0, ib+1 in 1, ...
+      plane(i, xa, xb, xq, 0, 1);
+      plane(i + 1, xb, xq, xa, 1, 2);
+      plane(i + 2, xq, xa, xb, 2, 0);
+    }
+    if (i < ie) plane(i, xa, xb, xq, 0, 1);
+    if (i + 1 < ie) plane(i + 1, xb, xq, xa, 1, 2);
+    st25_partials<P>(g, rd, plb, nw, ib, jt);
+    __syncthreads();  // plb and the ring are free for the next tile
+  }
+  st25_ticket(pol, g, rd, st, 0.0, 0, gridDim.x);
 }
 
 // ------------------------------------------------------------ policies
@@ -627,7 +889,8 @@ struct PolSpmvp {
     }
     return make_uint4(o[0], o[1], o[2], o[3]);
   }
-  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& pc) const {
+  __device__ uint4 pref(int64_t) const { return make_uint4(0, 0, 0, 0); }
+  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& pc, const uint4& = uint4()) const {
     const uint4 qv = make_uint4(pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), pack_h2(acc[4], acc[5]),
                                 pack_h2(acc[6], acc[7]));
     *reinterpret_cast<uint4*>(q + e0) = qv;
@@ -710,13 +973,18 @@ struct PolGmMatvec {
     }
     return make_uint4(o[0], o[1], o[2], o[3]);
   }
-  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& vc) const {
+  __device__ uint4 pref(int64_t e0) const {  // v_0 (unless v_j is v_0)
+    return vj == v0 ? make_uint4(0, 0, 0, 0) : __ldg(reinterpret_cast<const uint4*>(v0 + e0));
+  }
+  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& vc, const uint4& v0p) const {
     const uint4 wq = make_uint4(pack_h2(acc[0], acc[1]), pack_h2(acc[2], acc[3]), pack_h2(acc[4], acc[5]),
                                 pack_h2(acc[6], acc[7]));
     *reinterpret_cast<uint4*>(vj + e0) = vc;
     *reinterpret_cast<uint4*>(w + e0) = wq;
-    const uint4 v0u = vj == v0 ? vc : __ldg(reinterpret_cast<const uint4*>(v0 + e0));
-    return dot8h(wq, v0u);
+    return dot8h(wq, vj == v0 ? vc : v0p);
+  }
+  __device__ C epi_h(int64_t e0, const float (&acc)[8], const uint4& vc) const {
+    return epi_h(e0, acc, vc, pref(e0));
   }
   __device__ int nin() const { return 1; }
   __device__ const T* in(int) const { return wprev; }
