@@ -47,8 +47,11 @@ extern "C" {
 typedef enum { GADI_HALF = 0, GADI_SINGLE = 1, GADI_DOUBLE = 2 } gadi_precision;
 
 /* InnerMethod, inner_solver.hpp:15 (same numeric values). LU_DIRECT is the
- * reference's CPU band LU; it has no device implementation here and is
- * rejected with GADI_E_UNSUPPORTED (no CPU fallback). */
+ * reference's band LU with partial pivoting (band_lu.cpp), factored and
+ * applied on the device (gadi_lu.cu) in u_r, bit for bit the reference's; it
+ * ignores `accum` (the reference LU rounds every op to u_r) and needs
+ * (nb+8)(nb+kl) band values of shared memory per CTA (kl <= ~6000 binary32,
+ * ~3000 binary64), else GADI_E_UNSUPPORTED. */
 typedef enum { GADI_INNER_LU_DIRECT = 0, GADI_INNER_CG = 1, GADI_INNER_GMRES = 2 } gadi_inner_method;
 
 /* Inner arithmetic (extension). NATIVE = every scalar op rounded once to u_r,
@@ -80,7 +83,12 @@ typedef enum {
   GADI_E_CUDA = -5,
   GADI_E_NCCL = -6,
   GADI_E_OOM = -7,
-  GADI_E_STATE = -8        /* call order (e.g. solve_H before prepare)        */
+  GADI_E_STATE = -8,       /* call order (e.g. solve_H before prepare)        */
+  /* gadi_cuda_prepare only: the numerical exceptions GadiSystem::prepare
+   * throws for LU_DIRECT (band_lu.cpp:106-108,132-134); gadi_cuda_solve
+   * reports them as statuses, as run_gadi_ir does (solver.cpp:74-82). */
+  GADI_E_SINGULAR = -9,    /* SingularInPrecision */
+  GADI_E_OVERFLOW = -10    /* OverflowDetected    */
 } gadi_error;
 
 /* InnerSolverSpec, inner_solver.hpp:20-25; defaults from gadi_config_default. */
@@ -183,7 +191,8 @@ int gadi_cuda_residual_uf(gadi_handle* h, int32_t u_f, const double* x, double* 
 /* true_residual_norm: binary64 ||b - A x||_2 (solver.cpp:194-197). */
 int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_out);
 /* prepare: H = alpha I + M, S = alpha I + N rounded to u_r (splitting.cpp:37-47,
- * inner_solver.cpp:41-45). LU_DIRECT -> GADI_E_UNSUPPORTED. */
+ * inner_solver.cpp:41-45); LU_DIRECT also factors H then S (solver.cpp:204-207)
+ * and returns GADI_E_SINGULAR / GADI_E_OVERFLOW where the reference throws. */
 int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r,
                       const gadi_inner_spec* spec, int32_t accum);
 int gadi_cuda_set_inner_stop_norm(gadi_handle* h, double stop_norm);

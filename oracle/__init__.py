@@ -137,6 +137,7 @@ class Oracle:
                                  C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.orc_krylov_af.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, C.c_double, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.orc_lu_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, _f64p]
         L.orc_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, _f64p, C.POINTER(Config), _f64p, _f64p,
                                 C.c_int, C.POINTER(Report)]
         L.orc_gpr.argtypes = [_f64p, _f64p, C.c_int, C.POINTER(GprOpts), _f64p, C.c_int, _f64p,
@@ -240,6 +241,15 @@ class Oracle:
                              fmt if af is None else af, stop_norm, _p(x), C.byref(it), C.byref(st))
         return x, it.value, st.value
 
+    def lu_solve(self, M: CSR, rhs, fmt):
+        """BandLU factor + solve of M in fmt (band_lu.cpp); returns (x, status)
+        with status 0, 4 (SingularInPrecision) or 3 (OverflowDetected)."""
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.zeros(M.n)
+        oc = _oc(M)
+        st = self.L.orc_lu_solve(C.byref(oc), _p(rhs), fmt, _p(x))
+        return x, st
+
     def solve(self, A: CSR, b, cfg: Config, x0=None, cap=100000):
         b = np.ascontiguousarray(b, np.float64)
         x = np.zeros(A.n)
@@ -300,6 +310,7 @@ class Reference:
         L.ref_krylov.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, C.c_double, C.c_int,
                                  C.c_int, C.c_int, C.c_double, _f64p, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int)]
+        L.ref_lu_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, _f64p]
         L.ref_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.POINTER(Config), _f64p,
                                 _f64p, C.c_int, C.POINTER(Report)]
         L.ref_reference_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_double, C.c_double,
@@ -382,6 +393,13 @@ class Reference:
         assert self.L.ref_krylov(*self._a(M), _p(rhs), method, eps, max_inner, restart, fmt, stop_norm,
                                  _p(x), C.byref(it), C.byref(st)) == 0
         return x, it.value, st.value
+
+    def lu_solve(self, M, rhs, fmt):
+        rhs = np.ascontiguousarray(rhs, np.float64)
+        x = np.zeros(M.n)
+        st = self.L.ref_lu_solve(*self._a(M), _p(rhs), fmt, _p(x))
+        assert st >= 0, st
+        return x, st
 
     def solve(self, A, b, cfg, x0=None, cap=100000):
         b = np.ascontiguousarray(b, np.float64)

@@ -514,6 +514,126 @@ int orc_krylov(const orc_csr* M, const double* rhs, int method, double eps, int 
   return orc_krylov_af(M, rhs, method, eps, max_inner, restart, fmt, fmt, stop_norm, x, iters, status);
 }
 
+
+/* ------------------------------------------------------------------ band LU
+ * BandLU (band_lu.cpp:60-199): LAPACK-style band storage with kl extra
+ * superdiagonals of fill, partial pivoting, every scalar op of the
+ * elimination and the triangular solves rounded once to fmt. Values are
+ * carried in binary64: a*b of two binary16/32 numbers is exact in binary64,
+ * a-b of binary16 numbers is exact too, and the remaining roundings through
+ * binary64 are innocuous (53 >= 2p+2), so R(a op b) equals the reference's
+ * float-domain policies (band_lu.cpp:12-56) bit for bit. */
+#define AT(f, i, j) (f)->ab[(j) * (f)->ldab + ((f)->kl + (f)->ku + (i) - (j))]
+
+static double lu_tiny(int fmt) { /* format(fmt).min_normal */
+  return fmt == GADI_HALF ? 0x1p-14 : fmt == GADI_SINGLE ? 0x1p-126 : 0x1p-1022;
+}
+
+/* lower/upper_bandwidth, sparse.cpp:142-154 */
+static void bandwidths(const orc_csr* A, int64_t* kl, int64_t* ku) {
+  int64_t l = 0, u = 0;
+  for (int64_t i = 0; i < A->n; ++i)
+    if (A->rp[i] < A->rp[i + 1]) {
+      if (i - A->ci[A->rp[i]] > l) l = i - A->ci[A->rp[i]];
+      if (A->ci[A->rp[i + 1] - 1] - i > u) u = A->ci[A->rp[i + 1] - 1] - i;
+    }
+  *kl = l;
+  *ku = u;
+}
+
+/* BandLU::BandLU + factor, band_lu.cpp:60-135. Returns 0, or the SolveStatus
+ * the reference's exception maps to in run_gadi_ir (solver.cpp:74-82):
+ * GADI_SINGULAR_IN_PRECISION (pivot below min_normal, :106-108) or
+ * GADI_OVERFLOW_DETECTED (non-finite factor entry, :132-134). */
+int orc_blu_factor(const orc_csr* A, int fmt, orc_blu* f) {
+  const int64_t n = A->n;
+  memset(f, 0, sizeof(*f));
+  f->n = n;
+  f->fmt = fmt;
+  bandwidths(A, &f->kl, &f->ku);
+  f->ldab = 2 * f->kl + f->ku + 1;
+  f->ab = (double*)calloc((size_t)(f->ldab * n), 8);
+  f->ipiv = (int64_t*)calloc((size_t)n, 8);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = A->rp[i]; k < A->rp[i + 1]; ++k) AT(f, i, A->ci[k]) = R(A->v[k], fmt);
+  const double tiny = lu_tiny(fmt);
+  const int64_t band_cols = f->kl + f->ku;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t ilast = n - 1 < j + f->kl ? n - 1 : j + f->kl;
+    int64_t p = j;
+    double pmax = fabs(AT(f, j, j));
+    for (int64_t i = j + 1; i <= ilast; ++i) {
+      const double v = fabs(AT(f, i, j));
+      if (v > pmax) {
+        pmax = v;
+        p = i;
+      }
+    }
+    if (pmax < tiny) return GADI_SINGULAR_IN_PRECISION;
+    f->ipiv[j] = p;
+    const int64_t klast = n - 1 < j + band_cols ? n - 1 : j + band_cols;
+    if (p != j)
+      for (int64_t k = j; k <= klast; ++k) {
+        const double t = AT(f, j, k);
+        AT(f, j, k) = AT(f, p, k);
+        AT(f, p, k) = t;
+      }
+    const double piv = AT(f, j, j);
+    for (int64_t i = j + 1; i <= ilast; ++i) AT(f, i, j) = R(AT(f, i, j) / piv, fmt);
+    for (int64_t k = j + 1; k <= klast; ++k) {
+      const double ajk = AT(f, j, k);
+      if (ajk == 0.0) continue;
+      for (int64_t i = j + 1; i <= ilast; ++i) AT(f, i, k) = R(AT(f, i, k) - R(AT(f, i, j) * ajk, fmt), fmt);
+    }
+  }
+  for (int64_t t = 0; t < f->ldab * n; ++t)
+    if (!isfinite(f->ab[t])) return GADI_OVERFLOW_DETECTED;
+  return 0;
+}
+
+/* BandLU::solve_impl, band_lu.cpp:137-172. */
+void orc_blu_solve(const orc_blu* f, const double* rhs, double* x) {
+  const int64_t n = f->n, kl = f->kl, ubw = f->kl + f->ku;
+  const int fmt = f->fmt;
+  for (int64_t i = 0; i < n; ++i) x[i] = R(rhs[i], fmt);
+  for (int64_t j = 0; j < n; ++j) {
+    if (f->ipiv[j] != j) {
+      const double t = x[j];
+      x[j] = x[f->ipiv[j]];
+      x[f->ipiv[j]] = t;
+    }
+    const double xj = x[j];
+    if (xj == 0.0) continue;
+    const int64_t ilast = n - 1 < j + kl ? n - 1 : j + kl;
+    for (int64_t i = j + 1; i <= ilast; ++i) x[i] = R(x[i] - R(AT(f, i, j) * xj, fmt), fmt);
+  }
+  for (int64_t j = n - 1; j >= 0; --j) {
+    const double xj = R(x[j] / AT(f, j, j), fmt);
+    x[j] = xj;
+    if (xj != 0.0) {
+      const int64_t ifirst = j - ubw > 0 ? j - ubw : 0;
+      for (int64_t i = ifirst; i < j; ++i) x[i] = R(x[i] - R(AT(f, i, j) * xj, fmt), fmt);
+    }
+  }
+}
+
+void orc_blu_free(orc_blu* f) {
+  free(f->ab);
+  free(f->ipiv);
+  memset(f, 0, sizeof(*f));
+}
+
+/* factorize + solve_factored (inner_solver.cpp:27-39) in one call: x = M \ rhs
+ * in fmt; returns 0 or the factorization's status (see orc_blu_factor). */
+int orc_lu_solve(const orc_csr* M, const double* rhs, int fmt, double* x) {
+  orc_blu f;
+  const int st = orc_blu_factor(M, fmt, &f);
+  if (st == 0) orc_blu_solve(&f, rhs, x);
+  orc_blu_free(&f);
+  return st;
+}
+#undef AT
+
 /* -------------------------------------------------------------------- solver */
 /* run_gadi_ir (solver.cpp:57-179) over CsrGadiSystem (solver.cpp:183-246). */
 int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
@@ -526,7 +646,7 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
   if (cfg->max_outer_iters < 1) return GADI_E_PARAM;
   const double uu = unit_roundoff(cfg->u), uf = unit_roundoff(cfg->u_f), ur = unit_roundoff(cfg->u_r);
   if (!(uu <= uf && uf <= ur)) return GADI_E_PARAM;
-  if (cfg->inner.method == GADI_INNER_LU_DIRECT) return GADI_E_UNSUPPORTED;
+  if (cfg->inner.method < 0 || cfg->inner.method > 2) return GADI_E_PARAM;
   const double xi = cfg->xi > 0.0 ? cfg->xi : (cfg->u == D ? 1e-26 : cfg->u == GADI_SINGLE ? 1e-8 : 1e-4);
   const int ur_p = cfg->u_r, u_p = cfg->u;
   /* inner arithmetic: u_r (the reference), or binary32 over binary16 storage
@@ -567,6 +687,20 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
     goto done;
   }
   orc_regularize(A, cfg->alpha, H.rp, H.ci, H.v, S.v); /* prepare, solver.cpp:199-208 */
+  const int lu = cfg->inner.method == GADI_INNER_LU_DIRECT;
+  orc_blu fH, fS;
+  memset(&fH, 0, sizeof(fH));
+  memset(&fS, 0, sizeof(fS));
+  if (lu) { /* prepare: factorize H then S in u_r (solver.cpp:204-207); a throw -> status (:74-82) */
+    int st = orc_blu_factor(&H, ur_p, &fH);
+    if (st == 0) st = orc_blu_factor(&S, ur_p, &fS);
+    if (st != 0) {
+      rep->status = st;
+      orc_blu_free(&fH);
+      orc_blu_free(&fS);
+      goto done;
+    }
+  }
 
   int e = 0;
   /* rounded_scaled_residual, solver.cpp:86-92 + scaling_exponent :48-53 */
@@ -611,15 +745,24 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
     if (k >= cfg->max_outer_iters) { rep->status = GADI_MAX_ITERS; break; }
 
     int it = 0, st = 0;
-    orc_krylov_af(&H, rhat, cfg->inner.method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
-                  cfg->inner.restart, ur_p, af_p, stop_norm, z, &it, &st);
+    if (lu) { /* inner_solve LuDirect (solver.cpp:226-231): no iterations, Overflow if non-finite */
+      orc_blu_solve(&fH, rhat, z);
+      st = all_finite(z, n) ? GADI_INNER_CONVERGED : GADI_INNER_OVERFLOW;
+    } else
+      orc_krylov_af(&H, rhat, cfg->inner.method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
+                    cfg->inner.restart, ur_p, af_p, stop_norm, z, &it, &st);
     rep->inner_iter_totals += it;
     rep->h_iters += it;
     if (st == GADI_INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
     if (st == GADI_INNER_STAGNATED) ++rep->inner_stagnations;
     orc_scale(p_rounded, z, n, ur_p, pz);
-    orc_krylov_af(&S, pz, s_method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
-                  cfg->inner.restart, ur_p, af_p, stop_norm, yv, &it, &st);
+    if (lu) {
+      it = 0;
+      orc_blu_solve(&fS, pz, yv);
+      st = all_finite(yv, n) ? GADI_INNER_CONVERGED : GADI_INNER_OVERFLOW;
+    } else
+      orc_krylov_af(&S, pz, s_method, cfg->inner.tol_epsilon, cfg->inner.max_inner_iters,
+                    cfg->inner.restart, ur_p, af_p, stop_norm, yv, &it, &st);
     rep->inner_iter_totals += it;
     rep->s_iters += it;
     if (st == GADI_INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
@@ -644,6 +787,8 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
     last = tn / nt0;
     PUSH_HIST(last);
   }
+  orc_blu_free(&fH);
+  orc_blu_free(&fS);
 done:
   rep->history_len = hl;
   free(s);

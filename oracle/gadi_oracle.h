@@ -76,6 +76,18 @@ int orc_krylov(const orc_csr* M, const double* rhs, int method, double eps, int 
 int orc_krylov_af(const orc_csr* M, const double* rhs, int method, double eps, int max_inner, int restart,
                   int fmt, int af, double stop_norm, double* x, int* iters, int* status);
 
+/* ---- band_lu.cpp:60-172 (BandLU) + inner_solver.cpp:27-39 ---- */
+typedef struct {
+  int64_t n, kl, ku, ldab;
+  int fmt;
+  double* ab;     /* ldab x n, column j at ab + j*ldab, A(i,j) at row kl+ku+i-j */
+  int64_t* ipiv;
+} orc_blu;
+int orc_blu_factor(const orc_csr* A, int fmt, orc_blu* f);
+void orc_blu_solve(const orc_blu* f, const double* rhs, double* x);
+void orc_blu_free(orc_blu* f);
+int orc_lu_solve(const orc_csr* M, const double* rhs, int fmt, double* x);
+
 /* ---- solver.cpp:57-179 + 250-258 (gadi_ir_solve on a CSR system) ---- */
 int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
               double* hist, int cap, gadi_report* rep);

@@ -153,6 +153,24 @@ int ref_krylov(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
   }
 }
 
+// factorize + solve_factored (inner_solver.cpp:27-39, band_lu.cpp): x = M \ rhs
+// in fmt. Returns 0, or the status the thrown exception maps to in
+// run_gadi_ir (solver.cpp:74-82): 4 SingularInPrecision, 3 OverflowDetected.
+int ref_lu_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* rhs,
+                 int fmt, double* x) {
+  try {
+    const Factorization f = factorize(csr(n, rp, ci, v), static_cast<Precision>(fmt), "M");
+    out(solve_factored(f, vec(rhs, n)), x);
+    return 0;
+  } catch (const SingularInPrecision&) {
+    return 4;
+  } catch (const OverflowDetected&) {
+    return 3;
+  } catch (...) {
+    return -1;
+  }
+}
+
 // hss_split + gadi_ir_solve (solver.cpp:250-258)
 int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
               const double* x0, const gadi_config* cfg, double* x, double* hist, int cap,

@@ -93,7 +93,16 @@ class FitError(GadiError):  # errors.hpp:40-42
     code = -4
 
 
-_ERRS = {-1: ContractViolation, -2: ParameterError, -3: UnsupportedError, -4: FitError}
+class SingularInPrecision(GadiError):  # errors.hpp: thrown by prepare (band_lu.cpp:106-108)
+    code = -9
+
+
+class OverflowDetected(GadiError):  # errors.hpp: thrown by prepare (band_lu.cpp:132-134)
+    code = -10
+
+
+_ERRS = {-1: ContractViolation, -2: ParameterError, -3: UnsupportedError, -4: FitError,
+         -9: SingularInPrecision, -10: OverflowDetected}
 
 
 # ---------------------------------------------------------------- ctypes structs

@@ -127,29 +127,60 @@ void validate(const gadi_config* c) {
     if (p < 0 || p > 2) throw Err(GADI_E_PARAM, "unknown precision");
   const double uu = unit_roundoff(c->u), uf = unit_roundoff(c->u_f), ur = unit_roundoff(c->u_r);
   if (!(uu <= uf && uf <= ur)) throw Err(GADI_E_PARAM, "precision triple must satisfy u <= u_f <= u_r");
-  if (c->inner.method == GADI_INNER_LU_DIRECT)
-    throw Err(GADI_E_UNSUPPORTED, "inner method lu_direct has no device implementation (use cg or gmres)");
-  if (c->inner.method != GADI_INNER_CG && c->inner.method != GADI_INNER_GMRES)
+  if (c->inner.method != GADI_INNER_LU_DIRECT && c->inner.method != GADI_INNER_CG &&
+      c->inner.method != GADI_INNER_GMRES)
     throw Err(GADI_E_PARAM, "unknown inner method");
   if (c->accum != GADI_ACCUM_NATIVE && c->accum != GADI_ACCUM_FP32) throw Err(GADI_E_PARAM, "unknown accum");
+}
+
+// prepare threw SingularInPrecision / OverflowDetected (the LuDirect
+// factorizations, inner_solver.cpp:27-34 -> band_lu.cpp:106-108,132-134);
+// run_gadi_ir turns it into the solve status (solver.cpp:74-82).
+struct PrepareStatus {
+  int status;
+};
+
+// Factor H then S in u_r when the method is LuDirect (solver.cpp:204-207).
+void lu_factors(gadi_handle* h, EngineBase* e) {
+  for (int which : {1, 2}) {
+    if (e->lu[which]) continue;
+    int st = 0;
+    e->lu[which] = lu_factor_build(h, which, e->alpha, e->u_r, &st);
+    h->launches += e->lu[which]->launches;
+    if (st != 0) {
+      lu_release(e->lu[which]);
+      e->lu[which] = nullptr;
+      throw PrepareStatus{st};
+    }
+  }
 }
 
 void prepare(gadi_handle* h, double alpha, double omega, int ur, const gadi_inner_spec& sp, int accum) {
   if (!(alpha > 0.0)) throw Err(GADI_E_PARAM, "regularize: alpha must be positive");
   if (!(omega >= 0.0 && omega < 2.0)) throw Err(GADI_E_PARAM, "regularize: omega must be in [0, 2)");
-  if (sp.method == GADI_INNER_LU_DIRECT)
-    throw Err(GADI_E_UNSUPPORTED, "inner method lu_direct has no device implementation (use cg or gmres)");
+  if (sp.method != GADI_INNER_LU_DIRECT && sp.method != GADI_INNER_CG && sp.method != GADI_INNER_GMRES)
+    throw Err(GADI_E_PARAM, "unknown inner method");
+  if (sp.method == GADI_INNER_LU_DIRECT && h->sharded())
+    throw Err(GADI_E_UNSUPPORTED, "lu_direct: not on a shard (the band LU is one device)");
   if (accum != GADI_ACCUM_NATIVE && accum != GADI_ACCUM_FP32) throw Err(GADI_E_PARAM, "unknown accum");
   if (sp.restart > 64) throw Err(GADI_E_UNSUPPORTED, "gmres restart > 64");
   auto& e = h->eng;
   const bool same = e && e->u_r == ur && e->accum == accum && std::max(1, e->spec.restart) == std::max(1, sp.restart);
-  if (same && e->alpha == alpha && e->omega == omega) {
-    e->spec = sp;
-    return;
+  if (!(same && e->alpha == alpha && e->omega == omega)) {
+    e.reset();
+    CK(cudaStreamSynchronize(h->stream));
+    e.reset(make_engine(h, sp, alpha, omega, ur, accum));
   }
-  e.reset();
-  CK(cudaStreamSynchronize(h->stream));
-  e.reset(make_engine(h, sp, alpha, omega, ur, accum));
+  e->spec = sp;
+  if (sp.method == GADI_INNER_LU_DIRECT) lu_factors(h, e.get());
+}
+
+// solve_H / solve_S through LuDirect (solver.cpp:226-231)
+InnerOut lu_solve(gadi_handle* h, EngineBase* e, int which, const void* rhs, void* x) {
+  const int64_t l0 = e->lu[which]->launches;
+  InnerOut o = lu_inner_solve(e->lu[which], rhs, x, h->stream);
+  h->launches += e->lu[which]->launches - l0;
+  return o;
 }
 
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
@@ -204,8 +235,15 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     finish();
     return;
   }
-  prepare(h, cfg->alpha, cfg->omega, cfg->u_r, cfg->inner, cfg->accum);
+  try {
+    prepare(h, cfg->alpha, cfg->omega, cfg->u_r, cfg->inner, cfg->accum);
+  } catch (const PrepareStatus& ps) {  // solver.cpp:74-82
+    rep->status = ps.status;
+    finish();
+    return;
+  }
   EngineBase* e = h->eng.get();
+  const bool lu = cfg->inner.method == GADI_INNER_LU_DIRECT;
 
   // rounded_scaled_residual (solver.cpp:86-92); when u_f is binary64 the same
   // pass also yields true_residual_norm (the reference recomputes it).
@@ -260,8 +298,9 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     const double target = cfg->inner.tol_epsilon * stop_norm;
     CK(cudaEventRecord(h->evA, s));
     // solve_H uses the spec method (solver.cpp:212-216)
-    InnerOut zo = cfg->inner.method == GADI_INNER_CG ? e->cg(1, e->rhat, e->z, target)
-                                                     : e->gmres(1, e->rhat, e->z, target);
+    InnerOut zo = lu                                  ? lu_solve(h, e, 1, e->rhat, e->z)
+                  : cfg->inner.method == GADI_INNER_CG ? e->cg(1, e->rhat, e->z, target)
+                                                       : e->gmres(1, e->rhat, e->z, target);
     CK(cudaEventRecord(h->evB, s));
     rep->inner_iter_totals += zo.iters;
     rep->h_iters += zo.iters;
@@ -269,7 +308,7 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     if (zo.status == INNER_STAGNATED) ++rep->inner_stagnations;
     e->scale_pz(p_rounded);
     // solve_S: a cg request degrades to gmres (solver.cpp:217-221)
-    InnerOut yo = e->gmres(2, e->pz, e->y, target);
+    InnerOut yo = lu ? lu_solve(h, e, 2, e->pz, e->y) : e->gmres(2, e->pz, e->y, target);
     CK(cudaEventRecord(h->evC, s));
     rep->inner_iter_totals += yo.iters;
     rep->s_iters += yo.iters;
@@ -626,7 +665,13 @@ int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r, c
   if (!h || !spec) throw Err(GADI_E_CONTRACT, "prepare: null argument");
   if (u_r < 0 || u_r > 2) throw Err(GADI_E_PARAM, "unknown precision");
   CK(cudaSetDevice(h->device));
-  prepare(h, alpha, omega, u_r, *spec, accum);
+  try {
+    prepare(h, alpha, omega, u_r, *spec, accum);
+  } catch (const PrepareStatus& ps) {  // the exceptions prepare throws (inner_solver.cpp:27-34)
+    if (ps.status == GADI_SINGULAR_IN_PRECISION)
+      throw Err(GADI_E_SINGULAR, "SingularInPrecision: pivot below the normal range of u_r");
+    throw Err(GADI_E_OVERFLOW, "OverflowDetected: non-finite entry produced during banded elimination");
+  }
   API_END
 }
 
@@ -647,7 +692,8 @@ static int inner_call(gadi_handle* h, int which, const double* rhs, double* x_ou
   e->to_inner(h->d_t64, e->rhat);
   const double target = e->spec.tol_epsilon * h->stop_norm;
   InnerOut o;
-  if (which == 1 && e->spec.method == GADI_INNER_CG) o = e->cg(1, e->rhat, e->z, target);
+  if (e->spec.method == GADI_INNER_LU_DIRECT) o = lu_solve(h, e, which, e->rhat, e->z);
+  else if (which == 1 && e->spec.method == GADI_INNER_CG) o = e->cg(1, e->rhat, e->z, target);
   else o = e->gmres(which, e->rhat, e->z, target);
   e->to_double(e->z, h->d_t64);
   CK(cudaMemcpyAsync(x_out, h->d_t64, h->N * 8, cudaMemcpyDeviceToHost, h->stream));

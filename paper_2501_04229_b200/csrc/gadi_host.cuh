@@ -547,9 +547,32 @@ struct InnerOut {
   int status = INNER_CONVERGED;
 };
 
+// A device band LU factorization (gadi_lu.cu; BandLU, band_lu.cpp).
+struct LuFactor {
+  int device = 0, prec = GADI_DOUBLE;
+  int64_t N = 0, kl = 0, ku = 0, ldab = 1;
+  void* ab = nullptr;         // ldab x N band (binary64, or binary32 for single/half)
+  int32_t* ipiv = nullptr;    // N pivot rows
+  void* xw = nullptr;         // solve work vector (N)
+  int* err = nullptr;         // [0] 1 singular / 2 non-finite, [1] column, [2] solve non-finite
+  int* bad = nullptr;
+  int64_t launches = 0;
+};
+namespace gadi_host {
+LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* status);
+void lu_release(LuFactor* f);
+InnerOut lu_inner_solve(LuFactor* f, const void* rhs, void* x, cudaStream_t s);
+}  // namespace gadi_host
+
 // The inner solvers for one (operator, storage, arithmetic) choice.
 struct EngineBase {
-  virtual ~EngineBase() = default;
+  virtual ~EngineBase() {
+    for (LuFactor*& f : lu) {
+      gadi_host::lu_release(f);
+      f = nullptr;
+    }
+  }
+  LuFactor* lu[3] = {nullptr, nullptr, nullptr};  // LuDirect factors of H (1) and S (2)
   int u_r = GADI_DOUBLE, accum = 0, cprec = GADI_DOUBLE;
   size_t tsize = 8;
   gadi_inner_spec spec{};

@@ -1,0 +1,614 @@
+// gadi_lu.cu — the LuDirect inner method on the device: BandLU
+// (band_lu.cpp:60-172), the reference's default inner solver
+// (inner_solver.hpp:21), built by prepare (solver.cpp:199-208) for H and S and
+// applied by inner_solve (solver.cpp:224-231).
+//
+// Storage is the reference's LAPACK band layout (band_lu.cpp:83): column j at
+// ab + j*ldab, A(i,j) at row kl+ku+i-j, ldab = 2kl+ku+1 (kl rows of pivot
+// fill). Values are binary64 for u_r = double and binary32 otherwise
+// (binary16 values carried exactly in binary32, as the reference does).
+// Every scalar op is rounded once to u_r with the reference's policies
+// (band_lu.cpp:12-56); the element-wise operation sequence is the
+// reference's, so factors and solutions are bit for bit the reference's.
+//
+// Factorization, blocked right-looking without changing any element's
+// operation order: for a panel of nb columns,
+//   k_lu_panel  one CTA factors the panel columns in shared memory (pivot
+//               search = block argmax with the reference's first-max/NaN
+//               rule, row swap inside the panel, multipliers, update of the
+//               remaining panel columns);
+//   k_lu_trail  one warp per trailing column replays the panel's nb steps on
+//               that column (swap, then x -= l*a unless a == 0), reading the
+//               multipliers from shared memory. A column's replay is the
+//               reference's sequence of operations on that column.
+// Solves (one CTA; the recurrences are sequential in j):
+//   k_lu_fwd    blocks of 32 steps: warp 0 runs the 32x32 unit-lower triangle
+//               through shuffles, bringing any pivot row outside the block up
+//               to date before its swap; then every thread applies the block's
+//               32 updates to the positions below in step order.
+//   k_lu_bwd    the same with U, blocks of 32 descending steps.
+#include "gadi_host.cuh"
+
+#include <cfloat>
+#include <climits>
+
+namespace gadi_host {
+namespace {
+
+template <int P>
+struct LuPol;
+template <>
+struct LuPol<GADI_DOUBLE> {  // PolDouble, band_lu.cpp:12-24
+  using S = double;
+  static __device__ __forceinline__ S mul(S a, S b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ S sub(S a, S b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ S div(S a, S b) { return __ddiv_rn(a, b); }
+  static constexpr double tiny = DBL_MIN;
+};
+template <>
+struct LuPol<GADI_SINGLE> {  // PolSingle, band_lu.cpp:28-38
+  using S = float;
+  static __device__ __forceinline__ S mul(S a, S b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ S sub(S a, S b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ S div(S a, S b) { return __fdiv_rn(a, b); }
+  static constexpr double tiny = FLT_MIN;
+};
+template <>
+struct LuPol<GADI_HALF> {  // PolHalf, band_lu.cpp:44-56: binary32 op, then one RNE to binary16
+  using S = float;
+  static __device__ __forceinline__ S r16(S v) { return __half2float(__float2half_rn(v)); }
+  static __device__ __forceinline__ S mul(S a, S b) { return r16(__fmul_rn(a, b)); }
+  static __device__ __forceinline__ S sub(S a, S b) { return r16(__fsub_rn(a, b)); }
+  static __device__ __forceinline__ S div(S a, S b) { return r16(__fdiv_rn(a, b)); }
+  static constexpr double tiny = 6.103515625e-05;  // 2^-14
+};
+
+__device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+constexpr int kPanelThreads = 1024;
+constexpr int kTrailWarps = 8;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+// ------------------------------------------------------------- band assembly
+// BandLU ctor (band_lu.cpp:85-90): at(i, c) = round(value) for the stored
+// entries of H or S. Stencil: the 7 coefficients of the regularized operator
+// (already rounded to u_r), neighbours outside the grid absent.
+template <class S>
+__global__ void k_band_stencil(S* __restrict__ ab, int64_t n, int64_t N, int64_t ldoff, int64_t ldab,
+                               double clo, double cd, double cup) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  const int64_t nn = n * n, i = r / nn, j = (r / n) % n, k = r % n;
+  auto put = [&](int64_t c, double v) { ab[c * ldab + ldoff + r - c] = (S)v; };
+  if (i > 0) put(r - nn, clo);
+  if (j > 0) put(r - n, clo);
+  if (k > 0) put(r - 1, clo);
+  put(r, cd);
+  if (k + 1 < n) put(r + 1, cup);
+  if (j + 1 < n) put(r + n, cup);
+  if (i + 1 < n) put(r + nn, cup);
+}
+
+// CSR: the HSS union pattern (gadi_csr.cuh k_union) with the diagonal shift of
+// regularize (splitting.cpp:37-47, sparse.cpp:180-183), rounded to u_r.
+template <class S, int PR>
+__global__ void k_band_csr(S* __restrict__ ab, int64_t N, int64_t ldoff, int64_t ldab, const int64_t* __restrict__ rp,
+                           const int32_t* __restrict__ ci, const double* __restrict__ val,
+                           const int64_t* __restrict__ dpos, const uint8_t* __restrict__ din, double alpha) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+    double x = val[k];
+    if (k == dpos[r]) x = din[r] ? __dadd_rn(__dmul_rn(1.0, x), alpha) : alpha;
+    const int64_t c = ci[k];
+    ab[c * ldab + ldoff + r - c] = (S)round_p<PR>(x);
+  }
+}
+
+__global__ void k_bandwidths(int64_t N, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             unsigned long long* bw) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N || rp[r] == rp[r + 1]) return;
+  const int64_t lo = r - ci[rp[r]], hi = ci[rp[r + 1] - 1] - r;
+  if (lo > 0) atomicMax(bw, (unsigned long long)lo);
+  if (hi > 0) atomicMax(bw + 1, (unsigned long long)hi);
+}
+
+// ------------------------------------------------------------ factorization
+template <int P>
+__global__ void __launch_bounds__(kPanelThreads) k_lu_panel(typename LuPol<P>::S* __restrict__ ab, int64_t N,
+                                                           int64_t kl, int64_t ku, int64_t ldab, int64_t j0,
+                                                           int nbw, int R, int32_t* __restrict__ ipiv,
+                                                           int* __restrict__ err) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  extern __shared__ __align__(16) unsigned char lu_smem[];
+  S* Pm = reinterpret_cast<S*>(lu_smem);  // Pm[c*R + r] = A(j0+r, j0+c)
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ int s_p, s_bad;
+  if (*(volatile int*)err) return;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int64_t ldoff = kl + ku;
+  for (int c = 0; c < nbw; ++c) {
+    const int64_t k = j0 + c;
+    for (int r = tid; r < R; r += nt) {
+      const int64_t d = ldoff + j0 + r - k;
+      Pm[c * R + r] = (d >= 0 && d < ldab) ? ab[k * ldab + d] : S(0);
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < nbw; ++c) {
+    const int64_t j = j0 + c;
+    const int rl = (int)(lmin(N - 1, j + kl) - j0);
+    S* col = Pm + c * R;
+    // pivot search, band_lu.cpp:95-104: the first row of maximal |a| (NaN never wins)
+    double bv = -1.0;
+    int br = INT_MAX;
+    for (int r = c + tid; r <= rl; r += nt) {
+      const double v = fabs((double)col[r]);
+      if (v > bv) {
+        bv = v;
+        br = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(~0u, bv, o);
+      const int orr = __shfl_xor_sync(~0u, br, o);
+      if (ov > bv || (ov == bv && orr < br)) {
+        bv = ov;
+        br = orr;
+      }
+    }
+    if (lane == 0) {
+      rv[warp] = bv;
+      ri[warp] = br;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      bv = lane < nw ? rv[lane] : -1.0;
+      br = lane < nw ? ri[lane] : INT_MAX;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(~0u, bv, o);
+        const int orr = __shfl_xor_sync(~0u, br, o);
+        if (ov > bv || (ov == bv && orr < br)) {
+          bv = ov;
+          br = orr;
+        }
+      }
+      if (lane == 0) {
+        const double d0 = fabs((double)col[c]);
+        int p = br;
+        double pmax = bv;
+        if (isnan(d0) || br == INT_MAX) {  // pmax starts at |a_jj|: NaN there keeps p = j
+          p = c;
+          pmax = d0;
+        }
+        s_bad = pmax < Pol::tiny;  // SingularInPrecision, band_lu.cpp:106-108
+        s_p = p;
+        if (s_bad) {
+          err[1] = (int)j;
+          err[0] = 1;
+        } else {
+          ipiv[j] = (int32_t)(j0 + p);
+        }
+      }
+    }
+    __syncthreads();
+    if (s_bad) return;
+    const int p = s_p;
+    const int cmax = (int)lmin(nbw - 1, lmin(N - 1, j + ldoff) - j0);  // columns <= klast
+    if (p != c)  // band_lu.cpp:110-113 (the trailing columns swap in k_lu_trail)
+      for (int cc = c + tid; cc <= cmax; cc += nt) {
+        const S t = Pm[cc * R + c];
+        Pm[cc * R + c] = Pm[cc * R + p];
+        Pm[cc * R + p] = t;
+      }
+    __syncthreads();
+    const S piv = col[c];
+    for (int r = c + 1 + tid; r <= rl; r += nt) {  // band_lu.cpp:115-126, one row per thread
+      const S l = Pol::div(col[r], piv);
+      col[r] = l;
+      for (int cc = c + 1; cc <= cmax; ++cc) {
+        const S a = Pm[cc * R + c];
+        if (a != S(0)) Pm[cc * R + r] = Pol::sub(Pm[cc * R + r], Pol::mul(l, a));
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = 0; c < nbw; ++c) {
+    const int64_t k = j0 + c;
+    for (int r = tid; r < R; r += nt) {
+      const int64_t d = ldoff + j0 + r - k;
+      if (d >= 0 && d < ldab) ab[k * ldab + d] = Pm[c * R + r];
+    }
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kTrailWarps * 32) k_lu_trail(typename LuPol<P>::S* __restrict__ ab, int64_t N,
+                                                               int64_t kl, int64_t ku, int64_t ldab, int64_t j0,
+                                                               int nbw, int R, const int32_t* __restrict__ ipiv,
+                                                               const int* __restrict__ err, int64_t kfirst,
+                                                               int64_t kend) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  extern __shared__ __align__(16) unsigned char lu_smem[];
+  __shared__ int pv[32];
+  if (*(volatile int*)err) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  S* Lm = reinterpret_cast<S*>(lu_smem);  // the panel's multipliers, Lm[c*R + r]
+  S* cb = Lm + (size_t)nbw * R + (size_t)warp * R;
+  const int64_t ldoff = kl + ku;
+  for (int c = 0; c < nbw; ++c) {
+    const int64_t k = j0 + c;
+    for (int r = c + 1 + tid; r < R; r += blockDim.x) Lm[c * R + r] = ab[k * ldab + ldoff + j0 + r - k];
+  }
+  if (tid < nbw) pv[tid] = ipiv[j0 + tid] - (int)j0;
+  __syncthreads();
+  for (int64_t k = kfirst + (int64_t)blockIdx.x * kTrailWarps + warp; k <= kend;
+       k += (int64_t)gridDim.x * kTrailWarps) {
+    const int rlo = (int)lmax(0, k - ldoff - j0), rhi = (int)lmin(R - 1, k + kl - j0);
+    S* colk = ab + k * ldab + ldoff + j0 - k;  // colk[r] = A(j0+r, k)
+    for (int r = rlo + lane; r <= rhi; r += 32) cb[r] = colk[r];
+    __syncwarp();
+    for (int c = 0; c < nbw; ++c) {
+      const int64_t j = j0 + c;
+      if (k > j + ldoff) continue;  // beyond klast(j): neither swapped nor updated at step j
+      const int p = pv[c];
+      if (p != c) {
+        if (lane == 0) {
+          const S t = cb[c];
+          cb[c] = cb[p];
+          cb[p] = t;
+        }
+        __syncwarp();
+      }
+      const S a = cb[c];
+      if (a != S(0)) {  // band_lu.cpp:121-122
+        const int rl = (int)(lmin(N - 1, j + kl) - j0);
+        for (int r = c + 1 + lane; r <= rl; r += 32) cb[r] = Pol::sub(cb[r], Pol::mul(Lm[c * R + r], a));
+      }
+      __syncwarp();
+    }
+    for (int r = rlo + lane; r <= rhi; r += 32) colk[r] = cb[r];
+    __syncwarp();
+  }
+}
+
+template <class S>
+__global__ void k_lu_nonfinite(const S* __restrict__ ab, int64_t n, int* err) {  // band_lu.cpp:132-134
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite((double)ab[t])) {
+      err[0] = 2;
+      return;
+    }
+}
+
+// ------------------------------------------------------------------- solves
+template <class T, class S>
+__global__ void k_lu_in(const T* __restrict__ src, S* __restrict__ x, int64_t N) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) x[i] = (S)to_dbl(src[i]);  // from_double of a u_r value: exact
+}
+
+template <class T, class S>
+__global__ void k_lu_out(const S* __restrict__ x, T* __restrict__ dst, int64_t N, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const S v = x[i];
+  dst[i] = from_dbl<T>((double)v);
+  if (!isfinite((double)v)) *bad = 1;  // all_finite, solver.cpp:229
+}
+
+// forward sweep, band_lu.cpp:148-157
+template <int P>
+__global__ void __launch_bounds__(512, 1) k_lu_fwd(const typename LuPol<P>::S* __restrict__ ab, int64_t N,
+                                                     int64_t kl, int64_t ku, int64_t ldab,
+                                                     const int32_t* __restrict__ ipiv,
+                                                     typename LuPol<P>::S* __restrict__ x) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  __shared__ S xb[32];
+  __shared__ int64_t tpos[32];
+  __shared__ int64_t tat[32];
+  __shared__ int ntab;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t ldoff = kl + ku;
+  for (int64_t j0 = 0; j0 < N; j0 += 32) {
+    const int nb = (int)lmin(32, N - j0);
+    if (tid < 32) {
+      S v = lane < nb ? x[j0 + lane] : S(0);
+      S Lr[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        Lr[c] = (c < lane && lane < nb && lane - c <= kl) ? ab[(j0 + c) * ldab + ldoff + lane - c] : S(0);
+      const int pvl = lane < nb ? ipiv[j0 + lane] : 0;
+      int cnt = 0;  // lane 0: swapped positions beyond the block and the step they are current through
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        if (c < nb) {
+          const int64_t j = j0 + c;
+          const int64_t p = __shfl_sync(~0u, pvl, c);
+          if (p != j) {
+            const S vc = __shfl_sync(~0u, v, c);
+            if (p < j0 + nb) {
+              const S vp = __shfl_sync(~0u, v, (int)(p - j0));
+              if (lane == c) v = vp;
+              if (lane == (int)(p - j0)) v = vc;
+            } else {
+              S val = S(0);
+              if (lane == 0) {
+                int slot = -1;
+                int64_t at = j0 - 1;
+                for (int t = 0; t < cnt; ++t)
+                  if (tpos[t] == p) {
+                    slot = t;
+                    at = tat[t];
+                  }
+                val = x[p];
+                for (int64_t jj = at + 1; jj < j; ++jj) {
+                  const S xj = xb[jj - j0];
+                  if (xj != S(0) && p <= jj + kl) val = Pol::sub(val, Pol::mul(ab[jj * ldab + ldoff + p - jj], xj));
+                }
+                x[p] = vc;
+                if (slot < 0) slot = cnt++;
+                tpos[slot] = p;
+                tat[slot] = j - 1;
+              }
+              val = __shfl_sync(~0u, val, 0);
+              if (lane == c) v = val;
+            }
+          }
+          const S xj = __shfl_sync(~0u, v, c);
+          if (lane == 0) xb[c] = xj;
+          if (xj != S(0) && lane > c && lane < nb && lane - c <= kl) v = Pol::sub(v, Pol::mul(Lr[c], xj));
+        }
+      }
+      if (lane < nb) x[j0 + lane] = v;
+      if (lane == 0) ntab = cnt;
+    }
+    __syncthreads();
+    const int64_t iend = lmin(N - 1, j0 + nb - 1 + kl);
+    for (int64_t i = j0 + nb + tid; i <= iend; i += blockDim.x) {
+      int64_t at = j0 - 1;
+      for (int t = 0; t < ntab; ++t)
+        if (tpos[t] == i) at = tat[t];
+      const int c0 = (int)(at - j0 + 1);
+      S l[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int64_t j = j0 + c;
+        l[c] = (c >= c0 && c < nb && i <= j + kl) ? ab[j * ldab + ldoff + i - j] : S(0);
+      }
+      S val = x[i];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const S xj = xb[c];
+        if (c >= c0 && c < nb && xj != S(0) && i <= j0 + c + kl) val = Pol::sub(val, Pol::mul(l[c], xj));
+      }
+      x[i] = val;
+    }
+    __syncthreads();
+  }
+}
+
+// back substitution, band_lu.cpp:159-167
+template <int P>
+__global__ void __launch_bounds__(512, 1) k_lu_bwd(const typename LuPol<P>::S* __restrict__ ab, int64_t N,
+                                                     int64_t kl, int64_t ku, int64_t ldab,
+                                                     typename LuPol<P>::S* __restrict__ x) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  __shared__ S xb[32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t ldoff = kl + ku;  // ubw
+  for (int64_t jhi = N - 1; jhi >= 0; jhi -= 32) {
+    const int64_t jlo = lmax(0, jhi - 31);
+    const int nb = (int)(jhi - jlo + 1);
+    if (tid < 32) {
+      S v = lane < nb ? x[jlo + lane] : S(0);
+      const S dg = lane < nb ? ab[(jlo + lane) * ldab + ldoff] : S(1);
+      S Ur[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        Ur[c] = (lane < c && c < nb && c - lane <= ldoff) ? ab[(jlo + c) * ldab + ldoff + lane - c] : S(0);
+#pragma unroll
+      for (int c = 31; c >= 0; --c) {
+        if (c < nb) {
+          if (lane == c) v = Pol::div(v, dg);
+          const S xj = __shfl_sync(~0u, v, c);
+          if (lane == 0) xb[c] = xj;
+          if (xj != S(0) && lane < c && c - lane <= ldoff) v = Pol::sub(v, Pol::mul(Ur[c], xj));
+        }
+      }
+      if (lane < nb) x[jlo + lane] = v;
+    }
+    __syncthreads();
+    const int64_t ifirst = lmax(0, jlo - ldoff);
+    for (int64_t i = ifirst + tid; i < jlo; i += blockDim.x) {
+      S u[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int64_t j = jlo + c;
+        u[c] = (c < nb && j - i <= ldoff) ? ab[j * ldab + ldoff + i - j] : S(0);
+      }
+      S val = x[i];
+#pragma unroll
+      for (int c = 31; c >= 0; --c) {
+        const S xj = xb[c];
+        if (c < nb && xj != S(0) && jlo + c - i <= ldoff) val = Pol::sub(val, Pol::mul(u[c], xj));
+      }
+      x[i] = val;
+    }
+    __syncthreads();
+  }
+}
+
+template <class S>
+inline void pick_panel(int64_t kl, int& nb) {
+  nb = 32;
+  while (nb > 1 && (size_t)(nb + kTrailWarps) * (size_t)(nb + kl) * sizeof(S) > kSmemBudget) nb >>= 1;
+  if ((size_t)(nb + kTrailWarps) * (size_t)(nb + kl) * sizeof(S) > kSmemBudget)
+    throw Err(GADI_E_UNSUPPORTED, "lu_direct: the lower bandwidth " + std::to_string(kl) +
+                                      " is too wide for the device band LU (shared-memory panel)");
+}
+
+template <int P>
+int factor_impl(LuFactor* f, cudaStream_t s) {
+  using S = typename LuPol<P>::S;
+  const int64_t N = f->N, kl = f->kl, ku = f->ku, ldab = f->ldab;
+  int nb;
+  pick_panel<S>(kl, nb);
+  S* ab = static_cast<S*>(f->ab);
+  const size_t smem_max = (size_t)(nb + kTrailWarps) * (size_t)(nb + kl) * sizeof(S);
+  smem_attr(k_lu_panel<P>, smem_max);
+  smem_attr(k_lu_trail<P>, smem_max);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device);
+  for (int64_t j0 = 0; j0 < N; j0 += nb) {
+    const int nbw = (int)std::min<int64_t>(nb, N - j0);
+    const int R = (int)(std::min<int64_t>(N - 1, j0 + nbw - 1 + kl) - j0 + 1);
+    k_lu_panel<P><<<1, kPanelThreads, (size_t)nbw * R * sizeof(S), s>>>(ab, N, kl, ku, ldab, j0, nbw, R, f->ipiv,
+                                                                        f->err);
+    const int64_t kfirst = j0 + nbw, kend = std::min<int64_t>(N - 1, j0 + nbw - 1 + kl + ku);
+    if (kfirst <= kend) {
+      const int64_t cols = kend - kfirst + 1;
+      const unsigned grid = (unsigned)std::min<int64_t>((cols + kTrailWarps - 1) / kTrailWarps, sms);
+      k_lu_trail<P><<<grid, kTrailWarps * 32, (size_t)(nbw + kTrailWarps) * R * sizeof(S), s>>>(
+          ab, N, kl, ku, ldab, j0, nbw, R, f->ipiv, f->err, kfirst, kend);
+    }
+    f->launches += 2;
+  }
+  CKL();
+  int herr[2] = {0, 0};
+  CK(cudaMemcpyAsync(herr, f->err, sizeof(herr), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (herr[0] == 1) return GADI_SINGULAR_IN_PRECISION;
+  k_lu_nonfinite<S><<<(unsigned)sms * 4, 256, 0, s>>>(ab, ldab * N, f->err);
+  CKL();
+  ++f->launches;
+  CK(cudaMemcpyAsync(herr, f->err, sizeof(herr), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return herr[0] == 2 ? GADI_OVERFLOW_DETECTED : 0;
+}
+
+template <int P, class T>
+void solve_impl(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
+  using S = typename LuPol<P>::S;
+  const int64_t N = f->N;
+  S* xw = static_cast<S*>(f->xw);
+  const S* ab = static_cast<const S*>(f->ab);
+  const unsigned g = (unsigned)((N + 255) / 256);
+  k_lu_in<T, S><<<g, 256, 0, s>>>(static_cast<const T*>(rhs), xw, N);
+  k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
+  k_lu_bwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw);
+  k_lu_out<T, S><<<g, 256, 0, s>>>(xw, static_cast<T*>(x), N, f->bad);
+  CKL();
+  f->launches += 4;
+}
+
+}  // namespace
+
+// Builds and factors the band image of H (which = 1) or S (which = 2) of the
+// regularized pair in u_r (prepare, solver.cpp:204-207). Returns the factor
+// and sets *status to 0 or the SolveStatus of the reference's exception.
+LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* status) {
+  if (h->sharded()) throw Err(GADI_E_UNSUPPORTED, "lu_direct: not on a shard (the band LU is one device)");
+  std::unique_ptr<LuFactor> f(new LuFactor);
+  f->device = h->device;
+  f->prec = ur;
+  f->N = h->N;
+  if (h->stencil()) {
+    f->kl = f->ku = h->n > 1 ? h->n * h->n : 0;  // the i-1 / i+1 neighbours
+  } else {  // lower/upper_bandwidth of the union pattern (sparse.cpp:142-154)
+    unsigned long long* bw = dalloc<unsigned long long>(2);
+    CK(cudaMemsetAsync(bw, 0, 16, h->stream));
+    k_bandwidths<<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, h->d_urp, h->d_uci, bw);
+    CKL();
+    unsigned long long hb[2];
+    CK(cudaMemcpyAsync(hb, bw, 16, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(bw);
+    f->kl = (int64_t)hb[0];
+    f->ku = (int64_t)hb[1];
+  }
+  f->ldab = 2 * f->kl + f->ku + 1;
+  const size_t es = ur == GADI_DOUBLE ? 8 : 4;
+  cudaStream_t s = h->stream;
+  CK(cudaMalloc(&f->ab, (size_t)f->ldab * (size_t)f->N * es));
+  CK(cudaMemsetAsync(f->ab, 0, (size_t)f->ldab * (size_t)f->N * es, s));
+  CK(cudaMalloc(&f->ipiv, (size_t)f->N * sizeof(int32_t)));
+  CK(cudaMalloc(&f->xw, (size_t)f->N * es));
+  CK(cudaMalloc(&f->err, 4 * sizeof(int)));
+  CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
+  f->bad = f->err + 2;
+  const int64_t ldoff = f->kl + f->ku, N = f->N;
+  const unsigned g = (unsigned)((N + 255) / 256);
+  if (h->stencil()) {
+    // regularize of the HSS split (splitting.cpp:12-20,37-47) in closed form, as Engine::build_ops
+    const double t1 = h->t1, t2 = h->t2, t3 = h->t3;
+    double lo, dg, up;
+    if (which == 1) {
+      lo = 0.5 * t2 + 0.5 * t3;
+      up = 0.5 * t3 + 0.5 * t2;
+      dg = 1.0 * (0.5 * t1 + 0.5 * t1) + alpha;
+    } else {
+      lo = 0.5 * t2 + -0.5 * t3;
+      up = 0.5 * t3 + -0.5 * t2;
+      dg = 1.0 * (0.5 * t1 + -0.5 * t1) + alpha;
+    }
+    lo = hround(lo, ur);
+    dg = hround(dg, ur);
+    up = hround(up, ur);
+    if (ur == GADI_DOUBLE)
+      k_band_stencil<double><<<g, 256, 0, s>>>((double*)f->ab, h->n, N, ldoff, f->ldab, lo, dg, up);
+    else
+      k_band_stencil<float><<<g, 256, 0, s>>>((float*)f->ab, h->n, N, ldoff, f->ldab, lo, dg, up);
+  } else {
+    const double* v = which == 1 ? h->d_mv : h->d_nv;
+    if (ur == GADI_DOUBLE)
+      k_band_csr<double, P_DOUBLE><<<g, 256, 0, s>>>((double*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
+                                                       h->d_dpos, h->d_din, alpha);
+    else if (ur == GADI_SINGLE)
+      k_band_csr<float, P_SINGLE><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
+                                                      h->d_dpos, h->d_din, alpha);
+    else
+      k_band_csr<float, P_HALF><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
+                                                    h->d_dpos, h->d_din, alpha);
+  }
+  CKL();
+  ++f->launches;
+  *status = ur == GADI_DOUBLE ? factor_impl<GADI_DOUBLE>(f.get(), s)
+            : ur == GADI_SINGLE ? factor_impl<GADI_SINGLE>(f.get(), s)
+                                : factor_impl<GADI_HALF>(f.get(), s);
+  return f.release();
+}
+
+void lu_release(LuFactor* f) {
+  if (!f) return;
+  for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err})
+    if (p) cudaFree(p);
+  delete f;
+}
+
+// inner_solve LuDirect (solver.cpp:226-231): x = solve_factored(rhs) in u_r,
+// Overflow when x is not finite; rhs / x in the engine's u_r storage.
+InnerOut lu_inner_solve(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
+  CK(cudaMemsetAsync(f->bad, 0, sizeof(int), s));
+  if (f->prec == GADI_DOUBLE) solve_impl<GADI_DOUBLE, double>(f, rhs, x, s);
+  else if (f->prec == GADI_SINGLE) solve_impl<GADI_SINGLE, float>(f, rhs, x, s);
+  else solve_impl<GADI_HALF, __half>(f, rhs, x, s);
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, f->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  InnerOut o;
+  o.iters = 0;
+  o.status = bad ? INNER_OVERFLOW : INNER_CONVERGED;
+  return o;
+}
+
+}  // namespace gadi_host

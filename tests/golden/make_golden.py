@@ -15,7 +15,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle import CG, DOUBLE, GMRES, HALF, SINGLE, Config, Oracle, Reference  # noqa: E402
+from oracle import CG, CSR, DOUBLE, GMRES, HALF, SINGLE, Config, Oracle, Reference  # noqa: E402
+
+LU = 0  # InnerMethod::LuDirect
 
 
 def main():
@@ -78,6 +80,39 @@ def main():
         out[f"solve_{tag}_info"] = np.array([rep.status, rep.outer_iters, rep.inner_iter_totals,
                                              rep.inner_stagnations], dtype=np.int64)
         out[f"solve_{tag}_cfg"] = np.array([n, ur, alpha, seed, lo, hi])
+
+    # 6. LuDirect (BandLU, band_lu.cpp; the reference's default inner method):
+    #    factor + solve of H and S of sections 3 (n = 5, 8), a pivoting case
+    #    (strong convection, small alpha: S is far from diagonally dominant),
+    #    the two exceptions, and whole solves with inner lu.
+    lu_mats = {}
+    for n in (5, 8):
+        H = CSR(out[f"k{n}_H_rp"].size - 1, out[f"k{n}_H_rp"], out[f"k{n}_H_ci"], out[f"k{n}_H_v"])
+        S = CSR(H.n, H.rp, H.ci, out[f"k{n}_S_v"])
+        lu_mats[f"k{n}H"], lu_mats[f"k{n}S"] = H, S
+    Ap = o.convdiff(6, r=0.45)
+    Hp, Sp = R.regularize(Ap, 0.02)
+    lu_mats["pivH"], lu_mats["pivS"] = Hp, Sp
+    out["lu_piv_rp"], out["lu_piv_ci"], out["lu_piv_H"], out["lu_piv_S"] = Hp.rp, Hp.ci, Hp.v, Sp.v
+    out["lu_sing_v"] = np.array([1e-6, 2.0, 3.0])           # diagonal: below binary16 min_normal
+    out["lu_ovf_v"] = np.array([1.0, 60000.0, 0.5, -60000.0])  # U22 = -90000 overflows binary16
+    lu_mats["sing"] = CSR(3, np.array([0, 1, 2, 3]), np.array([0, 1, 2]), out["lu_sing_v"])
+    lu_mats["ovf"] = CSR(2, np.array([0, 2, 4]), np.array([0, 1, 0, 1]), out["lu_ovf_v"])
+    for tag, M in lu_mats.items():
+        for p, nm in ((HALF, "h"), (SINGLE, "s"), (DOUBLE, "d")):
+            rhs = R.round(rng.uniform(-1, 1, M.n), p)
+            x, st = R.lu_solve(M, rhs, p)
+            out[f"lu_{tag}_{nm}_rhs"], out[f"lu_{tag}_{nm}_x"], out[f"lu_{tag}_{nm}_st"] = rhs, x, np.array([st])
+    lu_solves = [("luh8", 8, HALF, 0.1), ("lus8", 8, SINGLE, 0.1), ("lud6", 6, DOUBLE, 0.5), ("luh12", 12, HALF, 0.3)]
+    for tag, n, ur, alpha in lu_solves:
+        A = o.convdiff(n)
+        _, b = o.make_rhs(A, 0, 0.0, 1.0)
+        cfg = Config.make(alpha=alpha, xi=1e-20 if ur != HALF else 1e-8, u_r=ur, method=LU)
+        x, rep, hist = R.solve(A, b, cfg)
+        out[f"solve_{tag}_b"], out[f"solve_{tag}_x"], out[f"solve_{tag}_hist"] = b, x, hist
+        out[f"solve_{tag}_info"] = np.array([rep.status, rep.outer_iters, rep.inner_iter_totals,
+                                             rep.inner_stagnations], dtype=np.int64)
+        out[f"solve_{tag}_cfg"] = np.array([n, ur, alpha, 0, 0.0, 1.0])
 
     # 5. GPR fit/predict through the reference's gpr.cpp (Eigen restated in oracle/eigen_shim)
     sizes = np.array([8 ** 3, 12 ** 3, 16 ** 3, 24 ** 3, 32 ** 3, 48 ** 3, 64 ** 3], dtype=np.int64)
