@@ -27,6 +27,8 @@ inline void check(int rc) {
     case GADI_E_PARAM: throw ParameterError(msg);
     case GADI_E_CONTRACT: throw ContractViolation(msg);
     case GADI_E_UNSUPPORTED: throw ParameterError("unsupported on the device: " + msg);
+    case GADI_E_SINGULAR: throw SingularInPrecision(msg);  // prepare, band_lu.cpp:106-108
+    case GADI_E_OVERFLOW: throw OverflowDetected(msg);     // prepare, band_lu.cpp:132-134
     default: throw std::runtime_error("gadi_cuda error " + std::to_string(rc) + ": " + msg);
   }
 }

@@ -556,6 +556,11 @@ struct LuFactor {
   void* xw = nullptr;         // solve work vector (N)
   int* err = nullptr;         // [0] 1 singular / 2 non-finite, [1] column, [2] solve non-finite
   int* bad = nullptr;
+  unsigned* flags = nullptr;  // pipelined solves: per-block epoch flags, then the block ticket
+  unsigned* ticket = nullptr;
+  unsigned epoch = 0;
+  bool swaps = false;         // any row interchange (forward solve needs the swap-aware kernel)
+  int sms = 148;
   int64_t launches = 0;
 };
 namespace gadi_host {

@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(kPanelThreads) k_lu_panel(typename LuPol<P>::S
           err[0] = 1;
         } else {
           ipiv[j] = (int32_t)(j0 + p);
+          if (p != c) err[3] = 1;  // a row interchange: the forward solve takes the swap-aware kernel
         }
       }
     }
@@ -448,6 +449,98 @@ __global__ void __launch_bounds__(512, 1) k_lu_bwd(const typename LuPol<P>::S* _
   }
 }
 
+// ------------------------------------------------- pipelined solves (no swaps)
+// Without row interchanges (ipiv[j] == j: every H, and S whenever it is
+// column diagonally dominant) element i of the forward sweep receives exactly
+// the updates x_i -= L(i,j) x_j for j = i-kl .. i-1 ascending (skipping
+// x_j == 0), and element i of the back sweep x_i -= U(i,j) x_j for j =
+// i+ubw .. i+1 descending, then x_i /= U(i,i) (band_lu.cpp:148-167). That
+// per-element sequence does not depend on how the sweep is scheduled, so the
+// 32-position blocks are processed by many CTAs at once: a CTA claims the next
+// block in sweep order from a ticket (claimed blocks only wait on earlier
+// claimed blocks: no deadlock whatever else runs on the device), applies the
+// updates of each earlier block as soon as its flag carries this solve's
+// epoch, runs its own 32 x 32 triangle through shuffles, publishes x and
+// raises its flag. The band reads are coalesced: for a fixed column the 32
+// lanes read 32 consecutive band rows.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int P, bool FWD>
+__global__ void __launch_bounds__(32) k_lu_pipe(const typename LuPol<P>::S* __restrict__ ab, int64_t N, int64_t kl,
+                                                int64_t ku, int64_t ldab, typename LuPol<P>::S* x,
+                                                unsigned* __restrict__ flags, unsigned* __restrict__ ticket,
+                                                unsigned epoch) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  const int lane = threadIdx.x;
+  const int64_t ldoff = kl + ku, nblk = (N + 31) / 32, reach = FWD ? kl : ldoff;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    t = __shfl_sync(~0u, t, 0);
+    if ((int64_t)t >= nblk) return;
+    const int64_t b = FWD ? (int64_t)t : nblk - 1 - (int64_t)t;  // block b holds positions 32b .. 32b+31
+    const int64_t i = 32 * b + lane;
+    const bool live = i < N;
+    S v = live ? x[i] : S(0);
+    // earlier blocks in sweep order whose columns reach this block
+    const int64_t dlo = FWD ? (32 * b - reach > 0 ? (32 * b - reach) / 32 : 0) : b + 1;
+    const int64_t dhi = FWD ? b - 1 : (32 * b + 31 + reach < N - 1 ? (32 * b + 31 + reach) / 32 : nblk - 1);
+    for (int64_t s = 0; s <= dhi - dlo; ++s) {
+      const int64_t d = FWD ? dlo + s : dhi - s;  // ascending j (forward), descending j (back)
+      S m[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {  // the band entries, issued before the wait
+        const int64_t j = 32 * d + c;
+        const int64_t off = FWD ? i - j : j - i;
+        m[c] = (live && j < N && off >= 1 && off <= reach) ? ab[j * ldab + ldoff + i - j] : S(0);
+      }
+      while (ld_acquire(flags + d) != epoch) {
+      }
+      const S xd = (32 * d + lane < N) ? __ldcg(x + 32 * d + lane) : S(0);
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const int c = FWD ? cc : 31 - cc;
+        const int64_t j = 32 * d + c;
+        const int64_t off = FWD ? i - j : j - i;
+        const S xj = __shfl_sync(~0u, xd, c);
+        if (live && xj != S(0) && j < N && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
+      }
+    }
+    // own triangle
+    S m[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int64_t j = 32 * b + c;
+      const int64_t off = FWD ? i - j : j - i;
+      m[c] = (live && j < N && off >= 0 && off <= reach && (FWD ? off >= 1 : true)) ? ab[j * ldab + ldoff + i - j]
+                                                                                    : S(1);
+    }
+#pragma unroll
+    for (int cc = 0; cc < 32; ++cc) {
+      const int c = FWD ? cc : 31 - cc;
+      const int64_t j = 32 * b + c;
+      if (j < N) {
+        if (!FWD && lane == c) v = Pol::div(v, m[c]);  // U(j,j)
+        const S xj = __shfl_sync(~0u, v, c);
+        const int64_t off = FWD ? i - j : j - i;
+        if (live && xj != S(0) && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
+      }
+    }
+    if (live) x[i] = v;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(flags + b, epoch);
+  }
+}
+
 template <class S>
 inline void pick_panel(int64_t kl, int& nb) {
   nb = 32;
@@ -484,10 +577,12 @@ int factor_impl(LuFactor* f, cudaStream_t s) {
     f->launches += 2;
   }
   CKL();
-  int herr[2] = {0, 0};
+  int herr[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(herr, f->err, sizeof(herr), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (herr[0] == 1) return GADI_SINGULAR_IN_PRECISION;
+  f->swaps = herr[3] != 0;
+  f->sms = sms;
   k_lu_nonfinite<S><<<(unsigned)sms * 4, 256, 0, s>>>(ab, ldab * N, f->err);
   CKL();
   ++f->launches;
@@ -504,8 +599,16 @@ void solve_impl(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
   const S* ab = static_cast<const S*>(f->ab);
   const unsigned g = (unsigned)((N + 255) / 256);
   k_lu_in<T, S><<<g, 256, 0, s>>>(static_cast<const T*>(rhs), xw, N);
-  k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
-  k_lu_bwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw);
+  const int64_t nblk = (N + 31) / 32;
+  const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)f->sms * 16);
+  if (f->swaps) {  // row interchanges in the forward sweep: one CTA (k_lu_fwd handles the swaps)
+    k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
+  } else {
+    CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
+    k_lu_pipe<P, true><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
+  }
+  CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
+  k_lu_pipe<P, false><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
   k_lu_out<T, S><<<g, 256, 0, s>>>(xw, static_cast<T*>(x), N, f->bad);
   CKL();
   f->launches += 4;
@@ -545,6 +648,9 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
   CK(cudaMalloc(&f->xw, (size_t)f->N * es));
   CK(cudaMalloc(&f->err, 4 * sizeof(int)));
   CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
+  CK(cudaMalloc(&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned)));
+  CK(cudaMemsetAsync(f->flags, 0, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
+  f->ticket = f->flags + (f->N + 31) / 32;
   f->bad = f->err + 2;
   const int64_t ldoff = f->kl + f->ku, N = f->N;
   const unsigned g = (unsigned)((N + 255) / 256);
@@ -590,7 +696,7 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
 
 void lu_release(LuFactor* f) {
   if (!f) return;
-  for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err})
+  for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err, (void*)f->flags})
     if (p) cudaFree(p);
   delete f;
 }
