@@ -88,7 +88,8 @@ typedef enum {
    * throws for LU_DIRECT (band_lu.cpp:106-108,132-134); gadi_cuda_solve
    * reports them as statuses, as run_gadi_ir does (solver.cpp:74-82). */
   GADI_E_SINGULAR = -9,    /* SingularInPrecision */
-  GADI_E_OVERFLOW = -10    /* OverflowDetected    */
+  GADI_E_OVERFLOW = -10,   /* OverflowDetected    */
+  GADI_E_NO_CONVERGENT_ALPHA = -11 /* NoConvergentAlpha (errors.hpp), alpha_bisection */
 } gadi_error;
 
 /* InnerSolverSpec, inner_solver.hpp:20-25; defaults from gadi_config_default. */
@@ -290,6 +291,33 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
 int gadi_gpr_params(const gadi_gpr* g, double* sigma_f2, double* length, double* sigma_n2,
                     double* lml, double* target_mean);
 int gadi_gpr_destroy(gadi_gpr* g);
+
+/* ---- GPR training-set generation (gpr.hpp:37-58; gpr.cpp:15-68) over the
+ * reference's convdiff family: size parameter n -> build_convdiff3d({n})
+ * (r = 1/(2n+2), b = A * ones, problems.cpp:8-43), HSS split. Each probe is a
+ * full device solve with u_r = u = u_f = fmt; the probes run concurrently
+ * (a pool of host threads, one handle and stream each; GADI_TRAIN_WORKERS,
+ * default 16) and are chosen in the reference's probe order, so the result is
+ * the reference's. ---- */
+typedef struct {            /* DichotomySettings, gpr.hpp:37-44 */
+  double alpha_lo;          /* 1e-2 */
+  double alpha_hi;          /* 1e2 */
+  int32_t budget;           /* 21 log-grid probes */
+  double train_xi;          /* 1e-8 */
+  int32_t max_outer;        /* 1500 */
+  gadi_inner_spec inner;    /* InnerSolverSpec{}: lu_direct, 1e-2, 1000, 30 */
+} gadi_dichotomy;
+void gadi_dichotomy_default(gadi_dichotomy* st);
+/* alpha_bisection (gpr.cpp:15-50): the grid alpha with the fewest outer
+ * iterations among converged probes (ties: the smaller alpha). Errors:
+ * GADI_E_PARAM (bracket, budget < 3), GADI_E_NO_CONVERGENT_ALPHA. */
+int gadi_alpha_bisection(int64_t size_param, int32_t fmt, double alpha_lo, double alpha_hi, int32_t budget,
+                         const gadi_dichotomy* st, int32_t device, double* alpha, int32_t* iters);
+/* generate_training_set (gpr.cpp:52-68): one pair per size parameter, sorted
+ * by system dimension size_n = n^3; GADI_E_PARAM on duplicate sizes. Feed
+ * size_n / alpha to gadi_gpr_fit. */
+int gadi_generate_training_set(const int64_t* size_params, int32_t count, int32_t fmt, const gadi_dichotomy* st,
+                               int32_t device, int64_t* size_n, double* alpha, int32_t* iters);
 
 #ifdef __cplusplus
 }

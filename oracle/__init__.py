@@ -57,6 +57,21 @@ class Config(C.Structure):
         return c
 
 
+class Dichotomy(C.Structure):  # gadi_dichotomy = DichotomySettings (gpr.hpp:37-44)
+    _fields_ = [("alpha_lo", C.c_double), ("alpha_hi", C.c_double), ("budget", C.c_int32),
+                ("train_xi", C.c_double), ("max_outer", C.c_int32), ("inner", InnerSpec)]
+
+    @classmethod
+    def make(cls, **kw):
+        d = cls(1e-2, 1e2, 21, 1e-8, 1500, InnerSpec(LU_DIRECT, 1e-2, 1000, 30))
+        for k, v in kw.items():
+            if k in ("method", "tol_epsilon", "max_inner_iters", "restart"):
+                setattr(d.inner, k, v)
+            else:
+                setattr(d, k, v)
+        return d
+
+
 class Report(C.Structure):
     _fields_ = [("status", C.c_int32), ("outer_iters", C.c_int32), ("final_rres", C.c_double),
                 ("inner_iter_totals", C.c_int64), ("inner_stagnations", C.c_int32),
@@ -137,6 +152,8 @@ class Oracle:
                                  C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.orc_krylov_af.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, C.c_double, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_double, _f64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.orc_alpha_bisection.argtypes = [C.c_int64, C.c_int, C.c_double, C.c_double, C.c_int,
+                                           C.POINTER(Dichotomy), _f64p, C.POINTER(C.c_int)]
         L.orc_lu_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, _f64p]
         L.orc_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, _f64p, C.POINTER(Config), _f64p, _f64p,
                                 C.c_int, C.POINTER(Report)]
@@ -241,6 +258,14 @@ class Oracle:
                              fmt if af is None else af, stop_norm, _p(x), C.byref(it), C.byref(st))
         return x, it.value, st.value
 
+    def alpha_bisection(self, n, fmt, lo, hi, budget, st):
+        """(alpha, iters), or raise on the reference's exceptions (rc -2 / -11)."""
+        a, it = C.c_double(), C.c_int()
+        rc = self.L.orc_alpha_bisection(n, fmt, lo, hi, budget, C.byref(st), C.byref(a), C.byref(it))
+        if rc != 0:
+            raise ValueError(rc)
+        return a.value, it.value
+
     def lu_solve(self, M: CSR, rhs, fmt):
         """BandLU factor + solve of M in fmt (band_lu.cpp); returns (x, status)
         with status 0, 4 (SingularInPrecision) or 3 (OverflowDetected)."""
@@ -310,6 +335,8 @@ class Reference:
         L.ref_krylov.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, C.c_double, C.c_int,
                                  C.c_int, C.c_int, C.c_double, _f64p, C.POINTER(C.c_int),
                                  C.POINTER(C.c_int)]
+        L.ref_alpha_bisection.argtypes = [C.c_int64, C.c_int, C.c_double, C.c_double, C.c_int,
+                                           C.POINTER(Dichotomy), _f64p, C.POINTER(C.c_int)]
         L.ref_lu_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, _f64p]
         L.ref_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.POINTER(Config), _f64p,
                                 _f64p, C.c_int, C.POINTER(Report)]
@@ -393,6 +420,14 @@ class Reference:
         assert self.L.ref_krylov(*self._a(M), _p(rhs), method, eps, max_inner, restart, fmt, stop_norm,
                                  _p(x), C.byref(it), C.byref(st)) == 0
         return x, it.value, st.value
+
+    def alpha_bisection(self, n, fmt, lo, hi, budget, st):
+        """(alpha, iters), or raise on the reference's exceptions (rc -2 / -11)."""
+        a, it = C.c_double(), C.c_int()
+        rc = self.L.ref_alpha_bisection(n, fmt, lo, hi, budget, C.byref(st), C.byref(a), C.byref(it))
+        if rc != 0:
+            raise ValueError(rc)
+        return a.value, it.value
 
     def lu_solve(self, M, rhs, fmt):
         rhs = np.ascontiguousarray(rhs, np.float64)

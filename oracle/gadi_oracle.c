@@ -806,6 +806,64 @@ done:
 #undef RSR
 }
 
+
+/* ------------------------------------------------------- training set (GPR)
+ * alpha_bisection (gpr.cpp:15-50) over the convdiff family (problems.cpp:8-43,
+ * r = 1/(2n+2), b = A * ones): budget log-spaced probes, each a solve with
+ * u_r = u = u_f = fmt; the fewest outer iterations among converged probes
+ * wins (strict <: ties keep the smaller alpha). Returns 0, GADI_E_PARAM or
+ * GADI_E_NO_CONVERGENT_ALPHA. */
+int orc_alpha_bisection(int64_t n, int fmt, double lo, double hi, int budget, const gadi_dichotomy* st,
+                        double* alpha, int* iters) {
+  if (!(lo > 0.0) || !(hi > lo)) return GADI_E_PARAM;
+  if (budget < 3) return GADI_E_PARAM;
+  const int64_t N = n * n * n;
+  const double r = 1.0 / (2.0 * (double)n + 2.0);
+  int64_t* rp = (int64_t*)malloc((size_t)(N + 1) * 8);
+  int64_t* ci = (int64_t*)malloc((size_t)(7 * N) * 8);
+  double* v = (double*)malloc((size_t)(7 * N) * 8);
+  double* b = (double*)malloc((size_t)N * 8);
+  double* ones = (double*)malloc((size_t)N * 8);
+  double* x = (double*)malloc((size_t)N * 8);
+  orc_convdiff_csr(n, 6.0, -1.0 - r, -1.0 + r, rp, ci, v);
+  orc_csr A = {N, rp, ci, v};
+  for (int64_t i = 0; i < N; ++i) ones[i] = 1.0;
+  orc_matvec(&A, ones, D, b);
+  const double ratio = hi / lo;
+  double best_alpha = 0.0;
+  long long best = 0x7fffffffffffffffLL;
+  for (int i = 0; i < budget; ++i) {
+    const double a = lo * pow(ratio, (double)i / (double)(budget - 1));
+    gadi_config cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.alpha = a;
+    cfg.omega = 1.0;
+    cfg.xi = st->train_xi;
+    cfg.u_r = cfg.u = cfg.u_f = fmt;
+    cfg.inner = st->inner;
+    cfg.max_outer_iters = st->max_outer;
+    cfg.divergence_factor = 1e6;
+    cfg.residual_scaling = 1;
+    gadi_report rep;
+    double h1;
+    orc_solve(&A, b, NULL, &cfg, x, &h1, 1, &rep);
+    if (rep.status == GADI_CONVERGED && (long long)rep.outer_iters < best) {
+      best = rep.outer_iters;
+      best_alpha = a;
+    }
+  }
+  free(rp);
+  free(ci);
+  free(v);
+  free(b);
+  free(ones);
+  free(x);
+  if (best_alpha == 0.0) return GADI_E_NO_CONVERGENT_ALPHA;
+  *alpha = best_alpha;
+  *iters = (int)best;
+  return 0;
+}
+
 /* ----------------------------------------------------------------------- GPR */
 typedef struct {
   double lml, sf, ell, sn;

@@ -92,6 +92,10 @@ int orc_lu_solve(const orc_csr* M, const double* rhs, int fmt, double* x);
 int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
               double* hist, int cap, gadi_report* rep);
 
+/* ---- gpr.cpp:15-50 (alpha_bisection on the convdiff family) ---- */
+int orc_alpha_bisection(int64_t n, int fmt, double lo, double hi, int budget, const gadi_dichotomy* st,
+                        double* alpha, int* iters);
+
 /* ---- gpr.cpp:72-169 ---- */
 /* mode: fixed hypers (opts->fixed_hypers) or the reference's 27-point grid.
  * params out: sigma_f2, length, sigma_n2, target_mean, lml. */

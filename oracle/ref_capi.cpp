@@ -171,6 +171,42 @@ int ref_lu_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* 
   }
 }
 
+// alpha_bisection (gpr.cpp:15-50) over the convdiff_builder family of
+// test_gpr.cpp:13-21. Returns 0, -2 ParameterError, -11 NoConvergentAlpha.
+int ref_alpha_bisection(int64_t n, int fmt, double lo, double hi, int budget, const gadi_dichotomy* st,
+                        double* alpha, int* iters) {
+  try {
+    DichotomySettings s;
+    s.alpha_lo = st->alpha_lo;
+    s.alpha_hi = st->alpha_hi;
+    s.budget = st->budget;
+    s.train_xi = st->train_xi;
+    s.max_outer = st->max_outer;
+    s.inner.method = static_cast<InnerMethod>(st->inner.method);
+    s.inner.tol_epsilon = st->inner.tol_epsilon;
+    s.inner.max_inner_iters = st->inner.max_inner_iters;
+    s.inner.restart = st->inner.restart;
+    auto builder = [](index_t sp) {
+      auto prob = build_convdiff3d({sp});
+      LinearProblem lp;
+      lp.split = hss_split(prob.A);
+      lp.A = std::move(prob.A);
+      lp.b = std::move(prob.b);
+      return lp;
+    };
+    auto [a, it] = alpha_bisection(builder, n, static_cast<Precision>(fmt), lo, hi, budget, s);
+    *alpha = a;
+    *iters = it;
+    return 0;
+  } catch (const ParameterError&) {
+    return -2;
+  } catch (const NoConvergentAlpha&) {
+    return -11;
+  } catch (...) {
+    return -1;
+  }
+}
+
 // hss_split + gadi_ir_solve (solver.cpp:250-258)
 int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
               const double* x0, const gadi_config* cfg, double* x, double* hist, int cap,

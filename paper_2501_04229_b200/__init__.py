@@ -101,8 +101,12 @@ class OverflowDetected(GadiError):  # errors.hpp: thrown by prepare (band_lu.cpp
     code = -10
 
 
+class NoConvergentAlpha(GadiError):  # errors.hpp:35-37, alpha_bisection (gpr.cpp:45-48)
+    code = -11
+
+
 _ERRS = {-1: ContractViolation, -2: ParameterError, -3: UnsupportedError, -4: FitError,
-         -9: SingularInPrecision, -10: OverflowDetected}
+         -9: SingularInPrecision, -10: OverflowDetected, -11: NoConvergentAlpha}
 
 
 # ---------------------------------------------------------------- ctypes structs
@@ -138,6 +142,11 @@ class _Problem(C.Structure):
 
 class _DevOpts(C.Structure):
     _fields_ = [("device", C.c_int32)]
+
+
+class _Dichotomy(C.Structure):
+    _fields_ = [("alpha_lo", C.c_double), ("alpha_hi", C.c_double), ("budget", C.c_int32),
+                ("train_xi", C.c_double), ("max_outer", C.c_int32), ("inner", _InnerSpec)]
 
 
 class _GprOpts(C.Structure):
@@ -203,6 +212,12 @@ def lib():
     L.gadi_cuda_solve_group.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(_Config),
                                         C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                         C.POINTER(_Report)]
+    L.gadi_dichotomy_default.argtypes = [C.POINTER(_Dichotomy)]
+    L.gadi_dichotomy_default.restype = None
+    L.gadi_alpha_bisection.argtypes = [C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                       C.POINTER(_Dichotomy), C.c_int32, _f64p, _i32p]
+    L.gadi_generate_training_set.argtypes = [_i64p, C.c_int32, C.c_int32, C.POINTER(_Dichotomy), C.c_int32,
+                                             _i64p, _f64p, _i32p]
     _lib = L
     return L
 
@@ -619,3 +634,99 @@ def gpr_fit(sizes, alphas, fixed=None, sigma_n2=None, device=0) -> GprModel:
     h = C.c_void_p()
     _check(lib().gadi_gpr_fit(_p(sizes), _p(alphas), len(sizes), C.byref(o), C.byref(h)))
     return GprModel(h)
+
+
+# ---------------------------------------------------------------- training set (gpr.hpp:17-58,85-96)
+@dataclass
+class DichotomySettings:  # gpr.hpp:37-44
+    alpha_lo: float = 1e-2
+    alpha_hi: float = 1e2
+    budget: int = 21
+    train_xi: float = 1e-8
+    max_outer: int = 1500
+    inner: InnerSolverSpec = field(default_factory=InnerSolverSpec)
+
+    def _c(self):
+        return _Dichotomy(self.alpha_lo, self.alpha_hi, self.budget, self.train_xi, self.max_outer,
+                          self.inner._c())
+
+
+@dataclass
+class TrainingPair:  # gpr.hpp:17-21
+    size_n: int = 0
+    alpha_opt: float = 0.0
+    iters_at_opt: int = 0  # 0 marks a pseudo-pair added by retraining
+
+
+@dataclass
+class TrainingSet:  # gpr.hpp:23-26
+    pairs: list = field(default_factory=list)  # sizes strictly increasing
+    generation_precision: Precision = Precision.Single
+
+
+def alpha_bisection(size_param: int, fmt: Precision, alpha_lo: float, alpha_hi: float, budget: int,
+                    settings: Optional[DichotomySettings] = None, device: int = 0):
+    """alpha_bisection (gpr.cpp:15-50) on the convdiff family (build_convdiff3d({n}), b = A*ones):
+    budget log-spaced alphas, each a device solve with u_r = u = u_f = fmt, run concurrently.
+    Returns (alpha, outer iterations); raises ParameterError / NoConvergentAlpha."""
+    st = (settings or DichotomySettings())._c()
+    a, it = C.c_double(), C.c_int32()
+    _check(lib().gadi_alpha_bisection(int(size_param), int(fmt), alpha_lo, alpha_hi, int(budget), C.byref(st),
+                                      device, C.byref(a), C.byref(it)))
+    return a.value, it.value
+
+
+def generate_training_set(size_params, fmt: Precision, settings: Optional[DichotomySettings] = None,
+                          device: int = 0) -> TrainingSet:
+    """generate_training_set (gpr.cpp:52-68): one (n^3, alpha_opt, iters) pair per size parameter."""
+    st = settings or DichotomySettings()
+    sp = np.ascontiguousarray(size_params, np.int64)
+    k = len(sp)
+    sn, al, it = np.zeros(k, np.int64), np.zeros(k), np.zeros(k, np.int32)
+    _check(lib().gadi_generate_training_set(_p(sp, _i64p), k, int(fmt), C.byref(st._c()), device, _p(sn, _i64p),
+                                            _p(al), _p(it, _i32p)))
+    return TrainingSet([TrainingPair(int(a), float(b), int(c)) for a, b, c in zip(sn, al, it)], Precision(fmt))
+
+
+def fit_training_set(ts: TrainingSet, sigma_n2=None, device=0) -> GprModel:
+    """fit(ts) (gpr.cpp:109-149) on a TrainingSet."""
+    return gpr_fit([p.size_n for p in ts.pairs], [p.alpha_opt for p in ts.pairs], sigma_n2=sigma_n2,
+                   device=device)
+
+
+def retrain_extend(model: GprModel, ts: TrainingSet, new_sizes) -> TrainingSet:
+    """retrain_extend (gpr.cpp:171-186): append (size, predicted alpha, 0) pseudo-pairs for sizes
+    not present, sorted by size."""
+    out = TrainingSet(list(ts.pairs), ts.generation_precision)
+    for s in new_sizes:
+        if any(p.size_n == s for p in out.pairs):
+            continue
+        mean, _ = model.predict([float(s)])
+        out.pairs.append(TrainingPair(int(s), float(mean[0]), 0))
+    out.pairs.sort(key=lambda p: p.size_n)
+    return out
+
+
+_PNAME = {Precision.Half: "half", Precision.Single: "single", Precision.Double: "double"}
+
+
+def write_training_csv(f, ts: TrainingSet):
+    """write_training_csv (gpr.cpp:188-196): header n,alpha,iters,precision; %.17g alphas."""
+    f.write("n,alpha,iters,precision\n")
+    for p in ts.pairs:
+        f.write(f"{p.size_n},{p.alpha_opt:.17g},{p.iters_at_opt},{_PNAME[ts.generation_precision]}\n")
+
+
+def read_training_csv(f) -> TrainingSet:
+    """read_training_csv (gpr.cpp:198-218)."""
+    lines = f.read().splitlines()
+    if not lines:
+        raise GadiError("training csv: empty stream")  # IoError
+    ts = TrainingSet()
+    for line in lines[1:]:
+        if not line:
+            continue
+        n, a, it, prec = line.split(",")[:4]
+        ts.pairs.append(TrainingPair(int(n), float(a), int(it)))
+        ts.generation_precision = {v: k for k, v in _PNAME.items()}[prec]
+    return ts

@@ -148,7 +148,7 @@ void lu_factors(gadi_handle* h, EngineBase* e) {
     e->lu[which] = lu_factor_build(h, which, e->alpha, e->u_r, &st);
     h->launches += e->lu[which]->launches;
     if (st != 0) {
-      lu_release(e->lu[which]);
+      lu_release(e->lu[which], h->stream);
       e->lu[which] = nullptr;
       throw PrepareStatus{st};
     }
@@ -167,9 +167,16 @@ void prepare(gadi_handle* h, double alpha, double omega, int ur, const gadi_inne
   auto& e = h->eng;
   const bool same = e && e->u_r == ur && e->accum == accum && std::max(1, e->spec.restart) == std::max(1, sp.restart);
   if (!(same && e->alpha == alpha && e->omega == omega)) {
-    e.reset();
-    CK(cudaStreamSynchronize(h->stream));
-    e.reset(make_engine(h, sp, alpha, omega, ur, accum));
+    if (same && e->set_alpha(alpha, omega)) {
+      for (LuFactor*& f : e->lu) {  // factors of the previous alpha
+        lu_release(f, h->stream);
+        f = nullptr;
+      }
+    } else {
+      e.reset();
+      CK(cudaStreamSynchronize(h->stream));
+      e.reset(make_engine(h, sp, alpha, omega, ur, accum));
+    }
   }
   e->spec = sp;
   if (sp.method == GADI_INNER_LU_DIRECT) lu_factors(h, e.get());

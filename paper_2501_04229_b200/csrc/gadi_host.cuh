@@ -17,7 +17,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -33,6 +35,7 @@ using namespace gadi;
 namespace gadi_host {
 
 inline thread_local std::string g_last_error;
+void set_last_error(const std::string& m);  // gadi_api.cu
 
 struct Err : std::runtime_error {
   int code;
@@ -118,10 +121,28 @@ inline Window window_for(const Geo& g, int vec, size_t tsize, int64_t max_band, 
   w.bytes = bytes;
   return w;
 }
+// The dynamic shared-memory cap is one value per kernel for the whole
+// process, while handles of different shapes launch concurrently from
+// several host threads (gadi_train.cu): the cap only ever grows, under a lock,
+// so no launch can find it lowered below its own request.
+inline std::mutex& smem_attr_mu() {
+  static std::mutex m;
+  return m;
+}
+inline std::map<std::pair<int, const void*>, size_t>& smem_attr_set() {
+  static std::map<std::pair<int, const void*>, size_t> s;
+  return s;
+}
 template <class K>
 inline void smem_attr(K kern, size_t bytes) {
-  if (bytes > 48 * 1024)
-    CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));  // the attribute is per device
+  std::lock_guard<std::mutex> g(smem_attr_mu());
+  size_t& cur = smem_attr_set()[{dev, (const void*)kern}];
+  if (bytes <= cur) return;
+  CK(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
 }
 
 inline bool aligned_for(int64_t N, int64_t n, bool stencil, int vec) {
@@ -565,7 +586,7 @@ struct LuFactor {
 };
 namespace gadi_host {
 LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* status);
-void lu_release(LuFactor* f);
+void lu_release(LuFactor* f, cudaStream_t s = nullptr);  // stream-ordered free (no device sync)
 InnerOut lu_inner_solve(LuFactor* f, const void* rhs, void* x, cudaStream_t s);
 }  // namespace gadi_host
 
@@ -573,7 +594,7 @@ InnerOut lu_inner_solve(LuFactor* f, const void* rhs, void* x, cudaStream_t s);
 struct EngineBase {
   virtual ~EngineBase() {
     for (LuFactor*& f : lu) {
-      gadi_host::lu_release(f);
+      gadi_host::lu_release(f, nullptr);
       f = nullptr;
     }
   }
@@ -593,6 +614,7 @@ struct EngineBase {
   virtual void to_inner(const double* src, void* dst) = 0;  // round_vec to u_r
   virtual void to_double(const void* src, double* dst) = 0;
   virtual void apply(int which, const void* x, void* yv) = 0;
+  virtual bool set_alpha(double a, double om) = 0;  // false: rebuild the engine
 };
 
 namespace gadi_host {
@@ -620,6 +642,7 @@ struct Engine final : EngineBase {
   St25Geo g25m;       // Arnoldi matvec: one staged input + operand ring
   St25Geo g25i;       // GMRES residual: identity operand, folded from the stages
   bool st25h = false;  // binary16 operator passes with register-resident operands (k_st25h)
+  bool st25h_geo = false;
   St25Geo g25h, g25mh;  // their geometries (3-plane operand ring)
   Window win;         // sparse operators: operand window in shared memory
 
@@ -652,6 +675,7 @@ struct Engine final : EngineBase {
         const char* e = std::getenv("GADI_ST25H");
         st25h = st25 && !(e && e[0] == '0') &&
                 make_st25h(h->n, 2, g25h, h->i0, h->i1) && make_st25h(h->n, 1, g25mh, h->i0, h->i1);
+        st25h_geo = st25h;
       }
     }
     if (h->sharded() && !SPARSE && !st25)
@@ -675,9 +699,29 @@ struct Engine final : EngineBase {
     owned.push_back(vb);
     V = vb + h->gh;
     build_ops();
+    check_st25h();
+  }
+
+  void check_st25h() {
     if constexpr (std::is_same<Op, Stencil7<C>>::value && PolSpmvp<T, C>::FASTH) {
+      st25h = st25h_geo;
       for (int k = 0; k < 7; ++k)  // k_st25h folds neutral operands at the boundary: finite coefficients only
         if (!std::isfinite((double)opH.c[k]) || !std::isfinite((double)opS.c[k])) st25h = false;
+    }
+  }
+
+  // A new (alpha, omega) on the same vectors: the stencil operators are seven
+  // coefficients, rebuilt in place (no device allocation, so no implicit
+  // device-wide synchronisation between concurrent handles).
+  bool set_alpha(double a, double om) override {
+    if constexpr (SPARSE) {
+      return false;
+    } else {
+      alpha = a;
+      omega = om;
+      build_ops();
+      check_st25h();
+      return true;
     }
   }
 

@@ -628,27 +628,29 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
   if (h->stencil()) {
     f->kl = f->ku = h->n > 1 ? h->n * h->n : 0;  // the i-1 / i+1 neighbours
   } else {  // lower/upper_bandwidth of the union pattern (sparse.cpp:142-154)
-    unsigned long long* bw = dalloc<unsigned long long>(2);
+    unsigned long long* bw = nullptr;
+    CK(cudaMallocAsync((void**)&bw, 16, h->stream));
     CK(cudaMemsetAsync(bw, 0, 16, h->stream));
     k_bandwidths<<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, h->d_urp, h->d_uci, bw);
     CKL();
     unsigned long long hb[2];
     CK(cudaMemcpyAsync(hb, bw, 16, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    cudaFree(bw);
+    cudaFreeAsync(bw, h->stream);
     f->kl = (int64_t)hb[0];
     f->ku = (int64_t)hb[1];
   }
   f->ldab = 2 * f->kl + f->ku + 1;
   const size_t es = ur == GADI_DOUBLE ? 8 : 4;
   cudaStream_t s = h->stream;
-  CK(cudaMalloc(&f->ab, (size_t)f->ldab * (size_t)f->N * es));
+  // stream-ordered allocations: concurrent handles (gadi_train.cu) never wait on each other here
+  CK(cudaMallocAsync(&f->ab, (size_t)f->ldab * (size_t)f->N * es, s));
   CK(cudaMemsetAsync(f->ab, 0, (size_t)f->ldab * (size_t)f->N * es, s));
-  CK(cudaMalloc(&f->ipiv, (size_t)f->N * sizeof(int32_t)));
-  CK(cudaMalloc(&f->xw, (size_t)f->N * es));
-  CK(cudaMalloc(&f->err, 4 * sizeof(int)));
+  CK(cudaMallocAsync((void**)&f->ipiv, (size_t)f->N * sizeof(int32_t), s));
+  CK(cudaMallocAsync(&f->xw, (size_t)f->N * es, s));
+  CK(cudaMallocAsync((void**)&f->err, 4 * sizeof(int), s));
   CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
-  CK(cudaMalloc(&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned)));
+  CK(cudaMallocAsync((void**)&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
   CK(cudaMemsetAsync(f->flags, 0, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
   f->ticket = f->flags + (f->N + 31) / 32;
   f->bad = f->err + 2;
@@ -694,10 +696,13 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
   return f.release();
 }
 
-void lu_release(LuFactor* f) {
+void lu_release(LuFactor* f, cudaStream_t s) {
   if (!f) return;
   for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err, (void*)f->flags})
-    if (p) cudaFree(p);
+    if (p) {
+      if (s) cudaFreeAsync(p, s);
+      else cudaFree(p);  // synchronous: the owner may not have synchronised its stream
+    }
   delete f;
 }
 

@@ -15,7 +15,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle import CG, CSR, DOUBLE, GMRES, HALF, SINGLE, Config, Oracle, Reference  # noqa: E402
+from oracle import CG, CSR, DOUBLE, GMRES, HALF, SINGLE, Config, Dichotomy, Oracle, Reference  # noqa: E402
 
 LU = 0  # InnerMethod::LuDirect
 
@@ -121,6 +121,19 @@ def main():
     mean, sd, params = R.gpr(sizes, alphas, q)
     out["gpr_sizes"], out["gpr_alphas"], out["gpr_q"] = sizes, alphas, q
     out["gpr_mean"], out["gpr_sd"], out["gpr_params"] = mean, sd, params
+
+    # 7. GPR training-set generation: alpha_bisection (gpr.cpp:15-50) on the
+    #    convdiff family, each probe a uniform-precision solve
+    bis = [("bs6", 6, SINGLE, 1e-2, 1e2, 17, dict(train_xi=1e-8, max_outer=1500)),          # test_gpr.cpp:53-63
+           ("bd5", 5, DOUBLE, 1e-2, 1e2, 9, dict(train_xi=1e-8, max_outer=800)),
+           ("bh4", 4, HALF, 1e-2, 1e2, 9, dict(train_xi=1e-3, max_outer=800)),
+           ("bcg5", 5, SINGLE, 1e-2, 1e2, 9, dict(method=CG, tol_epsilon=1e-6, max_inner_iters=50, max_outer=800))]
+    for tag, n, fmt, lo, hi, budget, kw in bis:
+        a, it = R.alpha_bisection(n, fmt, lo, hi, budget, Dichotomy.make(**kw))
+        out[f"bis_{tag}"] = np.array([n, fmt, lo, hi, budget, a, it], dtype=np.float64)
+    for n in (4, 5, 6):  # generate_training_set({4,5,6}, single, budget 9), test_gpr.cpp:144-160
+        a, it = R.alpha_bisection(n, SINGLE, 1e-2, 1e2, 9, Dichotomy.make(budget=9, train_xi=1e-8, max_outer=800))
+        out[f"ts_{n}"] = np.array([n ** 3, a, it], dtype=np.float64)
 
     path = os.path.join(HERE, "reference_vectors.npz")
     np.savez_compressed(path, **out)

@@ -93,3 +93,16 @@ def test_build_convdiff3d_coefficients():
     assert (S.t1, S.t2, S.t3) == (6.0, -1.0 - r, -1.0 + r)
     S2 = g.build_convdiff3d(512, beta=100.0)  # BASELINE configs[2]: r = beta h / 2
     assert S2.t2 == -1.0 - 100.0 / 1026.0
+
+
+def test_training_csv_round_trip():
+    """write_training_csv / read_training_csv (gpr.cpp:188-218): %.17g alphas survive."""
+    import io
+    import paper_2501_04229_b200 as g
+    ts = g.TrainingSet([g.TrainingPair(64, 0.1 + 1e-17 * 3, 12), g.TrainingPair(125, 1 / 3, 0)],
+                       g.Precision.Double)
+    buf = io.StringIO()
+    g.write_training_csv(buf, ts)
+    assert buf.getvalue().splitlines()[0] == "n,alpha,iters,precision"
+    back = g.read_training_csv(io.StringIO(buf.getvalue()))
+    assert back == ts
