@@ -89,7 +89,8 @@ typedef enum {
    * reports them as statuses, as run_gadi_ir does (solver.cpp:74-82). */
   GADI_E_SINGULAR = -9,    /* SingularInPrecision */
   GADI_E_OVERFLOW = -10,   /* OverflowDetected    */
-  GADI_E_NO_CONVERGENT_ALPHA = -11 /* NoConvergentAlpha (errors.hpp), alpha_bisection */
+  GADI_E_NO_CONVERGENT_ALPHA = -11, /* NoConvergentAlpha (errors.hpp), alpha_bisection */
+  GADI_E_IO = -12          /* IoError (errors.hpp:43-45), MatrixMarket files */
 } gadi_error;
 
 /* InnerSolverSpec, inner_solver.hpp:20-25; defaults from gadi_config_default. */
@@ -318,6 +319,22 @@ int gadi_alpha_bisection(int64_t size_param, int32_t fmt, double alpha_lo, doubl
  * size_n / alpha to gadi_gpr_fit. */
 int gadi_generate_training_set(const int64_t* size_params, int32_t count, int32_t fmt, const gadi_dichotomy* st,
                                int32_t device, int64_t* size_n, double* alpha, int32_t* iters);
+
+/* ---- MatrixMarket ingest (sparse.hpp:75-76; matrix_market.cpp:22-86) ----
+ * gadi_mm_read = read_matrix_market_file: coordinate real/integer,
+ * general/symmetric/skew-symmetric, 1-based, duplicates summed; the banner is
+ * parsed on the host, the from_triplets assembly (sort, duplicate sums,
+ * row_ptr) runs on `device`. The CSR stays owned by the library until
+ * gadi_csr_destroy; pass its arrays to gadi_cuda_create (GADI_PROBLEM_CSR).
+ * Errors: GADI_E_IO (IoError), GADI_E_CONTRACT (triplet out of range). */
+typedef struct gadi_csr gadi_csr;
+int gadi_mm_read(const char* path, int32_t device, gadi_csr** out);
+int gadi_csr_view(const gadi_csr* m, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, const int64_t** row_ptr,
+                  const int64_t** col_idx, const double** values);
+int gadi_csr_destroy(gadi_csr* m);
+/* write_matrix_market_file: "symmetric" (lower triangle) when A == A^T exactly */
+int gadi_mm_write(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                  const double* values);
 
 #ifdef __cplusplus
 }

@@ -337,6 +337,8 @@ class Reference:
                                  C.POINTER(C.c_int)]
         L.ref_alpha_bisection.argtypes = [C.c_int64, C.c_int, C.c_double, C.c_double, C.c_int,
                                            C.POINTER(Dichotomy), _f64p, C.POINTER(C.c_int)]
+        L.ref_mm_read.restype = C.c_int64
+        L.ref_mm_read.argtypes = [C.c_char_p, _i64p, _i64p, _i64p, _i64p, _f64p]
         L.ref_lu_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, _f64p]
         L.ref_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.POINTER(Config), _f64p,
                                 _f64p, C.c_int, C.POINTER(Report)]
@@ -428,6 +430,16 @@ class Reference:
         if rc != 0:
             raise ValueError(rc)
         return a.value, it.value
+
+    def mm_read(self, path):
+        """read_matrix_market_file: (n_rows, n_cols, rp, ci, v), or the error code (int)."""
+        nr, nc = C.c_int64(), C.c_int64()
+        nnz = self.L.ref_mm_read(path.encode(), C.byref(nr), C.byref(nc), None, None, None)
+        if nnz < 0:
+            return int(nnz)
+        rp, ci, v = np.zeros(nr.value + 1, np.int64), np.zeros(nnz, np.int64), np.zeros(nnz)
+        self.L.ref_mm_read(path.encode(), C.byref(nr), C.byref(nc), _p(rp, _i64p), _p(ci, _i64p), _p(v))
+        return nr.value, nc.value, rp, ci, v
 
     def lu_solve(self, M, rhs, fmt):
         rhs = np.ascontiguousarray(rhs, np.float64)

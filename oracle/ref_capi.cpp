@@ -207,6 +207,28 @@ int ref_alpha_bisection(int64_t n, int fmt, double lo, double hi, int budget, co
   }
 }
 
+// read_matrix_market_file (matrix_market.cpp:22-62). Two calls: with rp ==
+// nullptr returns nnz (or -12 IoError / -1 ContractViolation); then fills.
+int64_t ref_mm_read(const char* path, int64_t* n_rows, int64_t* n_cols, int64_t* rp, int64_t* ci, double* v) {
+  try {
+    SparseMatrix A = read_matrix_market_file(path);
+    *n_rows = A.n_rows();
+    *n_cols = A.n_cols();
+    if (rp) {
+      std::memcpy(rp, A.row_ptr().data(), A.row_ptr().size() * 8);
+      std::memcpy(ci, A.col_idx().data(), A.col_idx().size() * 8);
+      std::memcpy(v, A.values().data(), A.values().size() * 8);
+    }
+    return A.nnz();
+  } catch (const IoError&) {
+    return -12;
+  } catch (const ContractViolation&) {
+    return -1;
+  } catch (...) {
+    return -5;
+  }
+}
+
 // hss_split + gadi_ir_solve (solver.cpp:250-258)
 int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
               const double* x0, const gadi_config* cfg, double* x, double* hist, int cap,

@@ -105,8 +105,12 @@ class NoConvergentAlpha(GadiError):  # errors.hpp:35-37, alpha_bisection (gpr.cp
     code = -11
 
 
+class IoError(GadiError):  # errors.hpp:43-45 (MatrixMarket files)
+    code = -12
+
+
 _ERRS = {-1: ContractViolation, -2: ParameterError, -3: UnsupportedError, -4: FitError,
-         -9: SingularInPrecision, -10: OverflowDetected, -11: NoConvergentAlpha}
+         -9: SingularInPrecision, -10: OverflowDetected, -11: NoConvergentAlpha, -12: IoError}
 
 
 # ---------------------------------------------------------------- ctypes structs
@@ -218,6 +222,11 @@ def lib():
                                        C.POINTER(_Dichotomy), C.c_int32, _f64p, _i32p]
     L.gadi_generate_training_set.argtypes = [_i64p, C.c_int32, C.c_int32, C.POINTER(_Dichotomy), C.c_int32,
                                              _i64p, _f64p, _i32p]
+    L.gadi_mm_read.argtypes = [C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]
+    L.gadi_csr_view.argtypes = [C.c_void_p, _i64p, _i64p, _i64p, C.POINTER(_i64p), C.POINTER(_i64p),
+                                C.POINTER(_f64p)]
+    L.gadi_csr_destroy.argtypes = [C.c_void_p]
+    L.gadi_mm_write.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _i64p, _i64p, _f64p]
     _lib = L
     return L
 
@@ -730,3 +739,28 @@ def read_training_csv(f) -> TrainingSet:
         ts.pairs.append(TrainingPair(int(n), float(a), int(it)))
         ts.generation_precision = {v: k for k, v in _PNAME.items()}[prec]
     return ts
+
+
+# ---------------------------------------------------------------- MatrixMarket (sparse.hpp:75-76)
+def read_matrix_market_file(path: str, device: int = 0) -> SparseMatrix:
+    """read_matrix_market_file (matrix_market.cpp:22-62): host parse, from_triplets assembly on the
+    device. Raises IoError / ContractViolation like the reference."""
+    L = lib()
+    h = C.c_void_p()
+    _check(L.gadi_mm_read(os.fsencode(path), device, C.byref(h)))
+    try:
+        nr, nc, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+        rp, ci, v = _i64p(), _i64p(), _f64p()
+        _check(L.gadi_csr_view(h, C.byref(nr), C.byref(nc), C.byref(nnz), C.byref(rp), C.byref(ci), C.byref(v)))
+        k = nnz.value
+        arr = lambda ptr, n, dt: np.ctypeslib.as_array(ptr, (n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+        return SparseMatrix(nr.value, nc.value, arr(rp, nr.value + 1, np.int64), arr(ci, k, np.int64),
+                            arr(v, k, np.float64))
+    finally:
+        L.gadi_csr_destroy(h)
+
+
+def write_matrix_market_file(path: str, A: SparseMatrix):
+    """write_matrix_market_file (matrix_market.cpp:64-86)."""
+    _check(lib().gadi_mm_write(os.fsencode(path), A.n_rows, A.n_cols, _p(A.row_ptr, _i64p), _p(A.col_idx, _i64p),
+                               _p(A.values)))
