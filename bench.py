@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """GADI-IR time-to-1e-10 benchmark (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3|c2|c4|c1|c5]
 
 A step is one complete GADI-IR solve of the workload's system to relative
 residual 1e-10 (xi = 1e-20): FP64 outer residual/update, inner CG on H and
@@ -11,6 +11,9 @@ GMRES on S on the device. Workloads (BASELINE.json configs):
      outer, alpha=0.2, omega=1, CG/GMRES(30) with eps=1e-12, max_inner=5
      (the fastest time-to-solution of an alpha x max_inner sweep on B200).
   c2: n=256 (N = 16,777,216), beta=10, FP32 inner, alpha=0.05, max_inner=20.
+  c1: the reference's own CPU case: build_convdiff3d(32) (beta=1), FP16 inner
+     through its default inner method (BandLU, lu_direct), alpha=0.1; the
+     reference arm times its whole solve (measured, not projected).
 x_true ~ U[-1,1) from the splitmix64 counter RNG (seed 1), b = A x_true in
 binary64 on the device (the same generator the oracle uses).
 
@@ -37,6 +40,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
+    # BASELINE configs[0]: the reference's own build_convdiff3d(32) (beta = 1), x_true ~ U[0,1) seed 0,
+    # FP16 inner through the reference's default inner method (BandLU, lu_direct), FP64 outer
+    "c1": dict(n=32, beta=1.0, u_r=0, accum=0, method=0, alpha=0.1, eps=1e-2, max_inner=1000, restart=30,
+               seed=0, lo=0.0, hi=1.0, s_r=4, name="convdiff3d n=32 beta=1 fp16 lu_direct inner (BandLU)"),
     "c3": dict(n=512, beta=100.0, u_r=0, accum=1, alpha=0.2, eps=1e-12, max_inner=5, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=2, name="convdiff3d n=512 beta=100 fp16-storage/fp32-accum inner"),
     "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.05, eps=1e-12, max_inner=20, restart=30,
@@ -49,7 +56,7 @@ WORKLOADS = {
 }
 # outer iterations the device solve needs for each workload (measured on B200,
 # profiles/); used only to project the CPU reference's time-to-solution
-OUTER_ITERS = {"c3": 796, "c2": 366, "c4": 28}
+OUTER_ITERS = {"c3": 796, "c2": 366, "c4": 28, "c1": 0}
 
 
 def load_peaks():
@@ -108,7 +115,28 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def c1_cpu_full(wl):
+    """C1 fits the reference: time its whole solve (oracle/_ref, one core) on the
+    same system, config and right-hand side -- measured, not projected."""
+    from oracle import Config, Oracle, Reference
+    o = Oracle()
+    use_ref = Reference.available()
+    R = Reference() if use_ref else o
+    n = wl["n"]
+    A = o.convdiff(n, 6.0, -1.0 - 1.0 / (2 * n + 2), -1.0 + 1.0 / (2 * n + 2))
+    _, b = o.make_rhs(A, wl["seed"], wl["lo"], wl["hi"])
+    cfg = Config.make(alpha=wl["alpha"], xi=1e-20, u_r=wl["u_r"], method=wl["method"])
+    t = time.perf_counter()
+    _, rep, _ = R.solve(A, b, cfg)
+    dt = time.perf_counter() - t
+    return {"value": dt, "unit": "s", "cores": 1, "kind": "reference" if use_ref else "port",
+            "sample": (f"the whole C1 solve (build_convdiff3d(32), fp16 BandLU inner, alpha={wl['alpha']}): "
+                       f"status {rep.status}, {rep.outer_iters} outer, measured (not projected)")}
+
+
 def cpu_reference_sample(wl, threads_note=True):
+    if wl_key(wl) == "c1":
+        return c1_cpu_full(wl)
     """Time the reference's own CPU implementation (oracle/_ref, built from the
     reference sources; else the oracle restatement) on a bounded sample: one
     GADI-IR outer step (CG on H + GMRES on S + residuals, same inner budget and
@@ -256,7 +284,9 @@ def main():
     metric = "GADI-IR time-to-1e-10 residual"
     band = wl.get("kind") == "band"
     Nw = wl["N"] if band else wl["n"] ** 3
-    cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": 1.0, "inner": "cg(H)/gmres(S)",
+    lu = wl.get("method") == 0
+    cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": 1.0,
+                "inner": "lu_direct(H, S)" if lu else "cg(H)/gmres(S)",
                 "max_inner": wl["max_inner"], "tol_epsilon": wl["eps"], "xi": 1e-20,
                 "l2": "inputs larger than L2 (x, b: 8N bytes each)",
                 "parallelism": "single"}
@@ -311,11 +341,15 @@ def main():
     b_h = b.cpu().pin_memory()
     x_h = torch.empty(N, dtype=torch.float64).pin_memory()
     cfg = g.GadiConfig(alpha=wl["alpha"], xi=1e-20, u_r=g.Precision(wl["u_r"]), accum=g.Accum(wl["accum"]),
-                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, wl["eps"], wl["max_inner"], wl["restart"]))
+                       inner=g.InnerSolverSpec(g.InnerMethod(wl.get("method", 1)), wl["eps"], wl["max_inner"],
+                                               wl["restart"]))
     b_np = b_h.numpy()
     x_np = x_h.numpy()
 
     def step():
+        # every timed solve re-runs prepare (operators, and the factorizations for lu_direct),
+        # as the reference's gadi_ir_solve does on each call (solver.cpp:75, 199-208)
+        sysx.reset()
         return sysx.solve_into(b_np, x_np, cfg)
 
     for _ in range(args.warmup):
@@ -355,6 +389,14 @@ def main():
     if band:
         bytes_it += sysx.nnz()[1] * (wl["s_r"] + 4) + 4 * (N + 1)
     cg_gbs = bytes_it * h_it / (h_ms / 1e3) / 1e9 if h_ms > 0 else None
+    roof_kernel = ("inner CG iteration (p-update, SELL spmv + p.q, axpys + dots)" if band
+                   else "inner CG iteration (spmv+p-update, axpys+dots)")
+    if lu:  # one BandLU solve reads the factor band once: N (kl + (kl+ku) + 1) binary32 values (n^2 bands)
+        kl = wl["n"] ** 2
+        bytes_it = N * (kl + 2 * kl + 1) * 4
+        n_solves = sum(r.outer_iters for r in reps)
+        cg_gbs = bytes_it * n_solves / (h_ms / 1e3) / 1e9 if h_ms > 0 else None
+        roof_kernel = "BandLU solve of H (forward + back sweeps over the factor band, k_lu_pipe)"
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
     if os.path.exists(tp):
@@ -364,12 +406,12 @@ def main():
         "metric": metric, "value": solve_s, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": solve_s * 1e3, "higher_is_better": False,
         "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None, "dtype": "f64 outer / " + ("f16 storage, f32 arithmetic" if wl["u_r"] == 0 else "f32")
+        "vs_baseline": None, "dtype": "f64 outer / " + ("f16 (every op rounded to binary16)" if lu else
+                                                       "f16 storage, f32 arithmetic" if wl["u_r"] == 0 else "f32")
         + " inner", "data": "synthetic (seeded splitmix64 x_true, b = A x_true)", "config": cfg_json,
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(reps[0].h2d_bytes),
                 "d2h_bytes_per_step": int(reps[0].d2h_bytes)},
-        "roofline": {"bound": "hbm", "kernel": ("inner CG iteration (p-update, SELL spmv + p.q, axpys + dots)"
-                                                if band else "inner CG iteration (spmv+p-update, axpys+dots)"),
+        "roofline": {"bound": "hbm", "kernel": roof_kernel,
                      "achieved": cg_gbs, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (cg_gbs / peak) if cg_gbs else None, "traffic": traffic if world == 1 else None,
                      "algorithmic_bytes_per_iter": bytes_it, "per": "GPU (rank 0's shard)" if sharded else "GPU"},

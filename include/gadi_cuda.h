@@ -197,6 +197,11 @@ int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_o
  * and returns GADI_E_SINGULAR / GADI_E_OVERFLOW where the reference throws. */
 int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r,
                       const gadi_inner_spec* spec, int32_t accum);
+/* Drop the prepared inner engine (operators, work vectors, LU factors): the
+ * next solve re-runs prepare, exactly as a fresh gadi_ir_solve /
+ * CsrGadiSystem does (solver.cpp:75). A handle otherwise keeps the prepared
+ * state across solves with the same (alpha, omega, u_r, inner spec). */
+int gadi_cuda_reset(gadi_handle* h);
 int gadi_cuda_set_inner_stop_norm(gadi_handle* h, double stop_norm);
 /* solve_H: CG on H (inner_solver.cpp:47-83); solve_S: GMRES(restart) on S
  * (inner_solver.cpp:85-194; a CG request degrades to GMRES, solver.cpp:217-221).

@@ -189,6 +189,7 @@ def lib():
     L.gadi_cuda_prepare.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int32, C.POINTER(_InnerSpec),
                                     C.c_int32]
     L.gadi_cuda_set_inner_stop_norm.argtypes = [C.c_void_p, C.c_double]
+    L.gadi_cuda_reset.argtypes = [C.c_void_p]
     for f in ("gadi_cuda_solve_H", "gadi_cuda_solve_S"):
         getattr(L, f).argtypes = [C.c_void_p, _f64p, _f64p, _i32p, _i32p]
     L.gadi_cuda_solve.argtypes = [C.c_void_p, C.POINTER(_Config), _f64p, _f64p, _f64p, C.POINTER(_Report)]
@@ -444,6 +445,10 @@ class CudaGadiSystem:
 
     def prepare(self, alpha, omega, u_r: Precision, spec: InnerSolverSpec, accum: Accum = Accum.Native):
         _check(lib().gadi_cuda_prepare(self._h, alpha, omega, int(u_r), C.byref(spec._c()), int(accum)))
+
+    def reset(self):
+        """Drop the prepared inner state: the next solve re-runs prepare (factorizations included)."""
+        _check(lib().gadi_cuda_reset(self._h))
 
     def set_inner_stop_norm(self, s):
         _check(lib().gadi_cuda_set_inner_stop_norm(self._h, s))

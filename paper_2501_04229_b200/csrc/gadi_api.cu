@@ -682,6 +682,15 @@ int gadi_cuda_prepare(gadi_handle* h, double alpha, double omega, int32_t u_r, c
   API_END
 }
 
+int gadi_cuda_reset(gadi_handle* h) {
+  API_BEGIN
+  if (!h) throw Err(GADI_E_CONTRACT, "reset: null handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  h->eng.reset();
+  API_END
+}
+
 int gadi_cuda_set_inner_stop_norm(gadi_handle* h, double stop_norm) {
   if (!h) return GADI_E_CONTRACT;
   h->stop_norm = stop_norm;
