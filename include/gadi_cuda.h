@@ -341,6 +341,23 @@ int gadi_csr_destroy(gadi_csr* m);
 int gadi_mm_write(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
                   const double* values);
 
+/* ---- Sylvester GADI-AB (problems.hpp:44-89; sylvester.cpp): the
+ * reference's second GadiSystem, A X + X B = G (X m x n, column-major vec),
+ * solved by run_gadi_ir with splitting M = I (x) A, N = B^T (x) I: prepare
+ * factors alpha I + A and alpha I + B^T (BandLU in u_r, the inner spec is
+ * ignored as in the reference), solve_H runs the column solves, solve_S the
+ * row solves, one device thread per column / row. ---- */
+typedef struct gadi_sylv gadi_sylv;
+/* A (m x m) and B (n x n) in the reference's CSR layout, G (m x n) column-major;
+ * host pointers, copied. gadi_ab_solve passes G = -C (sylvester.cpp:125-127). */
+int gadi_sylv_create(int64_t m, const int64_t* a_rp, const int64_t* a_ci, const double* a_v, int64_t n,
+                     const int64_t* b_rp, const int64_t* b_ci, const double* b_v, const double* G, int32_t device,
+                     gadi_sylv** out);
+/* run_gadi_ir(SylvesterOperator, cfg, x0); x0 NULL: zeros (ones if ones_start). */
+int gadi_sylv_solve(gadi_sylv* s, const gadi_config* cfg, const double* x0, double* x_out, gadi_report* rep);
+int gadi_sylv_history(const gadi_sylv* s, double* out, int32_t cap);
+int gadi_sylv_destroy(gadi_sylv* s);
+
 #ifdef __cplusplus
 }
 #endif

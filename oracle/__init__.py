@@ -339,6 +339,8 @@ class Reference:
                                            C.POINTER(Dichotomy), _f64p, C.POINTER(C.c_int)]
         L.ref_mm_read.restype = C.c_int64
         L.ref_mm_read.argtypes = [C.c_char_p, _i64p, _i64p, _i64p, _i64p, _f64p]
+        L.ref_sylvester_solve.argtypes = [C.c_int64, C.c_double, C.POINTER(Config), _f64p, _f64p, C.c_int,
+                                           C.POINTER(Report)]
         L.ref_lu_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_int, _f64p]
         L.ref_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, _f64p, C.POINTER(Config), _f64p,
                                 _f64p, C.c_int, C.POINTER(Report)]
@@ -440,6 +442,14 @@ class Reference:
         rp, ci, v = np.zeros(nr.value + 1, np.int64), np.zeros(nnz, np.int64), np.zeros(nnz)
         self.L.ref_mm_read(path.encode(), C.byref(nr), C.byref(nc), _p(rp, _i64p), _p(ci, _i64p), _p(v))
         return nr.value, nc.value, rp, ci, v
+
+    def sylvester_solve(self, n, r, cfg, cap=100000):
+        """gadi_ab_solve(build_sylvester({n, r}), cfg): (X column-major vec, report, history)."""
+        X = np.zeros(n * n)
+        hist = np.zeros(cap)
+        rep = Report()
+        assert self.L.ref_sylvester_solve(n, r, C.byref(cfg), _p(X), _p(hist), cap, C.byref(rep)) == 0
+        return X, rep, hist[: min(rep.history_len, cap)].copy()
 
     def lu_solve(self, M, rhs, fmt):
         rhs = np.ascontiguousarray(rhs, np.float64)

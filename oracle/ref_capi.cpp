@@ -229,6 +229,33 @@ int64_t ref_mm_read(const char* path, int64_t* n_rows, int64_t* n_cols, int64_t*
   }
 }
 
+// gadi_ab_solve(build_sylvester({n, r}), cfg) (sylvester.cpp:122-133,
+// problems.cpp:45-66): X (n x n, column-major), history, report.
+int ref_sylvester_solve(int64_t n, double r, const gadi_config* cfg, double* X, double* hist, int cap,
+                        gadi_report* rep) {
+  try {
+    SylvesterSpec sp;
+    sp.n = n;
+    sp.r = r;
+    auto prob = build_sylvester(sp);
+    auto res = gadi_ab_solve(prob, to_cfg(cfg));
+    for (index_t j = 0; j < n; ++j)
+      for (index_t i = 0; i < n; ++i) X[j * n + i] = res.X(i, j);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = static_cast<int>(res.report.status);
+    rep->outer_iters = res.report.outer_iters;
+    rep->final_rres = res.report.final_rres;
+    rep->inner_iter_totals = res.report.inner_iter_totals;
+    rep->inner_stagnations = res.report.inner_stagnations;
+    const auto& h = res.report.rel_residual_history;
+    rep->history_len = static_cast<int>(h.size());
+    for (size_t i = 0; i < h.size() && static_cast<int>(i) < cap; ++i) hist[i] = h[i];
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
 // hss_split + gadi_ir_solve (solver.cpp:250-258)
 int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
               const double* x0, const gadi_config* cfg, double* x, double* hist, int cap,

@@ -228,6 +228,11 @@ def lib():
                                 C.POINTER(_f64p)]
     L.gadi_csr_destroy.argtypes = [C.c_void_p]
     L.gadi_mm_write.argtypes = [C.c_char_p, C.c_int64, C.c_int64, _i64p, _i64p, _f64p]
+    L.gadi_sylv_create.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_int64, _i64p, _i64p, _f64p, _f64p,
+                                   C.c_int32, C.POINTER(C.c_void_p)]
+    L.gadi_sylv_solve.argtypes = [C.c_void_p, C.POINTER(_Config), _f64p, _f64p, C.POINTER(_Report)]
+    L.gadi_sylv_history.argtypes = [C.c_void_p, _f64p, C.c_int32]
+    L.gadi_sylv_destroy.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -769,3 +774,75 @@ def write_matrix_market_file(path: str, A: SparseMatrix):
     """write_matrix_market_file (matrix_market.cpp:64-86)."""
     _check(lib().gadi_mm_write(os.fsencode(path), A.n_rows, A.n_cols, _p(A.row_ptr, _i64p), _p(A.col_idx, _i64p),
                                _p(A.values)))
+
+
+# ---------------------------------------------------------------- Sylvester GADI-AB (problems.hpp:34-89)
+def tridiag(n: int, sub: float, diag: float, sup: float) -> SparseMatrix:
+    """SparseMatrix::tridiag (sparse.cpp:76-85); zero bands are not stored."""
+    rp, ci, v = [0], [], []
+    for i in range(n):
+        for c, x in ((i - 1, sub), (i, diag), (i + 1, sup)):
+            if 0 <= c < n and x != 0.0:
+                ci.append(c)
+                v.append(x)
+        rp.append(len(ci))
+    return SparseMatrix(n, n, rp, ci, v)
+
+
+@dataclass
+class SylvesterProblem:  # problems.hpp:39-44
+    A: SparseMatrix
+    B: SparseMatrix
+    C_rhs: np.ndarray    # A X + X B + C = 0
+    X_exact: np.ndarray
+
+
+def build_sylvester(n: int, r: float = 1.0) -> SylvesterProblem:
+    """build_sylvester (problems.cpp:45-66): A = B = Tridiag(-1-r, 2+shift, -1+r),
+    shift = 100/(n+1)^2, X = ones, C = -(A X + X B) from row/column sums."""
+    if n < 2:
+        raise ContractViolation("sylvester: n >= 2 required")
+    if not r > 0.0:
+        raise ContractViolation("sylvester: r > 0 required")
+    sh = 100.0 / ((float(n) + 1.0) * (float(n) + 1.0))
+    A = tridiag(n, -1.0 - r, 2.0 + sh, -1.0 + r)
+    row, col = np.zeros(n), np.zeros(n)
+    for i in range(n):
+        for k in range(A.row_ptr[i], A.row_ptr[i + 1]):
+            row[i] += A.values[k]
+            col[A.col_idx[k]] += A.values[k]
+    C_rhs = -(row[:, None] + col[None, :])
+    return SylvesterProblem(A, A, C_rhs, np.ones((n, n)))
+
+
+@dataclass
+class SylvesterResult:  # problems.hpp:86-89
+    X: np.ndarray
+    report: SolveReport
+
+
+def gadi_ab_solve(prob: SylvesterProblem, cfg: GadiConfig, device: int = 0) -> SylvesterResult:
+    """gadi_ab_solve (sylvester.cpp:122-133): run_gadi_ir over the SylvesterOperator on the device
+    (G = -C, x0 = zeros or ones)."""
+    L = lib()
+    m, n = prob.A.n_rows, prob.B.n_rows
+    G = np.ascontiguousarray((-np.asarray(prob.C_rhs, np.float64)).T).reshape(-1)  # column-major vec
+    h = C.c_void_p()
+    A, B = prob.A, prob.B
+    _check(L.gadi_sylv_create(m, _p(A.row_ptr, _i64p), _p(A.col_idx, _i64p), _p(A.values), n,
+                              _p(B.row_ptr, _i64p), _p(B.col_idx, _i64p), _p(B.values), _p(G), device,
+                              C.byref(h)))
+    try:
+        x = np.empty(m * n)
+        rep = _Report()
+        c = cfg._c()
+        _check(L.gadi_sylv_solve(h, C.byref(c), None, _p(x), C.byref(rep)))
+        hist = np.empty(max(rep.history_len, 1))
+        L.gadi_sylv_history(h, _p(hist), len(hist))
+        r = SolveReport(status=SolveStatus(rep.status), outer_iters=rep.outer_iters,
+                        rel_residual_history=hist[:rep.history_len].copy(), final_rres=rep.final_rres,
+                        inner_iter_totals=rep.inner_iter_totals, inner_stagnations=rep.inner_stagnations,
+                        solve_ms=rep.solve_ms, launches=rep.launches)
+        return SylvesterResult(x.reshape(n, m).T.copy(), r)
+    finally:
+        L.gadi_sylv_destroy(h)

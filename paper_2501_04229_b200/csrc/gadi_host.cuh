@@ -588,6 +588,9 @@ namespace gadi_host {
 LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* status);
 void lu_release(LuFactor* f, cudaStream_t s = nullptr);  // stream-ordered free (no device sync)
 InnerOut lu_inner_solve(LuFactor* f, const void* rhs, void* x, cudaStream_t s);
+LuFactor* lu_factor_host_csr(int device, cudaStream_t s, int64_t N, const int64_t* rp, const int64_t* ci,
+                             const double* v, double alpha, int ur, int* status);
+bool lu_solve_many(LuFactor* f, double* X, int64_t es, int64_t rs, int64_t nrhs, cudaStream_t s);
 }  // namespace gadi_host
 
 // The inner solvers for one (operator, storage, arithmetic) choice.

@@ -614,6 +614,45 @@ void solve_impl(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
   f->launches += 4;
 }
 
+// Many right-hand sides against one (small-band) factor, one thread each:
+// the reference's solve_impl (band_lu.cpp:137-172) verbatim, swaps included.
+// Element t of right-hand side r is X[r*rs + t*es] (binary64 slots holding
+// u_r values, like the reference's Vector); bad = 1 on a non-finite result.
+template <int P>
+__global__ void k_lu_solve_many(const typename LuPol<P>::S* __restrict__ ab, int64_t N, int64_t kl, int64_t ku,
+                                int64_t ldab, const int32_t* __restrict__ ipiv, double* __restrict__ X, int64_t es,
+                                int64_t rs, int64_t nrhs, int* bad) {
+  using Pol = LuPol<P>;
+  using S = typename Pol::S;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrhs) return;
+  double* x = X + r * rs;
+  const int64_t ldoff = kl + ku;
+  for (int64_t j = 0; j < N; ++j) {
+    const int64_t p = ipiv[j];
+    if (p != j) {
+      const double t = x[j * es];
+      x[j * es] = x[p * es];
+      x[p * es] = t;
+    }
+    const S xj = (S)x[j * es];
+    if (xj == S(0)) continue;
+    const int64_t ilast = lmin(N - 1, j + kl);
+    for (int64_t i = j + 1; i <= ilast; ++i)
+      x[i * es] = (double)Pol::sub((S)x[i * es], Pol::mul(ab[j * ldab + ldoff + i - j], xj));
+  }
+  bool fin = true;
+  for (int64_t j = N - 1; j >= 0; --j) {
+    const S xj = Pol::div((S)x[j * es], ab[j * ldab + ldoff]);
+    x[j * es] = (double)xj;
+    fin = fin && isfinite((double)xj);
+    if (xj != S(0))
+      for (int64_t i = lmax(0, j - ldoff); i < j; ++i)
+        x[i * es] = (double)Pol::sub((S)x[i * es], Pol::mul(ab[j * ldab + ldoff + i - j], xj));
+  }
+  if (!fin) *bad = 1;
+}
+
 }  // namespace
 
 // Builds and factors the band image of H (which = 1) or S (which = 2) of the
@@ -694,6 +733,83 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
             : ur == GADI_SINGLE ? factor_impl<GADI_SINGLE>(f.get(), s)
                                 : factor_impl<GADI_HALF>(f.get(), s);
   return f.release();
+}
+
+// BandLU of shift_diagonal(M, alpha) (sparse.cpp:180-183: the diagonal is
+// 1.0*M_ii + alpha, or alpha where M has none) for a small host CSR M, in u_r
+// (the Sylvester coefficients' factorizations, sylvester.cpp:66-73).
+LuFactor* lu_factor_host_csr(int device, cudaStream_t s, int64_t N, const int64_t* rp, const int64_t* ci,
+                             const double* v, double alpha, int ur, int* status) {
+  std::unique_ptr<LuFactor> f(new LuFactor);
+  f->device = device;
+  f->prec = ur;
+  f->N = N;
+  int64_t kl = 0, ku = 0;
+  for (int64_t i = 0; i < N; ++i) {  // bandwidths of the shifted pattern (it has every diagonal)
+    const int64_t c0 = rp[i] < rp[i + 1] ? std::min<int64_t>(ci[rp[i]], i) : i;
+    const int64_t c1 = rp[i] < rp[i + 1] ? std::max<int64_t>(ci[rp[i + 1] - 1], i) : i;
+    kl = std::max(kl, i - c0);
+    ku = std::max(ku, c1 - i);
+  }
+  f->kl = kl;
+  f->ku = ku;
+  f->ldab = 2 * kl + ku + 1;
+  const int64_t ldoff = kl + ku;
+  std::vector<double> band((size_t)(f->ldab * N), 0.0);
+  for (int64_t i = 0; i < N; ++i) {
+    bool diag = false;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      double x = 1.0 * v[k];
+      if (ci[k] == i) {
+        x = 1.0 * v[k] + alpha;
+        diag = true;
+      }
+      band[(size_t)(ci[k] * f->ldab + ldoff + i - ci[k])] = hround(x, ur);
+    }
+    if (!diag) band[(size_t)(i * f->ldab + ldoff)] = hround(alpha, ur);
+  }
+  const size_t es = ur == GADI_DOUBLE ? 8 : 4;
+  CK(cudaMallocAsync(&f->ab, band.size() * es, s));
+  if (ur == GADI_DOUBLE) {
+    CK(cudaMemcpyAsync(f->ab, band.data(), band.size() * 8, cudaMemcpyHostToDevice, s));
+  } else {
+    std::vector<float> bf(band.begin(), band.end());
+    CK(cudaMemcpyAsync(f->ab, bf.data(), bf.size() * 4, cudaMemcpyHostToDevice, s));
+  }
+  CK(cudaMallocAsync((void**)&f->ipiv, (size_t)N * sizeof(int32_t), s));
+  CK(cudaMallocAsync(&f->xw, (size_t)N * es, s));
+  CK(cudaMallocAsync((void**)&f->err, 4 * sizeof(int), s));
+  CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
+  CK(cudaMallocAsync((void**)&f->flags, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
+  CK(cudaMemsetAsync(f->flags, 0, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
+  f->ticket = f->flags + (N + 31) / 32;
+  f->bad = f->err + 2;
+  *status = ur == GADI_DOUBLE ? factor_impl<GADI_DOUBLE>(f.get(), s)
+            : ur == GADI_SINGLE ? factor_impl<GADI_SINGLE>(f.get(), s)
+                                : factor_impl<GADI_HALF>(f.get(), s);
+  return f.release();
+}
+
+// x_r = F \ x_r for nrhs right-hand sides in place (binary64 slots of u_r
+// values); element t of r at X[r*rs + t*es]. Returns true if all finite.
+bool lu_solve_many(LuFactor* f, double* X, int64_t es, int64_t rs, int64_t nrhs, cudaStream_t s) {
+  CK(cudaMemsetAsync(f->bad, 0, sizeof(int), s));
+  const unsigned g = (unsigned)((nrhs + 127) / 128);
+  if (f->prec == GADI_DOUBLE)
+    k_lu_solve_many<GADI_DOUBLE><<<g, 128, 0, s>>>((const double*)f->ab, f->N, f->kl, f->ku, f->ldab, f->ipiv, X, es,
+                                                  rs, nrhs, f->bad);
+  else if (f->prec == GADI_SINGLE)
+    k_lu_solve_many<GADI_SINGLE><<<g, 128, 0, s>>>((const float*)f->ab, f->N, f->kl, f->ku, f->ldab, f->ipiv, X, es,
+                                                  rs, nrhs, f->bad);
+  else
+    k_lu_solve_many<GADI_HALF><<<g, 128, 0, s>>>((const float*)f->ab, f->N, f->kl, f->ku, f->ldab, f->ipiv, X, es,
+                                                rs, nrhs, f->bad);
+  CKL();
+  ++f->launches;
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, f->bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return bad == 0;
 }
 
 void lu_release(LuFactor* f, cudaStream_t s) {

@@ -135,6 +135,19 @@ def main():
         a, it = R.alpha_bisection(n, SINGLE, 1e-2, 1e2, 9, Dichotomy.make(budget=9, train_xi=1e-8, max_outer=800))
         out[f"ts_{n}"] = np.array([n ** 3, a, it], dtype=np.float64)
 
+    # 8. Sylvester GADI-AB (sylvester.cpp, problems.cpp:45-66): test_problems.cpp:152-160
+    #    and acceptance criterion 7's table configuration (n = 64, half/double/double)
+    syl = [("s16", 16, 0.1, dict(alpha=0.5, xi=1e-22, max_outer_iters=20000)),
+           ("c7a", 64, 0.1, dict(alpha=0.02, xi=0.0, u_r=HALF, max_outer_iters=30000, stall_window=400,
+                                 residual_scaling=0)),
+           ("c7b", 64, 1.0, dict(alpha=10.0, xi=0.0, u_r=HALF, max_outer_iters=30000, stall_window=400,
+                                 residual_scaling=0)),
+           ("sgl", 24, 0.5, dict(alpha=0.3, xi=1e-12, u_r=SINGLE, u=SINGLE, u_f=SINGLE, max_outer_iters=5000))]
+    for tag, n, r, kw in syl:
+        X, rep, hist = R.sylvester_solve(n, r, Config.make(**kw))
+        out[f"syl_{tag}_X"], out[f"syl_{tag}_hist"] = X, hist
+        out[f"syl_{tag}_info"] = np.array([rep.status, rep.outer_iters, rep.inner_iter_totals, rep.inner_stagnations])
+
     path = os.path.join(HERE, "reference_vectors.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path} ({os.path.getsize(path)} bytes, {len(out)} arrays)")

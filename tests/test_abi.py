@@ -7,6 +7,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 import paper_2501_04229_b200 as g
@@ -106,3 +107,16 @@ def test_training_csv_round_trip():
     assert buf.getvalue().splitlines()[0] == "n,alpha,iters,precision"
     back = g.read_training_csv(io.StringIO(buf.getvalue()))
     assert back == ts
+
+
+def test_build_sylvester_mirror():
+    """build_sylvester (problems.cpp:45-66): tridiagonal A = B, C = -(row + column sums)."""
+    import paper_2501_04229_b200 as g
+    p = g.build_sylvester(5, 0.5)
+    sh = 100.0 / 36.0
+    assert p.A.nnz() == 13 and p.A.values[0] == 2.0 + sh and p.A.values[1] == -1.0 + 0.5
+    dense = np.zeros((5, 5))
+    for i in range(5):
+        for k in range(p.A.row_ptr[i], p.A.row_ptr[i + 1]):
+            dense[i, p.A.col_idx[k]] = p.A.values[k]
+    assert np.allclose(dense @ np.ones((5, 5)) + np.ones((5, 5)) @ dense + p.C_rhs, 0.0, atol=1e-13)
