@@ -28,8 +28,8 @@ struct gadi_sylv {
   std::vector<double> av, tv;
   int64_t *d_arp = nullptr, *d_aci = nullptr, *d_trp = nullptr, *d_tci = nullptr;
   double *d_av = nullptr, *d_tv = nullptr, *d_g = nullptr;
-  double *x = nullptr, *sres = nullptr, *t = nullptr, *rhat = nullptr, *z = nullptr, *pz = nullptr;
-  double* scal = nullptr;  // device scalars: [0] norm result, [1] max bits
+  double *x = nullptr, *sres = nullptr, *t = nullptr, *rhat = nullptr, *z = nullptr, *pz = nullptr, *w = nullptr;
+  double* scal = nullptr;  // device scalars: [0] norm, [1] inf-norm bits, [2] flag, [3] norm max bits
   LuFactor *fa = nullptr, *fbt = nullptr;
   std::vector<double> history;
   int64_t launches = 0;
@@ -75,20 +75,36 @@ __global__ void k_sy_gap(int64_t m, int64_t n, const int64_t* __restrict__ arp, 
   r[q] = __dsub_rn(g[q], __dadd_rn(a, b));
 }
 
-// norm2_64 (kernels.cpp:184-194), sequential as the reference sums it
-__global__ void k_sy_norm2_64(const double* __restrict__ x, int64_t N, double* out) {
+// norm2_64 (kernels.cpp:184-194): m = max|x_i| (exact in any order), the
+// terms RN(RN(x_i/m)^2) in parallel, then their sum in the reference's
+// sequential order by one thread (only the additions form a chain).
+__global__ void k_sy_sq(const double* __restrict__ x, int64_t N, const unsigned long long* __restrict__ mbits,
+                        double* __restrict__ w) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const double m = __longlong_as_double((long long)*mbits);
+  const double q = __ddiv_rn(x[i], m);
+  w[i] = __dmul_rn(q, q);
+}
+
+__global__ void k_sy_seqsum(const double* __restrict__ w, int64_t N, const unsigned long long* __restrict__ mbits,
+                            double* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double m = 0.0;
-  for (int64_t i = 0; i < N; ++i) m = fmax_ref(m, fabs(x[i]));
+  const double m = __longlong_as_double((long long)*mbits);
   if (m == 0.0 || !isfinite(m)) {
     *out = m;
     return;
   }
   double s = 0.0;
-  for (int64_t i = 0; i < N; ++i) {
-    const double q = __ddiv_rn(x[i], m);
-    s = __dadd_rn(s, __dmul_rn(q, q));
+  int64_t i = 0;
+  for (; i + 8 <= N; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = w[i + k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s = __dadd_rn(s, v[k]);
   }
+  for (; i < N; ++i) s = __dadd_rn(s, w[i]);
   *out = __dmul_rn(m, __dsqrt_rn(s));
 }
 
@@ -149,9 +165,13 @@ double read_scalar(gadi_sylv* y) {
 }
 
 double norm2_64(gadi_sylv* y, const double* v) {
-  k_sy_norm2_64<<<1, 32, 0, y->s>>>(v, y->N, y->scal);
+  unsigned long long* mb = (unsigned long long*)(y->scal + 3);
+  CK(cudaMemsetAsync(mb, 0, 8, y->s));
+  k_sy_infnorm<<<grid(y->N), 256, 0, y->s>>>(v, y->N, mb);  // std::max(m, |x_i|): NaN never wins
+  k_sy_sq<<<grid(y->N), 256, 0, y->s>>>(v, y->N, mb, y->w);
+  k_sy_seqsum<<<1, 32, 0, y->s>>>(y->w, y->N, mb, y->scal);
   CKL();
-  ++y->launches;
+  y->launches += 3;
   return read_scalar(y);
 }
 
@@ -367,7 +387,7 @@ int gadi_sylv_create(int64_t m, const int64_t* a_rp, const int64_t* a_ci, const 
     y->d_tci = dupload(y->tci, y->s);
     y->d_tv = dupload(y->tv, y->s);
     y->d_g = dupload(std::vector<double>(G, G + y->N), y->s);
-    for (double** p : {&y->x, &y->sres, &y->t, &y->rhat, &y->z, &y->pz})
+    for (double** p : {&y->x, &y->sres, &y->t, &y->rhat, &y->z, &y->pz, &y->w})
       CK(cudaMallocAsync((void**)p, y->N * 8, y->s));
     CK(cudaMallocAsync((void**)&y->scal, 32, y->s));
     CK(cudaStreamSynchronize(y->s));
@@ -388,7 +408,7 @@ int gadi_sylv_destroy(gadi_sylv* y) {
   release_factors(y);
   for (void* p : {(void*)y->d_arp, (void*)y->d_aci, (void*)y->d_av, (void*)y->d_trp, (void*)y->d_tci,
                   (void*)y->d_tv, (void*)y->d_g, (void*)y->x, (void*)y->sres, (void*)y->t, (void*)y->rhat,
-                  (void*)y->z, (void*)y->pz, (void*)y->scal})
+                  (void*)y->z, (void*)y->pz, (void*)y->w, (void*)y->scal})
     if (p) cudaFreeAsync(p, y->s);
   cudaStreamSynchronize(y->s);
   cudaStreamDestroy(y->s);
