@@ -94,6 +94,8 @@ inline Geo make_geo(int64_t N, int vec) {
   g.L = (int)std::min<int64_t>(32, nseg);
   g.W = (int)std::min<int64_t>(8, nseg / g.L);
   g.R = RMAX;
+  if (const char* e = std::getenv("GADI_GEO_R"))  // tuning knob: segments per lane (<= RMAX)
+    g.R = std::max(1, std::min(RMAX, std::atoi(e)));
   while (g.R > 1 && nseg / ((int64_t)g.L * g.W * g.R) < 592) g.R /= 2;
   g.nblk = (int)(nseg / ((int64_t)g.L * g.W * g.R));
   return g;
