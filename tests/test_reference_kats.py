@@ -28,13 +28,18 @@ def csr_diag(d):
 
 
 KRYLOV = dict(method=CG, tol_epsilon=1e-12, max_inner_iters=200)
+# the reference's tests run its default InnerSolverSpec{} (lu_direct, inner_solver.hpp:20-25)
+LU = dict(method=0, tol_epsilon=1e-2, max_inner_iters=1000)
 
 
 class OracleBackend:
     name = "oracle"
 
+    def __init__(self, inner=KRYLOV):
+        self.inner = inner
+
     def solve(self, A, b, stencil_n=None, x0=None, **kw):
-        cfg = Config.make(**{**KRYLOV, **kw})
+        cfg = Config.make(**{**self.inner, **kw})
         try:
             x, rep, hist = ORC.solve(A, b, cfg, x0=x0)
         except ValueError as e:
@@ -50,9 +55,11 @@ class OracleBackend:
 class DeviceBackend:
     name = "device"
 
-    @staticmethod
-    def _cfg(kw):
-        kw = {**KRYLOV, **kw}
+    def __init__(self, inner=KRYLOV):
+        self.inner = inner
+
+    def _cfg(self, kw):
+        kw = {**self.inner, **kw}
         inner = g.InnerSolverSpec(g.InnerMethod(kw.pop("method")), kw.pop("tol_epsilon"), kw.pop("max_inner_iters"),
                                   kw.pop("restart", 30))
         for k in ("u_r", "u", "u_f"):
@@ -75,9 +82,12 @@ class DeviceBackend:
         return x, it, st
 
 
-@pytest.fixture(params=["oracle", pytest.param("device", marks=pytest.mark.gpu)])
+@pytest.fixture(params=["oracle-krylov", "oracle-lu", pytest.param("device-krylov", marks=pytest.mark.gpu),
+                        pytest.param("device-lu", marks=pytest.mark.gpu)])
 def be(request):
-    return OracleBackend() if request.param == "oracle" else DeviceBackend()
+    where, inner = request.param.split("-")
+    inner = LU if inner == "lu" else KRYLOV
+    return OracleBackend(inner) if where == "oracle" else DeviceBackend(inner)
 
 
 def convdiff(n):
@@ -139,7 +149,7 @@ def test_stall_window(be):
 def test_krylov_drives_outer_below_target(be):
     """test_solver.cpp:185-203."""
     A, b = convdiff(4)
-    _, st, _, _, inner, final = be.solve(A, b, stencil_n=4, alpha=0.5, xi=1e-18, tol_epsilon=1e-12,
+    _, st, _, _, inner, final = be.solve(A, b, stencil_n=4, alpha=0.5, xi=1e-18, method=CG, tol_epsilon=1e-12,
                                          max_inner_iters=3000, max_outer_iters=10000)
     assert st == g.SolveStatus.Converged and final <= 1e-9 and inner > 0
 
