@@ -10,6 +10,10 @@
 // order, which is unspecified among equal keys; for duplicate-free files (and
 // duplicates whose sum is exact) the result is the reference's bit for bit.
 #include <cub/device/device_radix_sort.cuh>
+#include <atomic>
+#include <charconv>
+#include <iterator>
+#include <thread>
 #include <cctype>
 #include <cinttypes>
 #include <cstdio>
@@ -136,6 +140,79 @@ void assemble(gadi_csr* out, std::vector<int64_t>& r, std::vector<int64_t>& c, s
   CK(cudaStreamDestroy(s));
 }
 
+bool is_ws(char ch) { return ch == ' ' || ch == '\n' || ch == '\t' || ch == '\r' || ch == '\v' || ch == '\f'; }
+
+// The first 3*entries whitespace-separated tokens of buf as (i, j, v) triples,
+// parsed by threads over whitespace-aligned chunks (std::from_chars: the
+// correctly rounded decimal conversion, as the stream's strtod). Returns 1 on
+// success, -1 if there are fewer tokens (truncated), 0 when some token is not
+// a plain decimal (then the caller re-parses with the reference's stream loop).
+int fast_entries(const std::string& buf, int64_t entries, std::vector<int64_t>& fi, std::vector<int64_t>& fj,
+                 std::vector<double>& fv) {
+  const size_t n = buf.size();
+  const int64_t need = 3 * entries;
+  const int T = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<size_t> cut(T + 1, n);
+  cut[0] = 0;
+  for (int t = 1; t < T; ++t) {
+    size_t p = std::max(cut[t - 1], n * t / T);
+    while (p < n && !is_ws(buf[p])) ++p;
+    cut[t] = p;
+  }
+  std::vector<int64_t> cnt(T + 1, 0);
+  auto tokens = [&](int t, auto&& f) {
+    size_t p = cut[t];
+    const size_t e = cut[t + 1];
+    while (p < e) {
+      while (p < e && is_ws(buf[p])) ++p;
+      if (p >= e) break;
+      size_t q = p;
+      while (q < e && !is_ws(buf[q])) ++q;
+      if (!f(p, q)) return;
+      p = q;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] { tokens(t, [&](size_t, size_t) { ++cnt[t + 1]; return true; }); });
+  for (auto& h : th) h.join();
+  th.clear();
+  for (int t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+  if (cnt[T] < need) return -1;
+  fi.resize(entries);
+  fj.resize(entries);
+  fv.resize(entries);
+  std::atomic<bool> ok{true};
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      int64_t k = cnt[t];
+      tokens(t, [&](size_t p, size_t q) {
+        if (k >= need || !ok) return false;
+        const char* a = buf.data() + p;
+        const char* b = buf.data() + q;
+        const int64_t e = k / 3;
+        if (k % 3 < 2) {  // an index: digits with an optional '-'
+          int64_t v = 0;
+          auto r = std::from_chars(a, b, v);
+          if (r.ec != std::errc() || r.ptr != b) ok = false;
+          (k % 3 == 0 ? fi : fj)[e] = v;
+        } else {  // a value: [-]digits[.digits][e[+-]digits]
+          for (const char* z = a; z < b; ++z)
+            if (!((*z >= '0' && *z <= '9') || *z == '-' || *z == '+' || *z == '.' || *z == 'e' || *z == 'E'))
+              ok = false;
+          double v = 0.0;
+          auto r = std::from_chars(a, b, v);
+          if (r.ec != std::errc() || r.ptr != b) ok = false;
+          fv[e] = v;
+        }
+        ++k;
+        return true;
+      });
+    });
+  for (auto& h : th) h.join();
+  return ok ? 1 : 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -173,10 +250,24 @@ int gadi_mm_read(const char* path, int32_t device, gadi_csr** out) {
     r.reserve(cap);
     c.reserve(cap);
     x.reserve(cap);
+    // the entry list: parsed in parallel when every token is a plain decimal
+    // (what write_matrix_market produces), else by the reference's stream loop
+    std::string rest((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    std::vector<int64_t> fi, fj;
+    std::vector<double> fv;
+    const int fast = fast_entries(rest, entries, fi, fj, fv);
+    if (fast < 0) throw Err(GADI_E_IO, "matrix market: truncated entry list");
+    std::istringstream slow(fast == 0 ? rest : std::string());
     for (int64_t k = 0; k < entries; ++k) {
       int64_t i = 0, j = 0;
       double v = 0.0;
-      if (!(in >> i >> j >> v)) throw Err(GADI_E_IO, "matrix market: truncated entry list");
+      if (fast) {
+        i = fi[k];
+        j = fj[k];
+        v = fv[k];
+      } else if (!(slow >> i >> j >> v)) {
+        throw Err(GADI_E_IO, "matrix market: truncated entry list");
+      }
       --i;
       --j;  // 1-based on disk
       if (i < 0 || i >= rows || j < 0 || j >= cols) bad = true;  // from_triplets throws after parsing

@@ -53,6 +53,9 @@ def main():
           "3 3 4\n3 2 -1.25\n2 2 4\n")
     write("skew.mtx", "%%MatrixMarket MATRIX Coordinate Real Skew-Symmetric\n3 3 2\n2 1 0.5\n3 1 -2\n")
     write("integer.mtx", "%%MatrixMarket matrix coordinate integer general\n2 2 3\n1 2 3\n2 1 -4\n2 2 1\n")
+    # tokens the parallel parser hands back to the stream loop: '+' signs, entries across lines
+    write("stream_tokens.mtx", "%%MatrixMarket matrix coordinate real general\n3 3 4\n+1 1 +2.5\n2\n2 -1e+1 3 3\n"
+          "0.5 1 3 +4.\n")
     write("empty.mtx", "%%MatrixMarket matrix coordinate real general\n3 3 0\n")
     # a larger random file: 2000 x 2000, 30000 entries, ~10% duplicates, dyadic values
     n, m = 2000, 30000
