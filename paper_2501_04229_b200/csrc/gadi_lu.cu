@@ -472,69 +472,95 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int P, bool FWD>
+template <int P, bool FWD, int POS>
 __global__ void __launch_bounds__(32) k_lu_pipe(const typename LuPol<P>::S* __restrict__ ab, int64_t N, int64_t kl,
                                                 int64_t ku, int64_t ldab, typename LuPol<P>::S* x,
                                                 unsigned* __restrict__ flags, unsigned* __restrict__ ticket,
                                                 unsigned epoch) {
+  // a block is B = 32*POS positions; lane l owns positions B*b + l + 32p (p < POS)
   using Pol = LuPol<P>;
   using S = typename Pol::S;
+  constexpr int B = 32 * POS;
   const int lane = threadIdx.x;
-  const int64_t ldoff = kl + ku, nblk = (N + 31) / 32, reach = FWD ? kl : ldoff;
+  const int64_t ldoff = kl + ku, nblk = (N + B - 1) / B, reach = FWD ? kl : ldoff;
   for (;;) {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(ticket, 1u);
     t = __shfl_sync(~0u, t, 0);
     if ((int64_t)t >= nblk) return;
-    const int64_t b = FWD ? (int64_t)t : nblk - 1 - (int64_t)t;  // block b holds positions 32b .. 32b+31
-    const int64_t i = 32 * b + lane;
-    const bool live = i < N;
-    S v = live ? x[i] : S(0);
+    const int64_t b = FWD ? (int64_t)t : nblk - 1 - (int64_t)t;
+    int64_t ip[POS];
+    S v[POS];
+#pragma unroll
+    for (int p = 0; p < POS; ++p) {
+      ip[p] = B * b + lane + 32 * p;
+      v[p] = ip[p] < N ? x[ip[p]] : S(0);
+    }
     // earlier blocks in sweep order whose columns reach this block
-    const int64_t dlo = FWD ? (32 * b - reach > 0 ? (32 * b - reach) / 32 : 0) : b + 1;
-    const int64_t dhi = FWD ? b - 1 : (32 * b + 31 + reach < N - 1 ? (32 * b + 31 + reach) / 32 : nblk - 1);
+    const int64_t dlo = FWD ? (B * b - reach > 0 ? (B * b - reach) / B : 0) : b + 1;
+    const int64_t dhi = FWD ? b - 1 : (B * b + B - 1 + reach < N - 1 ? (B * b + B - 1 + reach) / B : nblk - 1);
     for (int64_t s = 0; s <= dhi - dlo; ++s) {
       const int64_t d = FWD ? dlo + s : dhi - s;  // ascending j (forward), descending j (back)
-      S m[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {  // the band entries, issued before the wait
-        const int64_t j = 32 * d + c;
-        const int64_t off = FWD ? i - j : j - i;
-        m[c] = (live && j < N && off >= 1 && off <= reach) ? ab[j * ldab + ldoff + i - j] : S(0);
+      for (int kk = 0; kk < POS; ++kk) {
+        const int ch = FWD ? kk : POS - 1 - kk;  // 32-column chunk of block d
+        S m[POS][32];
+#pragma unroll
+        for (int p = 0; p < POS; ++p)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {  // the band entries, issued before the wait
+            const int64_t j = B * d + 32 * ch + c;
+            const int64_t off = FWD ? ip[p] - j : j - ip[p];
+            m[p][c] = (ip[p] < N && j < N && off >= 1 && off <= reach) ? ab[j * ldab + ldoff + ip[p] - j] : S(0);
+          }
+        if (kk == 0)
+          while (ld_acquire(flags + d) != epoch) {
+          }
+        const S xd = (B * d + 32 * ch + lane < N) ? __ldcg(x + B * d + 32 * ch + lane) : S(0);
+#pragma unroll
+        for (int cc = 0; cc < 32; ++cc) {
+          const int c = FWD ? cc : 31 - cc;
+          const int64_t j = B * d + 32 * ch + c;
+          const S xj = __shfl_sync(~0u, xd, c);
+#pragma unroll
+          for (int p = 0; p < POS; ++p) {
+            const int64_t off = FWD ? ip[p] - j : j - ip[p];
+            if (ip[p] < N && xj != S(0) && j < N && off >= 1 && off <= reach) v[p] = Pol::sub(v[p], Pol::mul(m[p][c], xj));
+          }
+        }
       }
-      while (ld_acquire(flags + d) != epoch) {
-      }
-      const S xd = (32 * d + lane < N) ? __ldcg(x + 32 * d + lane) : S(0);
+    }
+    // own triangle, chunk by chunk in sweep order
+#pragma unroll
+    for (int kk = 0; kk < POS; ++kk) {
+      const int ch = FWD ? kk : POS - 1 - kk;
+      S m[POS][32];
+#pragma unroll
+      for (int p = 0; p < POS; ++p)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int64_t j = B * b + 32 * ch + c;
+          const int64_t off = FWD ? ip[p] - j : j - ip[p];
+          m[p][c] = (ip[p] < N && j < N && off >= 0 && off <= reach) ? ab[j * ldab + ldoff + ip[p] - j] : S(1);
+        }
 #pragma unroll
       for (int cc = 0; cc < 32; ++cc) {
         const int c = FWD ? cc : 31 - cc;
-        const int64_t j = 32 * d + c;
-        const int64_t off = FWD ? i - j : j - i;
-        const S xj = __shfl_sync(~0u, xd, c);
-        if (live && xj != S(0) && j < N && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
+        const int64_t j = B * b + 32 * ch + c;
+        if (j < N) {
+          if (!FWD && lane == c) v[ch] = Pol::div(v[ch], m[ch][c]);  // U(j,j)
+          const S xj = __shfl_sync(~0u, v[ch], c);
+#pragma unroll
+          for (int p = 0; p < POS; ++p) {
+            const int64_t off = FWD ? ip[p] - j : j - ip[p];
+            if (ip[p] < N && xj != S(0) && off >= 1 && off <= reach) v[p] = Pol::sub(v[p], Pol::mul(m[p][c], xj));
+          }
+        }
       }
     }
-    // own triangle
-    S m[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const int64_t j = 32 * b + c;
-      const int64_t off = FWD ? i - j : j - i;
-      m[c] = (live && j < N && off >= 0 && off <= reach && (FWD ? off >= 1 : true)) ? ab[j * ldab + ldoff + i - j]
-                                                                                    : S(1);
-    }
-#pragma unroll
-    for (int cc = 0; cc < 32; ++cc) {
-      const int c = FWD ? cc : 31 - cc;
-      const int64_t j = 32 * b + c;
-      if (j < N) {
-        if (!FWD && lane == c) v = Pol::div(v, m[c]);  // U(j,j)
-        const S xj = __shfl_sync(~0u, v, c);
-        const int64_t off = FWD ? i - j : j - i;
-        if (live && xj != S(0) && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
-      }
-    }
-    if (live) x[i] = v;
+    for (int p = 0; p < POS; ++p)
+      if (ip[p] < N) x[ip[p]] = v[p];
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release(flags + b, epoch);
@@ -599,16 +625,25 @@ void solve_impl(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
   const S* ab = static_cast<const S*>(f->ab);
   const unsigned g = (unsigned)((N + 255) / 256);
   k_lu_in<T, S><<<g, 256, 0, s>>>(static_cast<const T*>(rhs), xw, N);
-  const int64_t nblk = (N + 31) / 32;
+  // 32-position blocks (one per lane); GADI_LU_POS=2 selects 64 (two per lane: half the dependent
+  // hops, but 3x slower at C1 -- register spills and twice the per-block work)
+  static const int pos_env = std::getenv("GADI_LU_POS") ? std::atoi(std::getenv("GADI_LU_POS")) : 0;
+  const int pos = pos_env == 2 ? 2 : 1;
+  const int64_t nblk = (N + 32 * pos - 1) / (32 * pos);
   const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)f->sms * 16);
-  if (f->swaps) {  // row interchanges in the forward sweep: one CTA (k_lu_fwd handles the swaps)
-    k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
-  } else {
+  auto pipe = [&](auto fwd) {
+    constexpr bool F = decltype(fwd)::value;
     CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
-    k_lu_pipe<P, true><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
-  }
-  CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
-  k_lu_pipe<P, false><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
+    if (pos == 2)
+      k_lu_pipe<P, F, 2><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
+    else
+      k_lu_pipe<P, F, 1><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
+  };
+  if (f->swaps)  // row interchanges in the forward sweep: one CTA (k_lu_fwd handles the swaps)
+    k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
+  else
+    pipe(std::true_type{});
+  pipe(std::false_type{});
   k_lu_out<T, S><<<g, 256, 0, s>>>(xw, static_cast<T*>(x), N, f->bad);
   CKL();
   f->launches += 4;
