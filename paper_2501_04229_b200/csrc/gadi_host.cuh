@@ -581,6 +581,7 @@ struct LuFactor {
   int* bad = nullptr;
   unsigned* flags = nullptr;  // pipelined solves: per-block epoch flags, then the block ticket
   unsigned* ticket = nullptr;
+  unsigned long long* xt = nullptr;  // binary32 sweeps: (value | epoch << 32) words
   unsigned epoch = 0;
   bool swaps = false;         // any row interchange (forward solve needs the swap-aware kernel)
   int sms = 148;

@@ -567,6 +567,96 @@ __global__ void __launch_bounds__(32) k_lu_pipe(const typename LuPol<P>::S* __re
   }
 }
 
+// The same sweeps for binary32 slots (u_r = half / single) without flags or
+// fences: every x value is published as one 64-bit word (value bits | epoch
+// << 32), written once with a single-copy-atomic store; a consumer lane polls
+// exactly the word it needs until the epoch matches. Each dependent hop is one
+// L2 round trip instead of store + fence + flag + load.
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int P, bool FWD>
+__global__ void __launch_bounds__(32) k_lu_pipe_t(const float* __restrict__ ab, int64_t N, int64_t kl, int64_t ku,
+                                                  int64_t ldab, const float* __restrict__ x0,
+                                                  unsigned long long* xt, unsigned* __restrict__ ticket,
+                                                  unsigned epoch) {
+  using Pol = LuPol<P>;
+  const int lane = threadIdx.x;
+  const int64_t ldoff = kl + ku, nblk = (N + 31) / 32, reach = FWD ? kl : ldoff;
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1u);
+    t = __shfl_sync(~0u, t, 0);
+    if ((int64_t)t >= nblk) return;
+    const int64_t b = FWD ? (int64_t)t : nblk - 1 - (int64_t)t;
+    const int64_t i = 32 * b + lane;
+    const bool live = i < N;
+    float v = live ? (FWD ? x0[i] : __uint_as_float((unsigned)xt[i])) : 0.f;
+    const int64_t dlo = FWD ? (32 * b - reach > 0 ? (32 * b - reach) / 32 : 0) : b + 1;
+    const int64_t dhi = FWD ? b - 1 : (32 * b + 31 + reach < N - 1 ? (32 * b + 31 + reach) / 32 : nblk - 1);
+    for (int64_t s = 0; s <= dhi - dlo; ++s) {
+      const int64_t d = FWD ? dlo + s : dhi - s;
+      float m[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int64_t j = 32 * d + c;
+        const int64_t off = FWD ? i - j : j - i;
+        m[c] = (live && j < N && off >= 1 && off <= reach) ? ab[j * ldab + ldoff + i - j] : 0.f;
+      }
+      float xd = 0.f;
+      if (32 * d + lane < N) {
+        unsigned long long w;
+        do {
+          w = ld_relaxed64(xt + 32 * d + lane);
+        } while ((unsigned)(w >> 32) != epoch);
+        xd = __uint_as_float((unsigned)w);
+      }
+#pragma unroll
+      for (int cc = 0; cc < 32; ++cc) {
+        const int c = FWD ? cc : 31 - cc;
+        const int64_t j = 32 * d + c;
+        const int64_t off = FWD ? i - j : j - i;
+        const float xj = __shfl_sync(~0u, xd, c);
+        if (live && xj != 0.f && j < N && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
+      }
+    }
+    float m[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      const int64_t j = 32 * b + c;
+      const int64_t off = FWD ? i - j : j - i;
+      m[c] = (live && j < N && off >= 0 && off <= reach && (FWD ? off >= 1 : true)) ? ab[j * ldab + ldoff + i - j] : 1.f;
+    }
+#pragma unroll
+    for (int cc = 0; cc < 32; ++cc) {
+      const int c = FWD ? cc : 31 - cc;
+      const int64_t j = 32 * b + c;
+      if (j < N) {
+        if (!FWD && lane == c) v = Pol::div(v, m[c]);
+        const float xj = __shfl_sync(~0u, v, c);
+        const int64_t off = FWD ? i - j : j - i;
+        if (live && xj != 0.f && off >= 1 && off <= reach) v = Pol::sub(v, Pol::mul(m[c], xj));
+      }
+    }
+    if (live) st_relaxed64(xt + i, ((unsigned long long)epoch << 32) | __float_as_uint(v));
+  }
+}
+
+__global__ void k_lu_untag(const unsigned long long* __restrict__ xt, float* __restrict__ x, int64_t N) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) x[i] = __uint_as_float((unsigned)xt[i]);
+}
+__global__ void k_lu_tag(const float* __restrict__ x, unsigned long long* __restrict__ xt, int64_t N) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N) xt[i] = __float_as_uint(x[i]);  // epoch 0: never a solve's epoch
+}
+
 template <class S>
 inline void pick_panel(int64_t kl, int& nb) {
   nb = 32;
@@ -639,6 +729,26 @@ void solve_impl(LuFactor* f, const void* rhs, void* x, cudaStream_t s) {
     else
       k_lu_pipe<P, F, 1><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->flags, f->ticket, ++f->epoch);
   };
+  if constexpr (!std::is_same<S, double>::value) {  // binary32 slots: tagged words, no flags
+    static const bool tagged = !(std::getenv("GADI_LU_TAGGED") && std::getenv("GADI_LU_TAGGED")[0] == '0');
+    if (tagged && pos == 1) {
+      const unsigned gN = (unsigned)((N + 255) / 256);
+      if (f->swaps) {
+        k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
+        k_lu_tag<<<gN, 256, 0, s>>>(xw, f->xt, N);
+      } else {
+        CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
+        k_lu_pipe_t<P, true><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->xt, f->ticket, ++f->epoch);
+      }
+      CK(cudaMemsetAsync(f->ticket, 0, sizeof(unsigned), s));
+      k_lu_pipe_t<P, false><<<grid, 32, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, xw, f->xt, f->ticket, ++f->epoch);
+      k_lu_untag<<<gN, 256, 0, s>>>(f->xt, xw, N);
+      k_lu_out<T, S><<<g, 256, 0, s>>>(xw, static_cast<T*>(x), N, f->bad);
+      CKL();
+      f->launches += 5;
+      return;
+    }
+  }
   if (f->swaps)  // row interchanges in the forward sweep: one CTA (k_lu_fwd handles the swaps)
     k_lu_fwd<P><<<1, 512, 0, s>>>(ab, N, f->kl, f->ku, f->ldab, f->ipiv, xw);
   else
@@ -727,6 +837,8 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
   CK(cudaMallocAsync((void**)&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
   CK(cudaMemsetAsync(f->flags, 0, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
   f->ticket = f->flags + (f->N + 31) / 32;
+  CK(cudaMallocAsync((void**)&f->xt, (size_t)f->N * 8, s));
+  CK(cudaMemsetAsync(f->xt, 0, (size_t)f->N * 8, s));  // epoch 0 on every word
   f->bad = f->err + 2;
   const int64_t ldoff = f->kl + f->ku, N = f->N;
   const unsigned g = (unsigned)((N + 255) / 256);
@@ -818,6 +930,8 @@ LuFactor* lu_factor_host_csr(int device, cudaStream_t s, int64_t N, const int64_
   CK(cudaMallocAsync((void**)&f->flags, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
   CK(cudaMemsetAsync(f->flags, 0, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
   f->ticket = f->flags + (N + 31) / 32;
+  CK(cudaMallocAsync((void**)&f->xt, (size_t)N * 8, s));
+  CK(cudaMemsetAsync(f->xt, 0, (size_t)N * 8, s));
   f->bad = f->err + 2;
   *status = ur == GADI_DOUBLE ? factor_impl<GADI_DOUBLE>(f.get(), s)
             : ur == GADI_SINGLE ? factor_impl<GADI_SINGLE>(f.get(), s)
@@ -849,7 +963,7 @@ bool lu_solve_many(LuFactor* f, double* X, int64_t es, int64_t rs, int64_t nrhs,
 
 void lu_release(LuFactor* f, cudaStream_t s) {
   if (!f) return;
-  for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err, (void*)f->flags})
+  for (void* p : {f->ab, (void*)f->ipiv, f->xw, (void*)f->err, (void*)f->flags, (void*)f->xt})
     if (p) {
       if (s) cudaFreeAsync(p, s);
       else cudaFree(p);  // synchronous: the owner may not have synchronised its stream
