@@ -652,9 +652,27 @@ struct Engine final : EngineBase {
   St25Geo g25h, g25mh;  // their geometries (3-plane operand ring)
   Window win;         // sparse operators: operand window in shared memory
 
+  // Work vectors come from the device's stream-ordered memory pool (kept,
+  // not released, between solves): re-preparing an engine -- every
+  // gadi_ir_solve does (solver.cpp:75) -- costs no cudaMalloc/cudaFree and no
+  // device-wide synchronisation.
+  T* salloc(int64_t n) {
+    static std::once_flag once[64];
+    std::call_once(once[h->device & 63], [&] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
+    T* p = nullptr;
+    CK(cudaMallocAsync((void**)&p, (size_t)n * sizeof(T), h->stream));
+    return p;
+  }
+
   T* vec() {  // a slab vector (ghost planes when sharded)
-    T* v = dalloc<T>(h->N + 2 * h->gh);
-    if (h->gh) CK(cudaMemset(v, 0, (h->N + 2 * h->gh) * sizeof(T)));
+    T* v = salloc(h->N + 2 * h->gh);
+    if (h->gh) CK(cudaMemsetAsync(v, 0, (h->N + 2 * h->gh) * sizeof(T), h->stream));
     owned.push_back(v);
     return v + h->gh;
   }
@@ -700,8 +718,8 @@ struct Engine final : EngineBase {
     // basis: m+1 vectors of ldv = N + 2 gh entries (a sharded sparse matvec
     // reads its operand v_j, a basis vector, at the ghost entries)
     ldv = N + 2 * h->gh;
-    T* vb = dalloc<T>((int64_t)(m_restart + 1) * ldv);
-    if (h->gh) CK(cudaMemset(vb, 0, (int64_t)(m_restart + 1) * ldv * sizeof(T)));
+    T* vb = salloc((int64_t)(m_restart + 1) * ldv);
+    if (h->gh) CK(cudaMemsetAsync(vb, 0, (int64_t)(m_restart + 1) * ldv * sizeof(T), h->stream));
     owned.push_back(vb);
     V = vb + h->gh;
     build_ops();
@@ -732,7 +750,7 @@ struct Engine final : EngineBase {
   }
 
   ~Engine() override {
-    for (T* v : owned) cudaFree(v);  // allocation bases
+    for (T* v : owned) cudaFreeAsync(v, h->stream);  // allocation bases, back to the pool
     if (dH) cudaFree(dH);
     if (dS) cudaFree(dS);
     sHS.release();
