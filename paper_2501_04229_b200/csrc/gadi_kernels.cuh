@@ -796,6 +796,23 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   double w1;
   seg_run_ld<VEC, true, false, G>(g, w, [&](const Seg& s, const T (&wv)[G], C& c, double&) {
     C tc[G];
+    if constexpr (MK && G % 2 == 0) {
+      // the same Markstein quotient and square per lane, two lanes per
+      // instruction (FMUL2 / FFMA2: one RN rounding per lane); the squares
+      // feed scalar FADDs, which ptxas never contracts with an FMUL2
+      const float2 y2 = make_float2(yf, yf), m2 = make_float2(-mf, -mf);
+#pragma unroll
+      for (int i = 0; i < G; i += 2) {
+        const float2 wf = __half22float2(__halves2half2(wv[i], wv[i + 1]));
+        const float2 q0 = __fmul2_rn(wf, y2);
+        const float2 q = __ffma2_rn(__ffma2_rn(q0, m2, wf), y2, q0);
+        const float2 sq = __fmul2_rn(q, q);
+        tc[i] = sq.x;
+        tc[i + 1] = sq.y;
+      }
+      c = seg_sum<C, G>(tc, s.len);
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       C qv;
