@@ -313,7 +313,8 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     rep->h_iters += zo.iters;
     if (zo.status == INNER_OVERFLOW) { rep->status = GADI_OVERFLOW_DETECTED; break; }
     if (zo.status == INNER_STAGNATED) ++rep->inner_stagnations;
-    e->scale_pz(p_rounded);
+    if (lu) e->scale_pz(p_rounded);
+    else e->defer_pz(p_rounded);  // formed inside the GMRES zero-start residual pass
     // solve_S: a cg request degrades to gmres (solver.cpp:217-221)
     InnerOut yo = lu ? lu_solve(h, e, 2, e->pz, e->y) : e->gmres(2, e->pz, e->y, target);
     CK(cudaEventRecord(h->evC, s));

@@ -101,6 +101,7 @@ inline Geo make_geo(int64_t N, int vec) {
   return g;
 }
 
+
 // Operand window of a banded sparse operator staged in shared memory
 // (gadi_kernels.cuh stage_window): the band passed to the kernel (0 = read the
 // operand from global memory) and the dynamic shared memory it needs. Used
@@ -616,6 +617,15 @@ struct EngineBase {
   virtual InnerOut gmres(int which, const void* rhs, void* x, double target) = 0;
   virtual void scale_round(const double* s) = 0;            // rhat = round(s 2^-e)
   virtual void scale_pz(double phat) = 0;                   // pz = round(phat z)
+  // pz = round(phat z) deferred: gmres(2, pz) forms it inside its zero-start
+  // residual pass and stores pz only if a later pass needs it (restart /
+  // happy-breakdown residual).
+  void defer_pz(double phat) {
+    pz_phat = phat;
+    pz_lazy = true;
+  }
+  double pz_phat = 0.0;
+  bool pz_lazy = false;
   virtual void update(double* x, int pu) = 0;               // x += 2^e y
   virtual void to_inner(const double* src, void* dst) = 0;  // round_vec to u_r
   virtual void to_double(const void* src, double* dst) = 0;
@@ -959,7 +969,13 @@ struct Engine final : EngineBase {
     auto HC = [&](int i, int j) -> double& { return Hc[(size_t)i * m + j]; };
     int total = 0, status = -1;
     bool x_zero = true;  // x = 0 until the first update (inner_solver.cpp:92)
+    bool lazy = rhs_v == pz && pz_lazy;  // rhs = round(pz_phat z), not stored yet
+    pz_lazy = false;
     auto resid = [&]() {  // r = rhs - S x ; flags, max, ||r||_2 (binary64), norm2 in fmt
+      if (lazy && !x_zero) {
+        scale_pz(pz_phat);
+        lazy = false;
+      }
       CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
@@ -969,7 +985,8 @@ struct Engine final : EngineBase {
           auto kern = k_gm_resid<Op, T, C, V_>;
           const size_t sm = x_zero ? 0 : win.bytes;
           smem_attr(kern, sm);
-          kern<<<geo.nblk, nt, sm, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st, x_zero ? 0 : win.band);
+          kern<<<geo.nblk, nt, sm, s>>>(o, x, x_zero ? 1 : 0, rhs, gr, geo, rd, h->st, x_zero ? 0 : win.band,
+                                        lazy ? static_cast<const T*>(z) : nullptr, pz_phat);
         }
         coll<C>(h, EpiRedD{});
         k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);

@@ -685,7 +685,8 @@ __device__ __forceinline__ C zero_resid(C acc, int f) {
 template <class Op, class T, class C, int VEC>
 __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x, int x_zero,
                                                   const T* __restrict__ rhs, T* __restrict__ r, Geo g, Red rd,
-                                                  DevState* st, int64_t wband = 0) {
+                                                  DevState* st, int64_t wband = 0,
+                                                  const T* __restrict__ zsrc = nullptr, double phat = 0.0) {
   GADI_G;
   constexpr bool EH = MatvecF<C, T>::EXACT_H;
   int bad = 0;
@@ -728,7 +729,25 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
     fin(s, d, acc);
   };
   if (x_zero) {  // from x = 0: the per-row zflag summaries, the matrix is not read
-    seg_run_ld<VEC, false, true, G>(g, rhs, [&](const Seg& s, const T (&bv)[G], C&, double& d) {
+    // zsrc != null: rhs = round(phat * z) is formed here (k_scale's formula;
+    // solver.cpp:155, the scale of z before solve_S) instead of being read.
+    // Binary16 z and phat: the product is exact in binary32 (22 significant
+    // bits, exponents in range), so one binary32 multiply and one rounding to
+    // binary16 equal the binary64 route.
+    const float pf = (float)phat;
+    bool f16 = false;
+    if constexpr (std::is_same<T, __half>::value) f16 = (double)__half2float(__float2half_rn(pf)) == phat;
+    seg_run_ld<VEC, false, true, G>(g, zsrc ? zsrc : rhs, [&](const Seg& s, const T (&bv0)[G], C&, double& d) {
+      T bv[G];
+      if (zsrc && f16) {
+        if constexpr (std::is_same<T, __half>::value) {
+#pragma unroll
+          for (int i = 0; i < G; ++i) bv[i] = __float2half_rn(__fmul_rn(pf, __half2float(bv0[i])));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < G; ++i) bv[i] = zsrc ? from_dbl<T>(__dmul_rn(phat, to_dbl(bv0[i]))) : bv0[i];
+      }
       C acc[G];
       if constexpr (VEC > 1) {
         int fl[VEC];
