@@ -616,6 +616,9 @@ struct EngineBase {
   virtual InnerOut cg(int which, void* rhs, void* x, double target) = 0;
   virtual InnerOut gmres(int which, const void* rhs, void* x, double target) = 0;
   virtual void scale_round(const double* s) = 0;            // rhat = round(s 2^-e)
+  // rhat = round(s 2^-ep) straight from the residual pass (u_f binary64,
+  // stencil operators); false: not available for this operator / shape
+  virtual bool resid_spec(const double* x, int ep, bool scaling) = 0;
   virtual void scale_pz(double phat) = 0;                   // pz = round(phat z)
   // pz = round(phat z) deferred: gmres(2, pz) forms it inside its zero-start
   // residual pass and stores pz only if a later pass needs it (restart /
@@ -1150,6 +1153,29 @@ struct Engine final : EngineBase {
     CKL();
     ++h->launches;
     coll<double>(h, EpiRhat{});
+  }
+  bool resid_spec(const double* x, int ep, bool scaling) override {
+    if constexpr (SPARSE) {
+      return false;
+    } else {
+      St25Geo gs;
+      if (!make_st25(h->n, 8, 1, gs, 1024, true, 0, h->i0, h->i1)) return false;
+      CK(cudaMemsetAsync(&h->st->maxbits, 0, sizeof(unsigned long long), h->stream));
+      halo(h, x);
+      const int64_t eo = h->e_off();
+      PolResidSpec<T> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3},
+                          x - eo,
+                          h->d_b - eo,
+                          static_cast<T*>(rhat) - eo,
+                          ep,
+                          (ep >= -1000 && ep <= 1000) ? std::ldexp(1.0, -ep) : 1.0,
+                          scaling ? 1 : 0};
+      launch_st25(pol, gs, h->stream, red_of(h), h->st);
+      CKL();
+      ++h->launches;
+      coll<double>(h, EpiResidSpec{scaling ? 1 : 0});
+      return true;
+    }
   }
   void scale_pz(double phat) override {
     V2([&](auto vt) {

@@ -996,6 +996,15 @@ struct EpiResidA {  // ||s||, max|s| and the scaling exponent (solver.cpp:48-53)
   __device__ int* flag_dst(DevState*) const { return nullptr; }
   __device__ bool skip(DevState* st) const { return (void)st, false; }
 };
+struct EpiResidSpec {  // EpiResidA + ||rhat||^2 of the speculative pass (PolResidSpec)
+  int scaling;
+  __device__ void finish(double rss, double ss, DevState* st) const {
+    EpiResidA{scaling}.finish(0.0, ss, st);
+    st->rhat_ss = rss;
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
 struct EpiRhat {  // ||rhat||_2
   __device__ void finish(double, double ss, DevState* st) const { st->rhat_ss = ss; }
   __device__ int* flag_dst(DevState*) const { return nullptr; }

@@ -246,7 +246,8 @@ constexpr int ST25_MAXW = 16;    // warps per CTA
 // subtree per (plane, tile) -> partials[plane * njt + tile].
 template <class P, class PL>
 __device__ __forceinline__ void st25_partials(const St25Geo& g, const Red& rd, const PL* plb, int nw, int ib,
-                                              int jt) {
+                                              int jt, const PL* plb1 = nullptr) {
+  if (!plb1) plb1 = plb;  // one reduced quantity: R1 shares the buffer
   using R0 = typename P::R0;
   if (P::HAS_R0 || P::HAS_R1) {
     __syncthreads();
@@ -257,7 +258,7 @@ __device__ __forceinline__ void st25_partials(const St25Geo& g, const Red& rd, c
       for (int k = 0; k < ST25_MAXW; ++k)
         if (k < nw) {
           if (P::HAS_R0) v0[k] = from_dbl<R0>(plb[t * nw + k]);
-          if (P::HAS_R1) v1[k] = plb[t * nw + k];
+          if (P::HAS_R1) v1[k] = plb1[t * nw + k];
         }
 #pragma unroll
       for (int s2 = 1; s2 < ST25_MAXW; s2 <<= 1)
@@ -324,8 +325,9 @@ __device__ __forceinline__ void st25_ticket(const P& pol, const St25Geo& g, cons
 
 template <class P, class PL>
 __device__ __forceinline__ void st25_finish(const P& pol, const St25Geo& g, const Red& rd, DevState* st,
-                                            const PL* plb, int nw, int ib, int jt, double mloc, int flag) {
-  st25_partials<P>(g, rd, plb, nw, ib, jt);
+                                            const PL* plb, int nw, int ib, int jt, double mloc, int flag,
+                                            const PL* plb1 = nullptr) {
+  st25_partials<P>(g, rd, plb, nw, ib, jt, plb1);
   st25_ticket(pol, g, rd, st, mloc, flag, (unsigned)g.nblk);
 }
 
@@ -354,8 +356,9 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
   RT* opr = reinterpret_cast<RT*>(raw + (size_t)S * P::NIN * pe);
   // per-(plane, warp) partial sums, folded over the warps once after the
   // plane loop (no block barrier per plane for the reductions)
-  static_assert(!(P::HAS_R0 && P::HAS_R1), "one reduced quantity per policy");
   __shared__ double plb[ST25_IL_MAX * ST25_MAXW];  // R0 values are held exactly in binary64
+  // a second reduced quantity (R0 and R1 both) gets its own buffer
+  __shared__ double plb1[(P::HAS_R0 && P::HAS_R1) ? ST25_IL_MAX * ST25_MAXW : 1];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int jt = blockIdx.x % g.njt, ic = blockIdx.x / g.njt;
@@ -583,7 +586,7 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
         }
     if (lane == 0) {
       if (P::HAS_R0) plb[(i - ib) * nw + warp] = to_dbl(a0[0]);
-      if (P::HAS_R1) plb[(i - ib) * nw + warp] = a1[0];
+      if (P::HAS_R1) ((P::HAS_R0 && P::HAS_R1) ? plb1 : plb)[(i - ib) * nw + warp] = a1[0];
     }
     if constexpr (P::IDENT) {
       __syncthreads();  // plane i is no longer read (plane i+1 folds it from xprv): refill its stage
@@ -593,7 +596,7 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
       }
     }
   }
-  st25_finish(pol, g, rd, st, plb, nw, ib, jt, mloc, flag);
+  st25_finish(pol, g, rd, st, plb, nw, ib, jt, mloc, flag, (P::HAS_R0 && P::HAS_R1) ? plb1 : plb);
 }
 
 // ------------------------------------------------ binary16 operator passes
@@ -1107,6 +1110,55 @@ struct PolResidA {
   }
   __device__ int* flag_dst(DevState*) const { return nullptr; }
   __device__ void finish(double t0, double ss, DevState* st) const { EpiResidA{scaling}.finish(t0, ss, st); }
+};
+
+// Speculative outer residual (u_f = binary64): s = b - A x as PolResidA, and in
+// the same pass rhat = round_{u_r}(s 2^-ep) (solver.cpp:86-92) with the
+// exponent ep of the previous outer step, plus ||rhat||^2 as a second
+// reduced quantity (R0). s itself is not stored. The host accepts the pass
+// when the exponent the epilogue derives from max|s| equals ep; otherwise it
+// reruns PolResidA + k_scale_round (same values, same trees).
+template <class TR>
+struct PolResidSpec {
+  using T = double;
+  using Acc = double;
+  using R0 = double;
+  using RT = double;
+  static constexpr int NIN = 1;
+  static constexpr bool HAS_R0 = true, HAS_R1 = true, HAS_MAX = true, HAS_FLAG = false, IDENT = true;
+  static constexpr bool FASTH = false;
+  double c7[7];
+  const double* x;
+  const double* b;
+  TR* rhat;
+  int ep;
+  double p2;  // 2^-ep
+  int scaling;
+  __device__ bool skip(DevState*) const { return false; }
+  __device__ void prepare(DevState*) {}
+  __device__ int nin() const { return 1; }
+  __device__ const double* in(int) const { return x; }
+  __device__ void make(const double* rs, int, int idx, double (&v)[2]) const { lds16<double, 2>(rs + idx, v); }
+  __device__ ResidAF<P_DOUBLE> fold() const { return ResidAF<P_DOUBLE>(); }
+  __device__ void init(int64_t e0, double (&acc)[2]) const { ld_vec<double, 2>(b, e0, acc); }
+  __device__ void epi(int64_t e0, const double (&acc)[2], const double (&)[2], double& c, double& d, double& m,
+                      int&) const {
+    double td[2], tc[2];
+    TR o[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      td[e] = __dmul_rn(acc[e], acc[e]);
+      m = (acc[e] == acc[e]) ? fmax(m, fabs(acc[e])) : m;
+      o[e] = from_dbl<TR>(ep != 0 ? ldexp_fast(acc[e], -ep, p2) : acc[e]);
+      const double dv = to_dbl(o[e]);
+      tc[e] = __dmul_rn(dv, dv);
+    }
+    st_vec<TR, 2>(rhat, e0, o);
+    c = seg_sum<double, 2>(tc, 2);
+    d = seg_sum<double, 2>(td, 2);
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ void finish(double t0, double ss, DevState* st) const { EpiResidSpec{scaling}.finish(t0, ss, st); }
 };
 
 #undef ST25_VEC
