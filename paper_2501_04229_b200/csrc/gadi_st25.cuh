@@ -242,6 +242,39 @@ constexpr int ST25_CPT_MAX = 4;
 constexpr int ST25_IL_MAX = 32;  // planes per CTA (make_st25)
 constexpr int ST25_MAXW = 16;    // warps per CTA
 
+// The pairwise trees of CPT per-lane values v[rr] over the 32 lanes (lane
+// levels xor 1, 2, ..., 16, as warp_tree), then over rr ((v0+v1)+(v2+v3)),
+// with the total in lane 0. The first log2(CPT) lane levels run as a
+// reduce-scatter (each lane keeps half of the trees and receives its
+// partner's half), so the CPT trees cost 2*CPT-2+5-log2(CPT) shuffles instead
+// of 5*CPT. Same pairs at every level, so bitwise equal to CPT warp_trees.
+template <int CPT, class C>
+__device__ __forceinline__ C warp_tree_cpt(C (&v)[CPT]) {
+  const int lane = threadIdx.x & 31;
+  C w[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) w[k] = v[k];
+  int o = 1;
+#pragma unroll
+  for (int m = CPT; m > 1; m >>= 1, o <<= 1) {  // keep trees [0,m/2) (bit clear) or [m/2,m) (bit set)
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < m / 2; ++k) {
+      const C send = hi ? w[k] : w[k + m / 2];
+      const C keep = hi ? w[k + m / 2] : w[k];
+      w[k] = Ar<C>::add(keep, shfl_xor_c(send, o, 0xffffffffu));
+    }
+  }
+  // this lane holds tree rr = sum_b bit_b(lane) * CPT / 2^(b+1) over levels 1..o
+  C t = w[0];
+#pragma unroll
+  for (int oo = o; oo < 32; oo <<= 1) t = Ar<C>::add(t, shfl_xor_c(t, oo, 0xffffffffu));
+  // tree over rr: its lowest level pairs rr differing in the last split bit
+#pragma unroll
+  for (int oo = o >> 1; oo >= 1; oo >>= 1) t = Ar<C>::add(t, shfl_xor_c(t, oo, 0xffffffffu));
+  return t;
+}
+
 // After a tile's plane loop: each plane's warp partials -> one pairwise
 // subtree per (plane, tile) -> partials[plane * njt + tile].
 template <class P, class PL>
@@ -514,8 +547,7 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
           fold8h<1>(acc, ch[4], ccu, k0 + VEC < n ? (uint32_t)ocu[sidx + VEC] : nh_of(ch[4]));
           if (j < n - 1) fold8h<0>(acc, ch[5], lds_u4(oc + sidx + n), 0u);
           if (op) fold8h<0>(acc, ch[6], lds_u4(op + sidx), 0u);
-          R0 c0 = pol.epi_h(e0, acc, ccu);
-          a0[rr] = warp_tree(c0, 32);
+          a0[rr] = pol.epi_h(e0, acc, ccu);
           continue;
         }
         Acc acc[VEC];
@@ -572,18 +604,14 @@ __global__ void __launch_bounds__(512) k_st25(const P pol_in, St25Geo g, Red rd,
         R0 c0 = Ar<R0>::zero();
         double d0 = 0.0;
         pol.epi(e0, acc, cc, c0, d0, mloc, flag);
-        if (P::HAS_R0) a0[rr] = warp_tree(c0, 32);
-        if (P::HAS_R1) a1[rr] = warp_tree(d0, 32);
+        if (P::HAS_R0) a0[rr] = c0;
+        if (P::HAS_R1) a1[rr] = d0;
       }
     }
-    // tree over this warp's CPT contiguous 32-chunk blocks, then over warps
-#pragma unroll
-    for (int s2 = 1; s2 < CPT; s2 <<= 1)
-#pragma unroll
-      for (int rr = 0; rr + s2 < CPT; rr += 2 * s2) {
-          if (P::HAS_R0) a0[rr] = Ar<R0>::add(a0[rr], a0[rr + s2]);
-          if (P::HAS_R1) a1[rr] = __dadd_rn(a1[rr], a1[rr + s2]);
-        }
+    // pairwise tree over each 32-chunk block's lanes, then over this warp's
+    // CPT contiguous blocks (total in lane 0), then over warps
+    if (P::HAS_R0) a0[0] = warp_tree_cpt<CPT>(a0);
+    if (P::HAS_R1) a1[0] = warp_tree_cpt<CPT>(a1);
     if (lane == 0) {
       if (P::HAS_R0) plb[(i - ib) * nw + warp] = to_dbl(a0[0]);
       if (P::HAS_R1) ((P::HAS_R0 && P::HAS_R1) ? plb1 : plb)[(i - ib) * nw + warp] = a1[0];
