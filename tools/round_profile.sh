@@ -12,7 +12,7 @@ python bench.py --workload c5 > "$OUT/bench_c5.json" 2> "$OUT/bench_c5.err"
 python bench.py --impl reference > "$OUT/bench_ref.json" 2> "$OUT/bench_ref.err"
 ncu -f --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file "$OUT/launches_c3_outer2.csv" python tools/profile_step.py --outer 2 > /dev/null 2>&1
-for k in PolSpmvp PolGmMatvec k_cg_update k_gm_mgs k_norm2 PolResidA; do
+for k in PolSpmvp PolGmMatvec k_cg_update k_gm_mgs k_norm2 PolResidSpec k_gm_resid; do
   ncu -f --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:$k \
     --launch-skip 2 -c 1 -o /tmp/full_$k python tools/profile_step.py --outer 1 > /dev/null 2>&1
   ncu -i /tmp/full_$k.ncu-rep --page raw --csv > "$OUT/raw_$k.csv"
