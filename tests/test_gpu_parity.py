@@ -314,3 +314,32 @@ def test_krylov_accum_fp32_bitwise(orc, kind, method):
                               af=SINGLE)
     assert (it, int(st)) == (wit, wst)
     assert same(x, wx)
+
+
+@pytest.mark.parametrize("n,fmt,accum,alpha", [(16, HALF, True, 0.4), (32, HALF, True, 0.5), (16, SINGLE, False, 0.1),
+                                               (8, DOUBLE, False, 0.5)])
+def test_speculative_outer_residual_equals_two_pass(orc, monkeypatch, n, fmt, accum, alpha):
+    """The single-pass outer residual (s, rhat with the previous step's
+    scaling exponent and ||rhat||^2 in one st25 pass, solver.cpp:86-92,
+    accepted iff the exponent is unchanged) against the two-pass route
+    (residual, then scale/round) forced with GADI_NO_SPEC: identical x,
+    residual history and counts, bit for bit, and both equal the oracle."""
+    S, A = stencil_and_csr(orc, n, r=0.0975 if n == 32 else None)
+    _, b = orc.make_rhs(A, 1, -1.0, 1.0)
+    gcfg = g.GadiConfig(alpha=alpha, xi=1e-20, u_r=g.Precision(fmt), stall_window=400,
+                        accum=g.Accum.Fp32 if accum else g.Accum.Native,
+                        inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30))
+    res = g.gadi_ir_solve(S, b, g.hss_split(S), gcfg)
+    monkeypatch.setenv("GADI_NO_SPEC", "1")
+    two = g.gadi_ir_solve(S, b, g.hss_split(S), gcfg)
+    monkeypatch.delenv("GADI_NO_SPEC")
+    assert int(res.report.status) == int(two.report.status) == 0
+    assert res.report.outer_iters == two.report.outer_iters
+    assert res.report.inner_iter_totals == two.report.inner_iter_totals
+    assert same(res.x, two.x)
+    assert same(res.report.rel_residual_history, two.report.rel_residual_history)
+    cfg = Config.make(alpha=alpha, xi=1e-20, u_r=fmt, method=CG, tol_epsilon=1e-12, max_inner_iters=5,
+                      stall_window=400, accum=1 if accum else 0)
+    wx, wrep, _ = orc.solve(A, b, cfg)
+    assert res.report.outer_iters == wrep.outer_iters
+    assert same(res.x, wx)
