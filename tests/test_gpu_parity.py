@@ -343,3 +343,53 @@ def test_speculative_outer_residual_equals_two_pass(orc, monkeypatch, n, fmt, ac
     wx, wrep, _ = orc.solve(A, b, cfg)
     assert res.report.outer_iters == wrep.outer_iters
     assert same(res.x, wx)
+
+
+@pytest.mark.parametrize("method", [CG, GMRES])
+def test_fast_binary16_passes_equal_generic_n256(monkeypatch, method):
+    """The register-operand binary16 stencil passes (k_st25h: CG p-update +
+    SpMV, Arnoldi matvec with the fused v = w/h scale) run
+    only when a warp's 32 chunks lie in one grid row (n >= 256); there they
+    must equal the generic st25 passes (validated against the oracle at small
+    n) bit for bit: GADI_ST25H=0 forces the generic ones."""
+    n = 256
+    S = g.build_convdiff3d(n, r=0.0975)
+    rng = np.random.default_rng(7)
+    rhs = rng.uniform(-1, 1, n ** 3).astype(np.float16).astype(np.float64)
+    rhs[3::11] = -0.0
+    rhs[::97] *= 1e-3
+    stop = float(np.sqrt(np.sum(rhs * rhs)))
+    spec = g.InnerSolverSpec(g.InnerMethod(method), 1e-9, 8, 5)
+
+    def run():
+        sysx = g.CudaGadiSystem(S)
+        sysx.prepare(0.2, 1.0, g.Precision.Half, spec, g.Accum.Fp32)
+        sysx.set_inner_stop_norm(stop)
+        return sysx.solve_H(rhs) if method == CG else sysx.solve_S(rhs)
+
+    x, it, st = run()
+    monkeypatch.setenv("GADI_ST25H", "0")
+    wx, wit, wst = run()
+    monkeypatch.delenv("GADI_ST25H")
+    assert (it, int(st)) == (wit, int(wst))
+    assert same(x, wx)
+
+
+def test_fast_path_whole_solve_n256_equals_generic(monkeypatch):
+    """Three outer steps at n = 256 (C3's operator and inner mode): the fast
+    binary16 passes, the speculative outer residual and the fused GMRES
+    zero-start residual against the generic passes and the two-pass outer
+    residual, bit for bit."""
+    n = 256
+    S = g.build_convdiff3d(n, r=0.0975)
+    b = np.random.default_rng(3).uniform(-1, 1, n ** 3)
+    cfg = g.GadiConfig(alpha=0.2, xi=1e-20, u_r=g.Precision.Half, accum=g.Accum.Fp32, max_outer_iters=3,
+                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30))
+    res = g.gadi_ir_solve(S, b, g.hss_split(S), cfg)
+    monkeypatch.setenv("GADI_ST25H", "0")
+    monkeypatch.setenv("GADI_NO_SPEC", "1")
+    ref = g.gadi_ir_solve(S, b, g.hss_split(S), cfg)
+    assert res.report.outer_iters == ref.report.outer_iters == 3
+    assert res.report.inner_iter_totals == ref.report.inner_iter_totals
+    assert same(res.x, ref.x)
+    assert same(res.report.rel_residual_history, ref.report.rel_residual_history)
