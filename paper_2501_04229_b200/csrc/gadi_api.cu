@@ -223,9 +223,9 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     CKL();
   }
   // nt0 = true_residual_norm(x) (solver.cpp:67)
-  OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
-  read_state(h);
-  const double nt0 = std::sqrt(h->h_st->res_ss);
+  h->ns = 0;
+  OuterA::resid_sync(h, h->d_x, nullptr, GADI_DOUBLE, false);
+  const double nt0 = res_norm(h);
   auto finish = [&]() {
     CK(cudaEventRecord(h->ev1, s));
     CK(cudaEventSynchronize(h->ev1));
@@ -255,38 +255,40 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
   // rounded_scaled_residual (solver.cpp:86-92); when u_f is binary64 the same
   // pass also yields true_residual_norm (the reference recomputes it).
   int ex = 0;
-  double tnorm = 0.0, rhat_ss = 0.0;
+  double tnorm = 0.0, rhat_n = 0.0;  // ||b - A x||_2 and ||rhat||_2 (in the scaled frame), binary64
   // spec: when u_f is binary64, first try the single pass that also rounds
   // rhat with the previous step's exponent (accepted iff the exponent is
   // unchanged -- the usual case; else the two-pass route below reruns).
   const bool can_spec = cfg->u_f == GADI_DOUBLE && !std::getenv("GADI_NO_SPEC");
   auto rsr = [&](bool spec) {
-    if (spec && can_spec && e->resid_spec(h->d_x, ex, cfg->residual_scaling != 0)) {
+    const bool sc = cfg->residual_scaling != 0;
+    if (spec && can_spec && e->resid_spec(h->d_x, ex, sc)) {
+      const int ns_r = sc ? 0 : h->ns;
       read_state(h);
-      if (h->h_st->res_e == ex) {
-        rhat_ss = h->h_st->rhat_ss;
-        tnorm = std::sqrt(h->h_st->res_ss);
+      if (res_norm_ok(h) && h->h_st->res_e == ex) {
+        rhat_n = std::ldexp(std::sqrt(h->h_st->rhat_ss), ns_r);
+        tnorm = res_norm(h);
         return;
       }
     }
-    OuterA::resid(h, h->d_x, h->d_s, cfg->u_f, cfg->residual_scaling != 0);
-    e->scale_round(h->d_s);
+    OuterA::resid_sync(h, h->d_x, h->d_s, cfg->u_f, sc);
+    const int ns_r = sc ? 0 : h->ns;
+    e->scale_round(h->d_s, ns_r);
     read_state(h);
     ex = h->h_st->res_e;
-    rhat_ss = h->h_st->rhat_ss;
+    rhat_n = std::ldexp(std::sqrt(h->h_st->rhat_ss), ns_r);
     if (cfg->u_f != GADI_DOUBLE) {
-      OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
-      read_state(h);
-      tnorm = std::sqrt(h->h_st->res_ss);
+      OuterA::resid_sync(h, h->d_x, nullptr, GADI_DOUBLE, false);
+      tnorm = res_norm(h);
       // keep the scaling exponent of the u_f residual on the device for k_update
       h->h_st->res_e = ex;
       CK(cudaMemcpyAsync(&h->st->res_e, &h->h_st->res_e, sizeof(int), cudaMemcpyHostToDevice, s));
     } else {
-      tnorm = std::sqrt(h->h_st->res_ss);
+      tnorm = res_norm(h);
     }
   };
   rsr(false);
-  const double g0 = std::ldexp(std::sqrt(rhat_ss), ex);
+  const double g0 = std::ldexp(rhat_n, ex);
   double stop_norm = std::ldexp(g0, -ex);
   const double p_rounded = hround((2.0 - cfg->omega) * cfg->alpha, cfg->u_r);
 
@@ -296,7 +298,7 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     const double rres = h->history.back();
     rep->final_rres = rres;
     rep->outer_iters = k;
-    const double gn = std::ldexp(std::sqrt(rhat_ss), ex);
+    const double gn = std::ldexp(rhat_n, ex);
     const bool guard = gn * gn <= g0 * g0 * xi;
     const bool truem = rres * rres <= xi;
     if (guard && truem) { rep->status = GADI_CONVERGED; break; }
@@ -342,9 +344,8 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     h_ms += ms_between(h->evA, h->evB);
     s_ms += ms_between(h->evB, h->evC);
     if (h->h_st->xbad) {
-      OuterA::resid(h, h->d_x, nullptr, GADI_DOUBLE, false);
-      read_state(h);
-      h->history.push_back(std::sqrt(h->h_st->res_ss) / nt0);
+      OuterA::resid_sync(h, h->d_x, nullptr, GADI_DOUBLE, false);
+      h->history.push_back(res_norm(h) / nt0);
       rep->outer_iters = k + 1;
       rep->final_rres = h->history.back();
       rep->status = GADI_OVERFLOW_DETECTED;
@@ -672,9 +673,8 @@ int gadi_cuda_true_residual_norm(gadi_handle* h, const double* x, double* norm_o
   if (!h || !x || !norm_out) throw Err(GADI_E_CONTRACT, "true_residual_norm: null argument");
   CK(cudaSetDevice(h->device));
   CK(cudaMemcpyAsync(h->d_t64, x, h->N * 8, cudaMemcpyHostToDevice, h->stream));
-  OuterA::resid(h, h->d_t64, nullptr, GADI_DOUBLE, false);
-  read_state(h);
-  *norm_out = std::sqrt(h->h_st->res_ss);
+  OuterA::resid_sync(h, h->d_t64, nullptr, GADI_DOUBLE, false);
+  *norm_out = res_norm(h);
   API_END
 }
 

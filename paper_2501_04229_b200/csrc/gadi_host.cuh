@@ -362,6 +362,12 @@ struct gadi_handle {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evA = nullptr, evB = nullptr, evC = nullptr;
   std::vector<cudaEvent_t> ring;
   int64_t launches = 0;
+  // Binary64 norms of the outer residual (norm2_64, kernels.cpp:184-194, scales
+  // by max|s| so the squares neither underflow nor overflow): the passes sum
+  // the squares of s 2^-ns, an exact scaling, and the host returns
+  // 2^ns sqrt(sum). ns stays 0 while |ilogb(max|s|)| <= 400; beyond that the
+  // pass is rerun with ns = ilogb(max|s|) (res_norm_ok).
+  int ns = 0;
   // prepared inner engine
   std::unique_ptr<EngineBase> eng;
   double stop_norm = 1.0;
@@ -457,6 +463,21 @@ inline void read_state(gadi_handle* h) {
 
 inline Red red_of(gadi_handle* h) { return Red{h->d_part0, h->d_part1, h->d_ticket}; }
 
+// 2^-ns for the residual passes; the norms they reduced (after read_state)
+inline double nsc_of(int ns) { return ns == 0 ? 1.0 : std::ldexp(1.0, -ns); }
+inline double res_norm(const gadi_handle* h) { return std::ldexp(std::sqrt(h->h_st->res_ss), h->ns); }
+// After a residual pass and read_state: true when max|s| lies within 2^+-400
+// of the scale the squares were taken at (the sum is then the exact scaled
+// sum); otherwise ns is moved to ilogb(max|s|) and the caller reruns the pass.
+inline bool res_norm_ok(gadi_handle* h) {
+  const double mx = h->h_st->res_max;
+  if (!(mx > 0.0) || !std::isfinite(mx)) return true;
+  const int e = std::ilogb(mx);
+  if (std::abs(e - h->ns) <= 400) return true;
+  h->ns = std::abs(e) <= 400 ? 0 : e;
+  return false;
+}
+
 // A slab vector of the handle: N entries with h->gh ghost entries on each
 // side (zero-filled), the interior pointer returned.
 template <class T>
@@ -510,7 +531,7 @@ struct OuterA {
         auto kern = k_resid_A<decltype(op), PF, V>;
         smem_attr(kern, win.bytes);
         kern<<<g.nblk, g.threads(), win.bytes, h->stream>>>(op, x, h->d_b, s, scaling ? 1 : 0, g, red_of(h), h->st,
-                                                            win.band);
+                                                            win.band, nsc_of(h->ns));
       };
       auto LV = [&](auto pt) {
         if (al) L(pt, VecTag<2>{});
@@ -525,7 +546,7 @@ struct OuterA {
       auto L = [&](auto pt) {
         constexpr int PF = decltype(pt)::v;
         PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x - eo, h->d_b - eo,
-                          s ? s - eo : nullptr, scaling ? 1 : 0};
+                          s ? s - eo : nullptr, scaling ? 1 : 0, nsc_of(h->ns)};
         launch_st25(pol, g25, h->stream, red_of(h), h->st);
       };
       if (uf == GADI_HALF) L(VecTag<P_HALF>{});
@@ -543,6 +564,14 @@ struct OuterA {
     CKL();
     ++h->launches;
     coll<double>(h, EpiResidA{scaling ? 1 : 0});
+  }
+  // resid + read_state, rerun once if max|s| is far from the norm scale
+  static void resid_sync(gadi_handle* h, const double* x, double* s, int uf, bool scaling) {
+    for (int pass = 0; pass < 2; ++pass) {
+      resid(h, x, s, uf, scaling);
+      read_state(h);
+      if (res_norm_ok(h)) return;
+    }
   }
   static void apply(gadi_handle* h, const double* x, double* y) {
     auto go = [&](auto op) {
@@ -615,7 +644,9 @@ struct EngineBase {
   // H/S solves on inner-format device vectors; CG consumes rhs (r in place)
   virtual InnerOut cg(int which, void* rhs, void* x, double target) = 0;
   virtual InnerOut gmres(int which, const void* rhs, void* x, double target) = 0;
-  virtual void scale_round(const double* s) = 0;            // rhat = round(s 2^-e)
+  // rhat = round(s 2^-e); the squares of rhat are taken at 2^-ns_r (0 when
+  // the residual scaling put max|rhat| in [1, 2), else the residual's ns)
+  virtual void scale_round(const double* s, int ns_r) = 0;
   // rhat = round(s 2^-ep) straight from the residual pass (u_f binary64,
   // stencil operators); false: not available for this operator / shape
   virtual bool resid_spec(const double* x, int ep, bool scaling) = 0;
@@ -1143,13 +1174,15 @@ struct Engine final : EngineBase {
   int outer_vec() const {
     return aligned_for(h->N, h->n, h->stencil(), 8) ? 8 : aligned_for(h->N, h->n, h->stencil(), 2) ? 2 : 1;
   }
-  void scale_round(const double* sv) override {
+  void scale_round(const double* sv, int ns_r) override {
     const Red rd = red_of(h);
     const int ov = outer_vec();
     const Geo g = make_geo(h->N, ov);
-    if (ov == 8) k_scale_round<T, 8><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
-    else if (ov == 2) k_scale_round<T, 2><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
-    else k_scale_round<T, 1><<<g.nblk, g.threads(), 0, h->stream>>>(sv, static_cast<T*>(rhat), g, rd, h->st);
+    const double nr = nsc_of(ns_r);
+    T* rh = static_cast<T*>(rhat);
+    if (ov == 8) k_scale_round<T, 8><<<g.nblk, g.threads(), 0, h->stream>>>(sv, rh, g, rd, h->st, nr);
+    else if (ov == 2) k_scale_round<T, 2><<<g.nblk, g.threads(), 0, h->stream>>>(sv, rh, g, rd, h->st, nr);
+    else k_scale_round<T, 1><<<g.nblk, g.threads(), 0, h->stream>>>(sv, rh, g, rd, h->st, nr);
     CKL();
     ++h->launches;
     coll<double>(h, EpiRhat{});
@@ -1172,7 +1205,9 @@ struct Engine final : EngineBase {
                           static_cast<T*>(rhat) - eo,
                           ep,
                           (ep >= -1000 && ep <= 1000) ? std::ldexp(1.0, -ep) : 1.0,
-                          scaling ? 1 : 0};
+                          scaling ? 1 : 0,
+                          nsc_of(h->ns),
+                          nsc_of(scaling ? 0 : h->ns)};
       launch_st25(pol, gs, h->stream, red_of(h), h->st);
       CKL();
       ++h->launches;

@@ -1016,9 +1016,10 @@ struct EpiRhat {  // ||rhat||_2
 template <class Op, int PF, int VEC>
 __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict__ x, const double* __restrict__ b,
                                                  double* __restrict__ sv, int scaling, Geo g, Red rd,
-                                                 DevState* st, int64_t wband = 0) {
+                                                 DevState* st, int64_t wband = 0, double nsc = 1.0) {
   GADI_G;
   double m = 0.0, w0, w1;
+  const bool nscale = nsc != 1.0;  // squares of s 2^-ns (norm2_64's max scaling as an exact power of two)
   auto body = [&](const Seg& s, double& d, const auto& src) {
     double acc[G], xc[G];
     load_seg<double, VEC, G>(b, s, acc);
@@ -1026,7 +1027,8 @@ __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
-      td[i] = __dmul_rn(acc[i], acc[i]);
+      const double av = nscale ? __dmul_rn(acc[i], nsc) : acc[i];
+      td[i] = __dmul_rn(av, av);
       if (GADI_LIVE(i)) m = (acc[i] == acc[i]) ? fmax(m, fabs(acc[i])) : m;
     }
     if (sv) store_seg<double, VEC, G>(sv, s, acc);
@@ -1050,9 +1052,10 @@ __global__ void __launch_bounds__(256) k_resid_A(Op op, const double* __restrict
 // rhat = round_{u_r}(s * 2^-e) (solver.cpp:86-92) and ||rhat||_2.
 template <class T, int VEC>
 __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ sv, T* __restrict__ rhat, Geo g,
-                                                     Red rd, DevState* st) {
+                                                     Red rd, DevState* st, double nsc = 1.0) {
   GADI_G;
   const int e = st->res_e;
+  const bool nscale = nsc != 1.0;
   const double p2 = (e >= -1000 && e <= 1000) ? pow2d(-e) : 1.0;
   double w0, w1;
   seg_run<VEC, false, true>(g, [&](const Seg& s, double&, double& d) {
@@ -1062,7 +1065,8 @@ __global__ void __launch_bounds__(256) k_scale_round(const double* __restrict__ 
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       o[i] = from_dbl<T>(e != 0 ? ldexp_fast(v[i], -e, p2) : v[i]);
-      const double dv = to_dbl(o[i]);
+      double dv = to_dbl(o[i]);
+      if (nscale) dv = __dmul_rn(dv, nsc);
       td[i] = __dmul_rn(dv, dv);
     }
     store_seg<T, VEC, G>(rhat, s, o);

@@ -1118,6 +1118,7 @@ struct PolResidA {
   const double* b;
   double* s;
   int scaling;
+  double nsc;  // 2^-ns: the squares are those of s 2^-ns (1.0: unscaled)
   __device__ bool skip(DevState*) const { return false; }
   __device__ void prepare(DevState*) {}
   __device__ int nin() const { return 1; }
@@ -1130,7 +1131,8 @@ struct PolResidA {
     double td[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      td[e] = __dmul_rn(acc[e], acc[e]);
+      const double av = nsc != 1.0 ? __dmul_rn(acc[e], nsc) : acc[e];
+      td[e] = __dmul_rn(av, av);
       m = (acc[e] == acc[e]) ? fmax(m, fabs(acc[e])) : m;
     }
     if (s) st_vec<double, 2>(s, e0, acc);
@@ -1162,6 +1164,7 @@ struct PolResidSpec {
   int ep;
   double p2;  // 2^-ep
   int scaling;
+  double nsc, nsc_r;  // 2^-ns for the squares of s, and for those of rhat (1.0: unscaled)
   __device__ bool skip(DevState*) const { return false; }
   __device__ void prepare(DevState*) {}
   __device__ int nin() const { return 1; }
@@ -1175,10 +1178,12 @@ struct PolResidSpec {
     TR o[2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      td[e] = __dmul_rn(acc[e], acc[e]);
+      const double av = nsc != 1.0 ? __dmul_rn(acc[e], nsc) : acc[e];
+      td[e] = __dmul_rn(av, av);
       m = (acc[e] == acc[e]) ? fmax(m, fabs(acc[e])) : m;
       o[e] = from_dbl<TR>(ep != 0 ? ldexp_fast(acc[e], -ep, p2) : acc[e]);
-      const double dv = to_dbl(o[e]);
+      double dv = to_dbl(o[e]);
+      if (nsc_r != 1.0) dv = __dmul_rn(dv, nsc_r);
       tc[e] = __dmul_rn(dv, dv);
     }
     st_vec<TR, 2>(rhat, e0, o);
