@@ -134,46 +134,74 @@ def c1_cpu_full(wl):
                        f"status {rep.status}, {rep.outer_iters} outer, measured (not projected)")}
 
 
-def cpu_reference_sample(wl, threads_note=True):
+def cpu_reference_sample(wl, full=False, outer=None):
+    """Time the reference's own CPU implementation (oracle/_ref, compiled from
+    the reference sources; else the oracle port) on a bounded sample of the
+    workload and project it to the workload's size.
+
+    The sample solves the same family at a size the host finishes in bounded
+    time -- the stencil at n_s with the workload's r = beta h / 2, the band CSR
+    at N_s rows with the same generator -- in the reference's FP32 Krylov mode
+    (its FP16 Krylov overflows in the dots at these sizes) with the
+    workload's alpha / eps / max_inner. hss_split runs once; gadi_ir_solve is
+    then capped at k1 and at k2 outer steps and the two times are subtracted,
+    so the one-time setup (CSR copy, split, regularize/prepare, the initial
+    residuals) is counted once, not per step:
+
+        per_outer_s = (t(k2) - t(k1)) / (k2 - k1)          at N_s
+        setup_s     = t_split + t(k1) - k1 per_outer_s      at N_s
+        value       = (N / N_s) (setup_s + outer_iters per_outer_s)
+
+    outer_iters is the device solve's count on the workload (the same
+    precision class converges within a few steps of it, tests/
+    test_gpu_baseline_shapes.py). full=True (the reference arm) samples at the
+    largest size that fits the host (n_s = 256, N_s = 2^21); the cpu_baseline
+    leg of the default run uses n_s = 128 / N_s = 2^19 (about 30 s)."""
     if wl_key(wl) == "c1":
         return c1_cpu_full(wl)
-    """Time the reference's own CPU implementation (oracle/_ref, built from the
-    reference sources; else the oracle restatement) on a bounded sample: one
-    GADI-IR outer step (CG on H + GMRES on S + residuals, same inner budget and
-    precision class where the reference can run it) at n=64 with the workload's
-    r = beta*h/2, then project per element and per outer step to the workload
-    size and the device's outer-iteration count."""
+    import psutil
     from oracle import CG, Config, Oracle, Reference
     o = Oracle()
     use_ref = Reference.available()
-    R = Reference() if use_ref else o
-    if wl.get("kind") == "band":  # the same generator at N = 2^16 (SURVEY §8(d): C4 cannot be split in host RAM)
-        ns, N_s, N_t = None, 1 << 16, wl["N"]
+    big = full and psutil.virtual_memory().available > 48 * 2 ** 30
+    if wl.get("kind") == "band":  # SURVEY §8(d): C4 cannot be split in host RAM
+        ns, N_s, N_t = None, (1 << 21) if big else (1 << 19), wl["N"]
         A = o.band(N_s, wl["k_off"], wl["band"], wl["mseed"])
         r = 0.0
     else:
-        ns = 64
+        ns = 256 if big else 128
         N_s, N_t = ns ** 3, wl["n"] ** 3
         r = wl["beta"] / (2.0 * (wl["n"] + 1.0))
         A = o.convdiff(ns, 6.0, -1.0 - r, -1.0 + r)
     _, b = o.make_rhs(A, wl["seed"], wl["lo"], wl["hi"])
-    # the reference's FP16 Krylov accumulates dots in binary16 and breaks on
-    # overflow at these sizes (SURVEY §0 finding 1); time its FP32 path
-    ur = 1
-    cfg = Config.make(alpha=wl["alpha"], xi=1e-20, u_r=ur, method=CG, tol_epsilon=wl["eps"],
-                      max_inner_iters=wl["max_inner"], restart=wl["restart"], max_outer_iters=1)
-    t = time.perf_counter()
-    R.solve(A, b, cfg)
-    dt = time.perf_counter() - t
-    per_outer_t = dt * N_t / N_s
-    proj = per_outer_t * OUTER_ITERS[wl_key(wl)]
+    k1, k2 = (1, 2) if big else (1, 3)
+    cfg = Config.make(alpha=wl["alpha"], xi=1e-20, u_r=1, method=CG, tol_epsilon=wl["eps"],
+                      max_inner_iters=wl["max_inner"], restart=wl["restart"])
+    if use_ref:
+        t_split, t1, t2, o1, o2 = Reference().solve_steps_timed(A, b, cfg, k1, k2)
+    else:  # the port has no separate split: both capped solves carry it
+        ts = []
+        for k in (k1, k2):
+            cfg.max_outer_iters = k
+            t = time.perf_counter()
+            _, rep, _ = o.solve(A, b, cfg)
+            ts.append(time.perf_counter() - t)
+        t_split, t1, t2, o1, o2 = 0.0, ts[0], ts[1], k1, k2
+    per_outer = (t2 - t1) / max(1, o2 - o1)
+    setup = t_split + t1 - o1 * per_outer
+    scale = N_t / N_s
+    outer = outer or OUTER_ITERS[wl_key(wl)]
+    proj = scale * (setup + outer * per_outer)
     what = (f"band CSR N={N_s}" if ns is None else f"n={ns} (N={N_s}) with r={r:.5f}")
     return {
         "value": proj, "unit": "s", "cores": 1, "kind": "reference" if use_ref else "port",
-        "sample": (f"1 GADI-IR outer step incl. setup (fp32 CG/GMRES, max_inner={wl['max_inner']}) on "
-                   f"{what}: {dt:.2f} s; projected x{N_t // N_s} elements and "
-                   f"x{OUTER_ITERS[wl_key(wl)]} outer steps (projected, single-threaded: the "
-                   f"reference has no intra-solve parallelism)"),
+        "setup_s": setup, "per_outer_s": per_outer, "sample_rows": N_s, "scale": scale, "outer_iters": outer,
+        "ns_per_row_per_outer": per_outer / N_s * 1e9,
+        "formula": "value = scale * (setup_s + outer_iters * per_outer_s); per_outer_s = (t(k2)-t(k1))/(k2-k1)",
+        "sample": (f"reference gadi_ir_solve (fp32 CG/GMRES, max_inner={wl['max_inner']}) on {what}: hss_split "
+                   f"{t_split:.2f} s, solve capped at {o1} outer {t1:.2f} s, at {o2} outer {t2:.2f} s -> "
+                   f"{per_outer:.3f} s per outer step, {setup:.2f} s setup; projected x{scale:g} rows and "
+                   f"{outer} outer steps (single-threaded: the reference has no intra-solve parallelism)"),
     }
 
 
@@ -275,6 +303,15 @@ def main():
     ap.add_argument("--workload", default="c3", choices=list(WORKLOADS) + ["c5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched bare: start one rank per GPU ourselves (the launch the driver uses)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -303,7 +340,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_reference_sample(wl)
+        cb = cpu_reference_sample(wl, full=True)
         print(json.dumps({"impl": "reference", "metric": metric, "value": cb["value"], "unit": "s",
                           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                           "higher_is_better": False, "dtype": "f64", "data": "synthetic",
@@ -423,7 +460,7 @@ def main():
                   "wall_s_per_step": wall / args.steps},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_reference_sample(wl)
+        out["cpu_baseline"] = cpu_reference_sample(wl, outer=reps[0].outer_iters)
     if rank == 0:
         print(json.dumps(out), flush=True)
     sysx.close()

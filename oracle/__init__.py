@@ -347,6 +347,8 @@ class Reference:
         L.ref_reference_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_double, C.c_double,
                                           C.c_double, C.c_int, _f64p, C.POINTER(C.c_int),
                                           C.POINTER(C.c_int)]
+        L.ref_solve_steps_timed.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.POINTER(Config), C.c_int,
+                                            C.c_int, _f64p, C.POINTER(C.c_int)]
         L.ref_gpr.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_double, _i64p, C.c_int, _f64p, _f64p,
                               _f64p]
 
@@ -469,6 +471,17 @@ class Reference:
         if rc != 0:
             raise ValueError(f"ref_solve rc={rc}")
         return x, rep, hist[: min(rep.history_len, cap)].copy()
+
+    def solve_steps_timed(self, A, b, cfg, k1, k2):
+        """(split_s, solve_k1_s, solve_k2_s, outer_k1, outer_k2): the split once, then
+        gadi_ir_solve capped at k1 and at k2 outer steps (bench.py's CPU baseline)."""
+        b = np.ascontiguousarray(b, np.float64)
+        t = np.zeros(3)
+        it = (C.c_int * 2)()
+        rc = self.L.ref_solve_steps_timed(*self._a(A), _p(b), C.byref(cfg), k1, k2, _p(t), it)
+        if rc != 0:
+            raise ValueError(f"ref_solve_steps_timed rc={rc}")
+        return t[0], t[1], t[2], it[0], it[1]
 
     def gpr(self, sizes, alphas, qsizes, sigma_n2=None):
         sizes = np.ascontiguousarray(sizes, np.int64)

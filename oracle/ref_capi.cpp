@@ -6,6 +6,7 @@
 // Each entry point forwards to the reference symbol named in its comment.
 #include <cstdint>
 #include <cstring>
+#include <ctime>
 #include <exception>
 #include <vector>
 
@@ -280,6 +281,40 @@ int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, 
     return GADI_E_PARAM;
   } catch (const ContractViolation&) {
     return GADI_E_CONTRACT;
+  } catch (...) {
+    return -99;
+  }
+}
+
+// bench.py's CPU baseline: hss_split once (splitting.cpp:12-20), then the
+// reference's gadi_ir_solve capped at k1 and at k2 outer steps, each timed
+// with the wall clock. t[0] = split, t[1] = solve capped at k1, t[2] = at k2:
+// (t[2] - t[1]) / (k2 - k1) is the cost of one outer step without any setup
+// (CSR copy, split, regularize/prepare and the initial residuals are in t[0]
+// and in both solves alike).
+int ref_solve_steps_timed(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b,
+                          const gadi_config* cfg, int k1, int k2, double* t, int* outer) {
+  try {
+    auto now = [] {
+      timespec ts;
+      clock_gettime(CLOCK_MONOTONIC, &ts);
+      return ts.tv_sec + 1e-9 * ts.tv_nsec;
+    };
+    SparseMatrix A = csr(n, rp, ci, v);
+    const Vector bv = vec(b, n);
+    double t0 = now();
+    Splitting s = hss_split(A);
+    t[0] = now() - t0;
+    GadiConfig c = to_cfg(cfg);
+    const int ks[2] = {k1, k2};
+    for (int i = 0; i < 2; ++i) {
+      c.max_outer_iters = ks[i];
+      t0 = now();
+      auto res = gadi_ir_solve(A, bv, s, c, nullptr);
+      t[1 + i] = now() - t0;
+      outer[i] = res.report.outer_iters;
+    }
+    return 0;
   } catch (...) {
     return -99;
   }
