@@ -19,8 +19,9 @@
  *     solver.hpp:17-38, inner_solver.hpp:20-25
  *   SolveReport / SolveStatus                   gadi_report / gadi_status
  *     solver.hpp:44-64
- *   hss_split + regularize                      gadi_cuda_create (split is implied:
- *     splitting.hpp:22-47                         HSS, built on the device)
+ *   hss_split + regularize                      gadi_cuda_create (HSS, built on the
+ *     splitting.hpp:22-47                         device) / gadi_cuda_prepare
+ *   explicit_splitting  splitting.hpp:25-26     gadi_cuda_set_split(EXPLICIT, M, N)
  *   build_convdiff3d  problems.hpp:16-42        GADI_PROBLEM_STENCIL7 (matrix free)
  *   fit / predict_alpha  gpr.hpp:72-87          gadi_gpr_fit / gadi_gpr_predict
  *
@@ -78,7 +79,7 @@ typedef enum {
   GADI_OK = 0,
   GADI_E_CONTRACT = -1,    /* ContractViolation: shapes, null pointers      */
   GADI_E_PARAM = -2,       /* ParameterError: alpha, omega, precision order */
-  GADI_E_UNSUPPORTED = -3, /* LU_DIRECT inner, unsupported layout            */
+  GADI_E_UNSUPPORTED = -3, /* a shape / layout this build has no kernel for   */
   GADI_E_FIT = -4,         /* FitError (gpr.hpp:83)                           */
   GADI_E_CUDA = -5,
   GADI_E_NCCL = -6,
@@ -181,6 +182,26 @@ int32_t gadi_abi_version(void);
  * constructor (solver.cpp:185-186) + hss_split. */
 int gadi_cuda_create(const gadi_problem_desc* desc, const gadi_device_opts* opts, gadi_handle** out);
 int gadi_cuda_destroy(gadi_handle* h);
+
+/* SplitKind, splitting.hpp:12 (Hss, Explicit; SylvesterAB is gadi_sylv_*). */
+typedef enum { GADI_SPLIT_HSS = 0, GADI_SPLIT_EXPLICIT = 1 } gadi_split_kind;
+/* A square CSR in the reference's SparseMatrix layout (sparse.hpp:17-65), host pointers. */
+typedef struct {
+  int64_t n_rows, n_cols, nnz;
+  const int64_t* row_ptr;
+  const int64_t* col_idx;
+  const double* values;
+} gadi_csr_desc;
+/* The splitting A = M + N the solves use (the `split` argument of
+ * gadi_ir_solve, solver.hpp:97-98). A new handle has hss_split(A).
+ * EXPLICIT = explicit_splitting(A, M, N) (splitting.cpp:22-35) on a
+ * GADI_PROBLEM_CSR handle: GADI_E_CONTRACT on a shape mismatch or when an
+ * entry of M + N differs from A's by more than one ulp ("M + N != A"); then
+ * prepare forms H = shift_diagonal(M, alpha), S = shift_diagonal(N, alpha)
+ * (splitting.cpp:37-47) on the device, each on its own pattern. M and N are
+ * copied. HSS (M, N ignored) returns to the HSS split. Drops the prepared
+ * inner engine. */
+int gadi_cuda_set_split(gadi_handle* h, int32_t kind, const gadi_csr_desc* M, const gadi_csr_desc* N);
 int gadi_cuda_dim(const gadi_handle* h, int64_t* n);
 
 /* ---- GadiSystem mirror (solver.hpp:74-89); host vectors of length dim, ----

@@ -157,6 +157,8 @@ class Oracle:
         L.orc_lu_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, C.c_int, _f64p]
         L.orc_solve.argtypes = [C.POINTER(_OrcCsr), _f64p, _f64p, C.POINTER(Config), _f64p, _f64p,
                                 C.c_int, C.POINTER(Report)]
+        L.orc_solve_split.argtypes = [C.POINTER(_OrcCsr), C.POINTER(_OrcCsr), C.POINTER(_OrcCsr), _f64p, _f64p,
+                                      C.POINTER(Config), _f64p, _f64p, C.c_int, C.POINTER(Report)]
         L.orc_gpr.argtypes = [_f64p, _f64p, C.c_int, C.POINTER(GprOpts), _f64p, C.c_int, _f64p,
                               _f64p, _f64p]
 
@@ -275,15 +277,21 @@ class Oracle:
         st = self.L.orc_lu_solve(C.byref(oc), _p(rhs), fmt, _p(x))
         return x, st
 
-    def solve(self, A: CSR, b, cfg: Config, x0=None, cap=100000):
+    def solve(self, A: CSR, b, cfg: Config, x0=None, cap=100000, split=None):
+        """split = (M, N): explicit_splitting(A, M, N) (splitting.cpp:22-35); None: hss_split."""
         b = np.ascontiguousarray(b, np.float64)
         x = np.zeros(A.n)
         hist = np.zeros(cap)
         rep = Report()
         oc = _oc(A)
         x0a = None if x0 is None else np.ascontiguousarray(x0, np.float64)
-        rc = self.L.orc_solve(C.byref(oc), _p(b), _p(x0a), C.byref(cfg), _p(x), _p(hist), cap,
-                              C.byref(rep))
+        if split is None:
+            rc = self.L.orc_solve(C.byref(oc), _p(b), _p(x0a), C.byref(cfg), _p(x), _p(hist), cap,
+                                  C.byref(rep))
+        else:
+            om, on = _oc(split[0]), _oc(split[1])
+            rc = self.L.orc_solve_split(C.byref(oc), C.byref(om), C.byref(on), _p(b), _p(x0a), C.byref(cfg),
+                                        _p(x), _p(hist), cap, C.byref(rep))
         if rc != 0:
             raise ValueError(f"orc_solve rc={rc}")
         return x, rep, hist[: min(rep.history_len, cap)].copy()
@@ -347,6 +355,8 @@ class Reference:
         L.ref_reference_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.c_double, C.c_double,
                                           C.c_double, C.c_int, _f64p, C.POINTER(C.c_int),
                                           C.POINTER(C.c_int)]
+        L.ref_solve_split.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _i64p, _i64p, _f64p, _i64p, _i64p, _f64p,
+                                      _f64p, C.POINTER(Config), _f64p, _f64p, C.c_int, C.POINTER(Report)]
         L.ref_solve_steps_timed.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p, C.POINTER(Config), C.c_int,
                                             C.c_int, _f64p, C.POINTER(C.c_int)]
         L.ref_gpr.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_double, _i64p, C.c_int, _f64p, _f64p,
@@ -470,6 +480,18 @@ class Reference:
                               C.byref(rep))
         if rc != 0:
             raise ValueError(f"ref_solve rc={rc}")
+        return x, rep, hist[: min(rep.history_len, cap)].copy()
+
+    def solve_split(self, A, M, N, b, cfg, cap=100000):
+        """gadi_ir_solve(A, b, explicit_splitting(A, M, N), cfg)."""
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(A.n)
+        hist = np.zeros(cap)
+        rep = Report()
+        rc = self.L.ref_solve_split(*self._a(A), *self._a(M)[1:], *self._a(N)[1:], _p(b), C.byref(cfg), _p(x),
+                                    _p(hist), cap, C.byref(rep))
+        if rc != 0:
+            raise ValueError(rc)
         return x, rep, hist[: min(rep.history_len, cap)].copy()
 
     def solve_steps_timed(self, A, b, cfg, k1, k2):

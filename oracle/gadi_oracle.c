@@ -305,6 +305,61 @@ int64_t orc_regularize(const orc_csr* A, double alpha, int64_t* rpH, int64_t* ci
   return c;
 }
 
+/* shift_diagonal (sparse.cpp:180-183) of a general CSR M: add(1.0, M, alpha, I),
+ * the pattern of M with the diagonal inserted where M has none (value alpha
+ * there, 1.0*M_ii + alpha elsewhere). rp == NULL: count only. */
+int64_t orc_shift_diagonal(const orc_csr* M, double alpha, int64_t* rp, int64_t* ci, double* v) {
+  int64_t c = 0;
+  if (rp) rp[0] = 0;
+  for (int64_t i = 0; i < M->n; ++i) {
+    int done = 0;
+    for (int64_t k = M->rp[i]; k < M->rp[i + 1] || !done;) {
+      const int64_t col = k < M->rp[i + 1] ? M->ci[k] : INT64_MAX;
+      if (!done && i <= col) {
+        if (rp) {
+          ci[c] = i;
+          v[c] = col == i ? 1.0 * M->v[k] + alpha : alpha;
+        }
+        if (col == i) ++k;
+        done = 1;
+      } else {
+        if (rp) {
+          ci[c] = col;
+          v[c] = 1.0 * M->v[k];
+        }
+        ++k;
+      }
+      ++c;
+    }
+    if (rp) rp[i + 1] = c;
+  }
+  return c;
+}
+
+/* explicit_splitting's check (splitting.cpp:22-35): every entry of
+ * add(1.0, M, 1.0, N) equals A's entry there (0 where A has none) within one
+ * ulp of |a|. Returns 0 or GADI_E_CONTRACT. */
+int orc_explicit_check(const orc_csr* A, const orc_csr* M, const orc_csr* N) {
+  if (M->n != A->n || N->n != A->n) return GADI_E_CONTRACT;
+  for (int64_t i = 0; i < A->n; ++i) {
+    int64_t m = M->rp[i], me = M->rp[i + 1], q = N->rp[i], qe = N->rp[i + 1], a = A->rp[i], ae = A->rp[i + 1];
+    while (m < me || q < qe) {
+      const int64_t cm = m < me ? M->ci[m] : INT64_MAX, cn = q < qe ? N->ci[q] : INT64_MAX;
+      const int64_t col = cm < cn ? cm : cn;
+      double sum = 0.0;
+      if (cm == col && cn == col) sum = 1.0 * M->v[m] + 1.0 * N->v[q];
+      else if (cm == col) sum = 1.0 * M->v[m];
+      else sum = 1.0 * N->v[q];
+      if (cm == col) ++m;
+      if (cn == col) ++q;
+      while (a < ae && A->ci[a] < col) ++a;
+      const double av = (a < ae && A->ci[a] == col) ? A->v[a] : 0.0;
+      if (fabs(sum - av) > fabs(av) * 2.220446049250313e-16) return GADI_E_CONTRACT;
+    }
+  }
+  return GADI_OK;
+}
+
 /* -------------------------------------------------------------------- krylov
  * The Krylov solvers take a storage format `fmt` (u_r: every vector entry
  * and matrix value is a u_r number) and an arithmetic format `af`. af == fmt
@@ -635,10 +690,13 @@ int orc_lu_solve(const orc_csr* M, const double* rhs, int fmt, double* x) {
 #undef AT
 
 /* -------------------------------------------------------------------- solver */
-/* run_gadi_ir (solver.cpp:57-179) over CsrGadiSystem (solver.cpp:183-246). */
-int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
-              double* hist, int cap, gadi_report* rep) {
+/* run_gadi_ir (solver.cpp:57-179) over CsrGadiSystem (solver.cpp:183-246).
+ * Ms/Ns NULL: the HSS split of A (hss_split); else explicit_splitting(A, Ms, Ns)
+ * (splitting.cpp:22-35), H = shift_diagonal(Ms), S = shift_diagonal(Ns). */
+int orc_solve_split(const orc_csr* A, const orc_csr* Ms, const orc_csr* Ns, const double* b, const double* x0,
+                    const gadi_config* cfg, double* x, double* hist, int cap, gadi_report* rep) {
   const int64_t n = A->n;
+  if (Ms && orc_explicit_check(A, Ms, Ns) != GADI_OK) return GADI_E_CONTRACT;
   /* validate, solver.cpp:33-40 */
   if (!(cfg->alpha > 0.0)) return GADI_E_PARAM;
   if (!(cfg->omega >= 0.0 && cfg->omega < 2.0)) return GADI_E_PARAM;
@@ -665,11 +723,19 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
   double* z = (double*)malloc((size_t)n * 8);
   double* pz = (double*)malloc((size_t)n * 8);
   double* yv = (double*)malloc((size_t)n * 8);
-  int64_t nnzH = orc_regularize(A, cfg->alpha, NULL, NULL, NULL, NULL);
+  int64_t nnzH = Ms ? orc_shift_diagonal(Ms, cfg->alpha, NULL, NULL, NULL)
+                    : orc_regularize(A, cfg->alpha, NULL, NULL, NULL, NULL);
   orc_csr H = {n, (int64_t*)malloc((size_t)(n + 1) * 8), (int64_t*)malloc((size_t)nnzH * 8 + 8),
                (double*)malloc((size_t)nnzH * 8 + 8)};
   orc_csr S = H;
-  S.v = (double*)malloc((size_t)nnzH * 8 + 8);
+  if (Ms) {
+    const int64_t nnzS = orc_shift_diagonal(Ns, cfg->alpha, NULL, NULL, NULL);
+    S.rp = (int64_t*)malloc((size_t)(n + 1) * 8);
+    S.ci = (int64_t*)malloc((size_t)nnzS * 8 + 8);
+    S.v = (double*)malloc((size_t)nnzS * 8 + 8);
+  } else {
+    S.v = (double*)malloc((size_t)nnzH * 8 + 8);
+  }
 
   for (int64_t i = 0; i < n; ++i) x[i] = R(x0 ? x0[i] : (cfg->ones_start ? 1.0 : 0.0), u_p);
   double last = 1.0;
@@ -686,7 +752,12 @@ int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_co
     rep->final_rres = 0.0;
     goto done;
   }
-  orc_regularize(A, cfg->alpha, H.rp, H.ci, H.v, S.v); /* prepare, solver.cpp:199-208 */
+  if (Ms) { /* prepare, solver.cpp:199-208 */
+    orc_shift_diagonal(Ms, cfg->alpha, H.rp, H.ci, H.v);
+    orc_shift_diagonal(Ns, cfg->alpha, S.rp, S.ci, S.v);
+  } else {
+    orc_regularize(A, cfg->alpha, H.rp, H.ci, H.v, S.v);
+  }
   const int lu = cfg->inner.method == GADI_INNER_LU_DIRECT;
   orc_blu fH, fS;
   memset(&fH, 0, sizeof(fH));
@@ -796,6 +867,10 @@ done:
   free(z);
   free(pz);
   free(yv);
+  if (Ms) {
+    free(S.rp);
+    free(S.ci);
+  }
   free(H.rp);
   free(H.ci);
   free(H.v);
@@ -804,6 +879,11 @@ done:
 #undef PUSH_HIST
 #undef TRUE_NORM
 #undef RSR
+}
+
+int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
+              double* hist, int cap, gadi_report* rep) {
+  return orc_solve_split(A, NULL, NULL, b, x0, cfg, x, hist, cap, rep);
 }
 
 

@@ -89,6 +89,10 @@ void orc_blu_free(orc_blu* f);
 int orc_lu_solve(const orc_csr* M, const double* rhs, int fmt, double* x);
 
 /* ---- solver.cpp:57-179 + 250-258 (gadi_ir_solve on a CSR system) ---- */
+int64_t orc_shift_diagonal(const orc_csr* M, double alpha, int64_t* rp, int64_t* ci, double* v);
+int orc_explicit_check(const orc_csr* A, const orc_csr* M, const orc_csr* N);
+int orc_solve_split(const orc_csr* A, const orc_csr* Ms, const orc_csr* Ns, const double* b, const double* x0,
+                    const gadi_config* cfg, double* x, double* hist, int cap, gadi_report* rep);
 int orc_solve(const orc_csr* A, const double* b, const double* x0, const gadi_config* cfg, double* x,
               double* hist, int cap, gadi_report* rep);
 

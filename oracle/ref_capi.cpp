@@ -286,6 +286,33 @@ int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, 
   }
 }
 
+// gadi_ir_solve with explicit_splitting(A, M, N) (splitting.cpp:22-35)
+int ref_solve_split(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const int64_t* mrp,
+                    const int64_t* mci, const double* mv, const int64_t* nrp, const int64_t* nci, const double* nv,
+                    const double* b, const gadi_config* cfg, double* x, double* hist, int cap, gadi_report* rep) {
+  try {
+    SparseMatrix A = csr(n, rp, ci, v);
+    Splitting s = explicit_splitting(A, csr(n, mrp, mci, mv), csr(n, nrp, nci, nv));
+    auto res = gadi_ir_solve(A, vec(b, n), s, to_cfg(cfg), nullptr);
+    out(res.x, x);
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = static_cast<int>(res.report.status);
+    rep->outer_iters = res.report.outer_iters;
+    rep->final_rres = res.report.final_rres;
+    rep->inner_iter_totals = res.report.inner_iter_totals;
+    rep->inner_stagnations = res.report.inner_stagnations;
+    rep->history_len = static_cast<int>(res.report.rel_residual_history.size());
+    for (int i = 0; i < rep->history_len && i < cap; ++i) hist[i] = res.report.rel_residual_history[i];
+    return 0;
+  } catch (const ParameterError&) {
+    return GADI_E_PARAM;
+  } catch (const ContractViolation&) {
+    return GADI_E_CONTRACT;
+  } catch (...) {
+    return -99;
+  }
+}
+
 // bench.py's CPU baseline: hss_split once (splitting.cpp:12-20), then the
 // reference's gadi_ir_solve capped at k1 and at k2 outer steps, each timed
 // with the wall clock. t[0] = split, t[1] = solve capped at k1, t[2] = at k2:

@@ -144,6 +144,11 @@ class _Problem(C.Structure):
                 ("seed", C.c_uint64)]
 
 
+class _CsrDesc(C.Structure):  # gadi_csr_desc
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64), ("row_ptr", _i64p),
+                ("col_idx", _i64p), ("values", _f64p)]
+
+
 class _DevOpts(C.Structure):
     _fields_ = [("device", C.c_int32)]
 
@@ -183,6 +188,7 @@ def lib():
     L.gadi_cuda_create.argtypes = [C.POINTER(_Problem), C.POINTER(_DevOpts), C.POINTER(C.c_void_p)]
     L.gadi_cuda_destroy.argtypes = [C.c_void_p]
     L.gadi_cuda_dim.argtypes = [C.c_void_p, _i64p]
+    L.gadi_cuda_set_split.argtypes = [C.c_void_p, C.c_int32, C.POINTER(_CsrDesc), C.POINTER(_CsrDesc)]
     L.gadi_cuda_set_rhs.argtypes = [C.c_void_p, _f64p]
     L.gadi_cuda_residual_uf.argtypes = [C.c_void_p, C.c_int32, _f64p, _f64p]
     L.gadi_cuda_true_residual_norm.argtypes = [C.c_void_p, _f64p, _f64p]
@@ -381,14 +387,27 @@ def build_convdiff3d(n: int, r: Optional[float] = None, beta: Optional[float] = 
 
 
 @dataclass
-class Splitting:  # splitting.hpp:17-22; HSS split built on the device
+class Splitting:  # splitting.hpp:17-22; the HSS split is built on the device
     A: object
-    kind: str = "hss"
+    kind: str = "hss"            # SplitKind: "hss" | "explicit"
+    M: Optional["SparseMatrix"] = None
+    N: Optional["SparseMatrix"] = None
 
 
 def hss_split(A) -> Splitting:
     """M = (A+A^T)/2, N = (A-A^T)/2 (splitting.cpp:12-20); the device builds it."""
     return Splitting(A, "hss")
+
+
+def explicit_splitting(A, M: "SparseMatrix", N: "SparseMatrix") -> Splitting:
+    """User-supplied splitting A = M + N (splitting.cpp:22-35). Shapes are
+    checked here; the one-ulp M + N = A check runs in gadi_cuda_set_split when
+    the split is bound to a handle (ContractViolation "M + N != A")."""
+    if not isinstance(A, SparseMatrix):
+        raise UnsupportedError("explicit_splitting: A must be a SparseMatrix (CSR)")
+    if (M.n_rows != A.n_rows or N.n_rows != A.n_rows or M.n_cols != A.n_cols or N.n_cols != A.n_cols):
+        raise ContractViolation("explicit_splitting: shape mismatch")
+    return Splitting(A, "explicit", M, N)
 
 
 # ---------------------------------------------------------------- GadiSystem mirror
@@ -400,7 +419,7 @@ class CudaGadiSystem:
     numpy arrays like the reference's Vector.
     """
 
-    def __init__(self, A, b=None, device: int = 0):
+    def __init__(self, A, b=None, device: int = 0, split: Optional[Splitting] = None):
         L = lib()
         self._h = C.c_void_p()
         self._A = A
@@ -409,8 +428,27 @@ class CudaGadiSystem:
         n = C.c_int64()
         L.gadi_cuda_dim(self._h, C.byref(n))
         self.n = n.value
+        if split is not None:
+            try:
+                self.set_split(split)
+            except Exception:
+                self.close()
+                raise
         if b is not None:
             self.set_rhs(b)
+
+    def set_split(self, split: Splitting):
+        """Bind the splitting the solves use (the `split` argument of
+        gadi_ir_solve, solver.hpp:97-98): hss_split(A) or explicit_splitting(A, M, N)."""
+        if split.A is not self._A:
+            raise ContractViolation("set_split: split does not belong to A")
+        if split.kind == "hss":
+            _check(lib().gadi_cuda_set_split(self._h, 0, None, None))
+            return
+        d = []
+        for m in (split.M, split.N):
+            d.append(_CsrDesc(m.n_rows, m.n_cols, m.nnz(), _p(m.row_ptr, _i64p), _p(m.col_idx, _i64p), _p(m.values)))
+        _check(lib().gadi_cuda_set_split(self._h, 1, C.byref(d[0]), C.byref(d[1])))
 
     def close(self):
         if self._h:
@@ -589,7 +627,7 @@ def gadi_ir_solve(A, b, split: Splitting, cfg: GadiConfig, x0=None, device: int 
         raise ContractViolation("gadi_ir_solve: split does not belong to A")
     if len(b) != A.n_rows:
         raise ContractViolation("gadi_ir_solve: dimension mismatch")  # solver.cpp:252-253
-    sys_ = CudaGadiSystem(A, device=device)
+    sys_ = CudaGadiSystem(A, device=device, split=split if split.kind != "hss" else None)
     try:
         return sys_.solve(b, cfg, x0)
     finally:

@@ -622,6 +622,9 @@ int gadi_cuda_destroy(gadi_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   h->eng.reset();
+  for (auto& p : h->ex)
+    for (void* q : {(void*)p.rp, (void*)p.ci, (void*)p.v, (void*)p.dpos, (void*)p.din})
+      if (q) cudaFree(q);
   for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_urp, (void*)h->d_uci,
                   (void*)h->d_mv, (void*)h->d_nv, (void*)h->d_dpos, (void*)h->d_din, (void*)h->st,
                   (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_ticket})
@@ -637,6 +640,120 @@ int gadi_cuda_destroy(gadi_handle* h) {
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return GADI_OK;
+}
+
+// explicit_splitting(A, M, N) (splitting.cpp:22-35): shapes, the M + N = A
+// check on the entries of add(1.0, M, 1.0, N) (A's entry there, 0 where A has
+// none, within one ulp of |a|), then M and N go to the device on
+// shift_diagonal's pattern (their own plus the diagonal, sparse.cpp:180-183);
+// the alpha shift itself happens on the device when prepare fills the operator
+// images (k_sell_fill / k_band_csr). HSS drops an explicit split again.
+int gadi_cuda_set_split(gadi_handle* h, int32_t kind, const gadi_csr_desc* M, const gadi_csr_desc* Nn) {
+  API_BEGIN
+  if (!h) throw Err(GADI_E_CONTRACT, "set_split: null handle");
+  if (kind != GADI_SPLIT_HSS && kind != GADI_SPLIT_EXPLICIT) throw Err(GADI_E_PARAM, "set_split: unknown split kind");
+  if (h->sharded()) throw Err(GADI_E_UNSUPPORTED, "set_split: not on a shard");
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->stream));
+  h->eng.reset();  // operators of the previous split
+  auto drop = [&]() {
+    for (auto& p : h->ex) {
+      for (void* q : {(void*)p.rp, (void*)p.ci, (void*)p.v, (void*)p.dpos, (void*)p.din})
+        if (q) cudaFree(q);
+      p = gadi_handle::SplitPart{};
+    }
+    h->explicit_split = false;
+  };
+  drop();
+  if (kind == GADI_SPLIT_HSS) return GADI_OK;
+  if (h->stencil() || h->kind == GADI_PROBLEM_BAND)
+    throw Err(GADI_E_UNSUPPORTED, "set_split: explicit splittings need a GADI_PROBLEM_CSR handle");
+  if (!M || !Nn) throw Err(GADI_E_CONTRACT, "explicit_splitting: null argument");
+  const int64_t n = h->N;
+  for (const gadi_csr_desc* m : {M, Nn}) {
+    if (m->n_rows != n || m->n_cols != n) throw Err(GADI_E_CONTRACT, "explicit_splitting: shape mismatch");
+    if (!m->row_ptr || (m->nnz > 0 && (!m->col_idx || !m->values)) || m->row_ptr[0] != 0 || m->row_ptr[n] != m->nnz)
+      throw Err(GADI_E_CONTRACT, "explicit_splitting: bad CSR arrays");
+    for (int64_t i = 0; i < n; ++i) {  // the SparseMatrix invariants, sparse.cpp:19-34
+      if (m->row_ptr[i] > m->row_ptr[i + 1]) throw Err(GADI_E_CONTRACT, "row_ptr must be non-decreasing");
+      for (int64_t k = m->row_ptr[i]; k < m->row_ptr[i + 1]; ++k) {
+        if (m->col_idx[k] < 0 || m->col_idx[k] >= n) throw Err(GADI_E_CONTRACT, "column index out of range");
+        if (k > m->row_ptr[i] && m->col_idx[k] <= m->col_idx[k - 1])
+          throw Err(GADI_E_CONTRACT, "column indices must be strictly increasing within a row");
+      }
+    }
+  }
+  // A back from the device (this is setup; the handle keeps no host copy)
+  std::vector<int64_t> arp(n + 1);
+  std::vector<int32_t> aci(h->nnzA);
+  std::vector<double> av(h->nnzA);
+  CK(cudaMemcpy(arp.data(), h->d_rpA, (n + 1) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(aci.data(), h->d_ciA, h->nnzA * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(av.data(), h->d_vA, h->nnzA * 8, cudaMemcpyDeviceToHost));
+  int64_t band = h->max_band;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t m = M->row_ptr[i], me = M->row_ptr[i + 1], q = Nn->row_ptr[i], qe = Nn->row_ptr[i + 1];
+    int64_t a = arp[i];
+    const int64_t ae = arp[i + 1];
+    while (m < me || q < qe) {
+      const int64_t cm = m < me ? M->col_idx[m] : INT64_MAX, cn = q < qe ? Nn->col_idx[q] : INT64_MAX;
+      const int64_t col = std::min(cm, cn);
+      double sum;
+      if (cm == col && cn == col) sum = 1.0 * M->values[m] + 1.0 * Nn->values[q];
+      else if (cm == col) sum = 1.0 * M->values[m];
+      else sum = 1.0 * Nn->values[q];
+      if (cm == col) ++m;
+      if (cn == col) ++q;
+      while (a < ae && aci[a] < col) ++a;
+      const double aa = (a < ae && aci[a] == col) ? av[a] : 0.0;
+      if (std::fabs(sum - aa) > std::fabs(aa) * 2.220446049250313e-16)
+        throw Err(GADI_E_CONTRACT, "explicit_splitting: M + N != A");
+      band = std::max<int64_t>(band, std::llabs(col - i));
+    }
+  }
+  for (int w = 0; w < 2; ++w) {
+    const gadi_csr_desc* m = w == 0 ? M : Nn;
+    std::vector<int64_t> rp(n + 1, 0), dpos(n);
+    std::vector<int32_t> ci;
+    std::vector<double> v;
+    std::vector<uint8_t> din(n);
+    ci.reserve(m->nnz + n);
+    v.reserve(m->nnz + n);
+    for (int64_t i = 0; i < n; ++i) {
+      bool done = false;
+      for (int64_t k = m->row_ptr[i]; k < m->row_ptr[i + 1] || !done;) {
+        const int64_t col = k < m->row_ptr[i + 1] ? m->col_idx[k] : INT64_MAX;
+        if (!done && i <= col) {
+          dpos[i] = (int64_t)ci.size();
+          din[i] = col == i;
+          ci.push_back((int32_t)i);
+          v.push_back(col == i ? m->values[k] : 0.0);
+          if (col == i) ++k;
+          done = true;
+        } else {
+          ci.push_back((int32_t)col);
+          v.push_back(m->values[k]);
+          ++k;
+        }
+      }
+      rp[i + 1] = (int64_t)ci.size();
+    }
+    auto& p = h->ex[w];
+    p.nnz = (int64_t)ci.size();
+    p.rp = dalloc<int64_t>(n + 1);
+    p.ci = dalloc<int32_t>(p.nnz);
+    p.v = dalloc<double>(p.nnz);
+    p.dpos = dalloc<int64_t>(n);
+    p.din = dalloc<uint8_t>(n);
+    CK(cudaMemcpy(p.rp, rp.data(), (n + 1) * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.ci, ci.data(), p.nnz * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.v, v.data(), p.nnz * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.dpos, dpos.data(), n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.din, din.data(), n, cudaMemcpyHostToDevice));
+  }
+  h->ex_band = band;
+  h->explicit_split = true;
+  API_END
 }
 
 int gadi_cuda_dim(const gadi_handle* h, int64_t* n) {

@@ -350,6 +350,26 @@ struct gadi_handle {
   double *d_mv = nullptr, *d_nv = nullptr;
   int64_t* d_dpos = nullptr;
   uint8_t* d_din = nullptr;
+  // explicit_splitting(A, M, N) (splitting.cpp:22-35; gadi_cuda_set_split): M
+  // and N on their own patterns, each with the diagonal inserted where it has
+  // none (shift_diagonal's pattern, sparse.cpp:180-183)
+  struct SplitPart {
+    int64_t* rp = nullptr;
+    int32_t* ci = nullptr;
+    double* v = nullptr;
+    int64_t* dpos = nullptr;  // position of the diagonal entry of each row
+    uint8_t* din = nullptr;   // 1: the matrix's own pattern had it
+    int64_t nnz = 0;
+  };
+  bool explicit_split = false;
+  SplitPart ex[2];
+  int64_t ex_band = 0;  // max |column - row| over A, M and N
+  int64_t hs_band() const { return explicit_split ? ex_band : max_band; }  // band of the H / S operators
+  // M (which = 1) or N (which = 2) of the active split
+  SplitPart part(int which) const {
+    if (explicit_split) return ex[which - 1];
+    return SplitPart{d_urp, d_uci, which == 1 ? d_mv : d_nv, d_dpos, d_din, nnzHS};
+  }
   // outer vectors (binary64)
   double *d_x = nullptr, *d_b = nullptr, *d_s = nullptr, *d_t64 = nullptr;
   // reductions / state
@@ -684,7 +704,7 @@ struct Engine final : EngineBase {
   OV* dH = nullptr;  // sparse operators: H / S values in the SELL image sHS
   OV* dS = nullptr;
   uint8_t *zfH = nullptr, *zfS = nullptr;  // per-row zflag summaries of H / S (residual from x = 0)
-  SellImage sHS;
+  SellImage sHS, sS2;
   int m_restart = 30;
   std::vector<T*> owned;
   bool st25 = false;  // 2.5D TMA stencil kernels (gadi_st25.cuh) for the operator passes
@@ -733,7 +753,7 @@ struct Engine final : EngineBase {
     aligned = aligned_for(N, h->n, h->stencil(), VA);
     geo = make_geo(N, aligned ? VA : 1);
     geo.gh = h->gh;
-    if constexpr (SPARSE) win = window_for(geo, VA, sizeof(T), h->max_band, aligned);
+    if constexpr (SPARSE) win = window_for(geo, VA, sizeof(T), h->hs_band(), aligned);
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       constexpr int rsz = sizeof(typename RingOf<T, C>::type);
       st25 = make_st25(h->n, sizeof(T), 2, g25, 512, false, rsz, h->i0, h->i1) &&
@@ -798,6 +818,7 @@ struct Engine final : EngineBase {
     if (dH) cudaFree(dH);
     if (dS) cudaFree(dS);
     sHS.release();
+    sS2.release();
     if (zfH) cudaFree(zfH);
     if (zfS) cudaFree(zfS);
   }
@@ -837,27 +858,31 @@ struct Engine final : EngineBase {
     } else {
       // SELL image of the union pattern with VA rows per lane, values of
       // H / S rounded to u_r (rounded_copy, inner_solver.cpp:41-45) on the device
-      build_sell_layout(h->stream, h->N, ilog2(32 * VA), h->d_urp, h->d_uci, sHS, h->max_band < 32768);
-      auto fill = [&](const double* src) -> OV* {
+      // (an explicit split has one pattern per operator: S gets its own image sS2)
+      const auto pH = h->part(1), pS = h->part(2);
+      const bool rel = h->hs_band() < 32768;
+      build_sell_layout(h->stream, h->N, ilog2(32 * VA), pH.rp, pH.ci, sHS, rel);
+      if (h->explicit_split) build_sell_layout(h->stream, h->N, ilog2(32 * VA), pS.rp, pS.ci, sS2, rel);
+      const SellImage& iS = h->explicit_split ? sS2 : sHS;
+      auto fill = [&](const SellImage& im, const gadi_handle::SplitPart& pt) -> OV* {
         if (u_r == GADI_HALF)
-          return fill_sell_values<OV, P_HALF>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+          return fill_sell_values<OV, P_HALF>(h->stream, h->N, im, pt.rp, pt.v, pt.dpos, pt.din, alpha);
         if (u_r == GADI_SINGLE)
-          return fill_sell_values<OV, P_SINGLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
-        return fill_sell_values<OV, P_DOUBLE>(h->stream, h->N, sHS, h->d_urp, src, h->d_dpos, h->d_din, alpha);
+          return fill_sell_values<OV, P_SINGLE>(h->stream, h->N, im, pt.rp, pt.v, pt.dpos, pt.din, alpha);
+        return fill_sell_values<OV, P_DOUBLE>(h->stream, h->N, im, pt.rp, pt.v, pt.dpos, pt.din, alpha);
       };
-      dH = fill(h->d_mv);
-      dS = fill(h->d_nv);
-      auto zflags = [&](const OV* v) {
+      dH = fill(sHS, pH);
+      dS = fill(iS, pS);
+      auto zflags = [&](const SellImage& im, const OV* v) {
         uint8_t* z = dalloc<uint8_t>(h->N);
-        k_sell_zflags<OV><<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, sHS.lgSR, sHS.soff, sHS.len,
-                                                                                 v, z);
+        k_sell_zflags<OV><<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, im.lgSR, im.soff, im.len, v, z);
         CKL();
         return z;
       };
-      zfH = zflags(dH);
-      zfS = zflags(dS);
+      zfH = zflags(sHS, dH);
+      zfS = zflags(iS, dS);
       opH = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dH, sHS.off, zfH};
-      opS = Op{h->N, sHS.lgSR, sHS.soff, sHS.len, sHS.col, dS, sHS.off, zfS};
+      opS = Op{h->N, iS.lgSR, iS.soff, iS.len, iS.col, dS, iS.off, zfS};
     }
   }
 

@@ -815,7 +815,8 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
     unsigned long long* bw = nullptr;
     CK(cudaMallocAsync((void**)&bw, 16, h->stream));
     CK(cudaMemsetAsync(bw, 0, 16, h->stream));
-    k_bandwidths<<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, h->d_urp, h->d_uci, bw);
+    const auto pt = h->part(which);  // the operator's own pattern (the HSS union, or an explicit M / N)
+    k_bandwidths<<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, pt.rp, pt.ci, bw);
     CKL();
     unsigned long long hb[2];
     CK(cudaMemcpyAsync(hb, bw, 16, cudaMemcpyDeviceToHost, h->stream));
@@ -863,16 +864,16 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
     else
       k_band_stencil<float><<<g, 256, 0, s>>>((float*)f->ab, h->n, N, ldoff, f->ldab, lo, dg, up);
   } else {
-    const double* v = which == 1 ? h->d_mv : h->d_nv;
+    const auto pt = h->part(which);
     if (ur == GADI_DOUBLE)
-      k_band_csr<double, P_DOUBLE><<<g, 256, 0, s>>>((double*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
-                                                       h->d_dpos, h->d_din, alpha);
+      k_band_csr<double, P_DOUBLE><<<g, 256, 0, s>>>((double*)f->ab, N, ldoff, f->ldab, pt.rp, pt.ci, pt.v, pt.dpos,
+                                                       pt.din, alpha);
     else if (ur == GADI_SINGLE)
-      k_band_csr<float, P_SINGLE><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
-                                                      h->d_dpos, h->d_din, alpha);
+      k_band_csr<float, P_SINGLE><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, pt.rp, pt.ci, pt.v, pt.dpos,
+                                                      pt.din, alpha);
     else
-      k_band_csr<float, P_HALF><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, h->d_urp, h->d_uci, v,
-                                                    h->d_dpos, h->d_din, alpha);
+      k_band_csr<float, P_HALF><<<g, 256, 0, s>>>((float*)f->ab, N, ldoff, f->ldab, pt.rp, pt.ci, pt.v, pt.dpos,
+                                                    pt.din, alpha);
   }
   CKL();
   ++f->launches;
