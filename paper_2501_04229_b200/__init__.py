@@ -145,8 +145,9 @@ class _Problem(C.Structure):
 
 
 class _CsrDesc(C.Structure):  # gadi_csr_desc
-    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64), ("row_ptr", _i64p),
-                ("col_idx", _i64p), ("values", _f64p)]
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.POINTER(C.c_int64)), ("col_idx", C.POINTER(C.c_int64)),
+                ("values", C.POINTER(C.c_double))]
 
 
 class _DevOpts(C.Structure):
