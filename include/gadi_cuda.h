@@ -317,6 +317,12 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
 int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, double* stddev);
 int gadi_gpr_params(const gadi_gpr* g, double* sigma_f2, double* length, double* sigma_n2,
                     double* lml, double* target_mean);
+/* Device times of the last fit / inverse-factor formation / variance pass
+ * (CUDA events, ms), the variance path the last predict took (1 = tcgen05
+ * tensor cores with fp16 hi/lo operands, 2 = binary64) and the kernels
+ * launched so far (bench / driver evidence). Any pointer may be NULL. */
+int gadi_gpr_timings(const gadi_gpr* g, double* fit_ms, double* inverse_ms, double* variance_ms,
+                     int32_t* variance_path, int64_t* launches);
 int gadi_gpr_destroy(gadi_gpr* g);
 
 /* ---- GPR training-set generation (gpr.hpp:37-58; gpr.cpp:15-68) over the

@@ -211,6 +211,7 @@ def lib():
     L.gadi_gpr_predict.argtypes = [C.c_void_p, _f64p, C.c_int32, _f64p, _f64p]
     L.gadi_gpr_params.argtypes = [C.c_void_p, _f64p, _f64p, _f64p, _f64p, _f64p]
     L.gadi_gpr_destroy.argtypes = [C.c_void_p]
+    L.gadi_gpr_timings.argtypes = [C.c_void_p, _f64p, _f64p, _f64p, _i32p, _i64p]
     L.gadi_cuda_launch_count.argtypes = [C.c_void_p]
     L.gadi_cuda_launch_count.restype = C.c_int64
     L.gadi_cuda_nnz.argtypes = [C.c_void_p, _i64p, _i64p]
@@ -660,6 +661,15 @@ class GprModel:
         v = [C.c_double() for _ in range(5)]
         _check(lib().gadi_gpr_params(self._h, *[C.byref(t) for t in v]))
         return dict(zip(("sigma_f2", "length", "sigma_n2", "lml", "target_mean"), [t.value for t in v]))
+
+    def timings(self):
+        """Device times (ms) of the fit, the inverse-factor formation and the last
+        variance pass; the variance path taken ("tensor" = tcgen05, "fp64"); kernels launched."""
+        f, i, v = C.c_double(), C.c_double(), C.c_double()
+        path, n = C.c_int32(), C.c_int64()
+        _check(lib().gadi_gpr_timings(self._h, C.byref(f), C.byref(i), C.byref(v), C.byref(path), C.byref(n)))
+        return {"fit_ms": f.value, "inverse_ms": i.value, "variance_ms": v.value,
+                "variance_path": {1: "tensor", 2: "fp64"}.get(path.value, "none"), "launches": n.value}
 
     def predict(self, sizes):
         sizes = _f64(sizes)

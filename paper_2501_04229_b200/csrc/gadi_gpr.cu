@@ -1,5 +1,6 @@
 // gadi_gpr.cu — the GPR alpha predictor on the device (gpr.hpp:60-87;
-// fit gpr.cpp:109-149 with try_fit :84-105, predict_alpha :151-169).
+// fit gpr.cpp:109-149 with try_fit :84-105, predict_alpha :151-169), on
+// hand-written sm_100a kernels only (no cuSOLVER / cuBLAS).
 //
 // Inputs are ln(size) (gpr.cpp:114), targets centred on their mean, the
 // squared-exponential Gram matrix K_ij = sf2 exp(-(x_i - x_j)^2 / (2 l^2))
@@ -7,17 +8,28 @@
 // either searches the reference's 27-point grid (sf2 in {1/4,1,4} var,
 // l in {1/2,1,2} spacing, sn2 in {1e-10,1e-8,1e-6} var; strict '>' keeps the
 // first maximum of the log marginal likelihood) or takes fixed (sf2, l, sn2)
-// (BASELINE configs[4]: l = 1, sn2 = 1e-4). The Gram matrix is built by a
-// device kernel and factored by cuSOLVER's Dpotrf (a plain library
-// factorization); predictions build K_* on the device, the mean is a fused
-// kernel-vector pass and the variance sf2 + sn2 - ||L^-1 k_*||^2 is one
-// cuBLAS Dtrsm over a block of queries followed by a fused column-norm pass.
-#include <cublas_v2.h>
+// (BASELINE configs[4]: l = 1, sn2 = 1e-4).
+//
+//   fit      K on the device, blocked right-looking Cholesky in binary64
+//            (gadi_gpr_dense.cuh: k_potrf128 / k_trsm_right / k_dgemm), a =
+//            K^-1 y by blocked forward / backward substitution, LML.
+//   predict  mean: binary64, kernel values on the fly (k_mean).
+//            variance sf2 + sn2 - ||L^-1 k_*||^2: the m^2 q contraction. The
+//            inverse factor X = L^-1 is formed once (binary64, right-looking
+//            block substitution) and
+//              * tensor path (gadi_gpr_umma.cuh): X is split into fp16 hi/lo
+//                operand tiles, K_* is generated on the fly, D = X K_* runs on
+//                tcgen05.mma with fp32 accumulators in TMEM, the epilogue
+//                reduces ||.||^2 per query;
+//              * binary64 path: V = X K_* with k_dgemm, column sums of squares.
+//            The tensor path is taken when its error model allows it
+//            (use_tensor below); GADI_GPR_VAR=fp64|tensor overrides.
 #include <cuda_runtime.h>
-#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -25,10 +37,14 @@
 #include <vector>
 
 #include "../../include/gadi_cuda.h"
+#include "gadi_gpr_dense.cuh"
+#include "gadi_gpr_umma.cuh"
 
 namespace gadi_host {
 void set_last_error(const std::string& m);  // gadi_api.cu: shared by gadi_last_error()
 }
+
+using namespace gpr_dev;
 
 namespace {
 
@@ -40,79 +56,10 @@ struct GErr : std::runtime_error {
 #define GCK(x)                                                                            \
   do {                                                                                    \
     cudaError_t e_ = (x);                                                                 \
-    if (e_ != cudaSuccess) throw GErr(GADI_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    if (e_ != cudaSuccess)                                                                \
+      throw GErr(e_ == cudaErrorMemoryAllocation ? GADI_E_OOM : GADI_E_CUDA,             \
+                 std::string(#x) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
-#define BCK(x)                                                                     \
-  do {                                                                             \
-    if ((x) != CUBLAS_STATUS_SUCCESS) throw GErr(GADI_E_CUDA, std::string(#x));    \
-  } while (0)
-#define SCK(x)                                                                     \
-  do {                                                                             \
-    if ((x) != CUSOLVER_STATUS_SUCCESS) throw GErr(GADI_E_CUDA, std::string(#x));  \
-  } while (0)
-
-// K (column major, m x m) = sf2 * exp(-0.5 d^2), d = (x_i - x_j) / l (gpr.cpp:70-73),
-// diagonal += sn2 + 1e-12 * max(1, sf2) (gpr.cpp:88)
-__global__ void k_gram(const double* __restrict__ x, int m, double sf2, double ell, double jitter,
-                       double* __restrict__ K) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)m * m) return;
-  const int i = (int)(idx % m), j = (int)(idx / m);
-  const double d = __ddiv_rn(__dsub_rn(x[i], x[j]), ell);
-  double v = __dmul_rn(sf2, exp(__dmul_rn(-0.5, __dmul_rn(d, d))));
-  if (i == j) v = __dadd_rn(v, jitter);
-  K[idx] = v;
-}
-
-// K_*^T block (m x qb, column major): k(x_i, xq_t)
-__global__ void k_cross(const double* __restrict__ x, int m, const double* __restrict__ xq, int qb, double sf2,
-                        double ell, double* __restrict__ Ks) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)m * qb) return;
-  const int i = (int)(idx % m), t = (int)(idx / m);
-  const double d = __ddiv_rn(__dsub_rn(xq[t], x[i]), ell);
-  Ks[idx] = __dmul_rn(sf2, exp(__dmul_rn(-0.5, __dmul_rn(d, d))));
-}
-
-// per query column t: mean = mu + k.a, and ||v||^2 of the solved column (one warp each)
-__global__ void k_pred_cols(const double* __restrict__ Ks, const double* __restrict__ V, const double* __restrict__ a,
-                            int m, int qb, double mu, double sfsn, double floor_mean, double* __restrict__ mean,
-                            double* __restrict__ sd) {
-  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= qb) return;
-  double kd = 0.0, vn = 0.0;
-  for (int i = lane; i < m; i += 32) {
-    kd = fma(Ks[(int64_t)t * m + i], a[i], kd);
-    const double v = V[(int64_t)t * m + i];
-    vn = fma(v, v, vn);
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    kd += __shfl_xor_sync(0xffffffffu, kd, o);
-    vn += __shfl_xor_sync(0xffffffffu, vn, o);
-  }
-  if (lane == 0) {
-    double mn = mu + kd;
-    double var = sfsn - vn;
-    if (var < 0.0) var = 0.0;
-    if (mn < floor_mean) mn = floor_mean;
-    mean[t] = mn;
-    sd[t] = sqrt(var);
-  }
-}
-
-__global__ void k_logdiag(const double* __restrict__ L, int m, double* __restrict__ out) {
-  __shared__ double sm[256];
-  double s = 0.0;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) s += log(L[(int64_t)i * m + i]);
-  sm[threadIdx.x] = s;
-  __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = sm[0];
-}
 
 template <class T>
 T* galloc(size_t n) {
@@ -121,53 +68,170 @@ T* galloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+constexpr size_t SM_POTRF = (size_t)NB * 129 * 8;
+constexpr size_t SM_TRSM_R = ((size_t)NB * (NB + 1) / 2 + 64 * 129) * 8;
+constexpr size_t SM_TRSM_L = ((size_t)NB * (NB + 1) / 2 + NB * 64) * 8;
+constexpr size_t SM_TRSV_T = ((size_t)NB * (NB + 1) / 2) * 8;
+
+void set_attrs() {  // per device: the large dynamic shared-memory sizes
+  static bool done[64] = {};
+  int dev = 0;
+  GCK(cudaGetDevice(&dev));
+  if (done[dev & 63]) return;
+  GCK(cudaFuncSetAttribute(k_potrf128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_POTRF));
+  GCK(cudaFuncSetAttribute(k_trsm_right, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSM_R));
+  GCK(cudaFuncSetAttribute(k_trsm_left, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSM_L));
+  GCK(cudaFuncSetAttribute(k_trsv_diag_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSV_T));
+  GCK(cudaFuncSetAttribute(k_var_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
+  done[dev & 63] = true;
+}
+
 }  // namespace
 
 struct gadi_gpr {
-  int device = 0, m = 0;
+  int device = 0, m = 0, mp = 0;
   cudaStream_t s = nullptr;
-  cublasHandle_t cb = nullptr;
-  cusolverDnHandle_t cs = nullptr;
   double mu = 0, sf2 = 1, ell = 1, sn2 = 1e-8, lml = 0, tmin = 0;
-  double* d_x = nullptr;  // ln(size)
-  double* d_L = nullptr;  // lower Cholesky factor of K (column major)
-  double* d_a = nullptr;  // K^-1 (y - mu)
-  double fit_ms = 0.0;
+  double* d_x = nullptr;    // ln(size), m
+  double* d_L = nullptr;    // lower Cholesky factor of K, mp x mp row-major (rows >= m: identity)
+  double* d_a = nullptr;    // K^-1 (y - mu), mp (zero padded)
+  double* d_X = nullptr;    // L^-1 (binary64), formed at the first predict
+  uint8_t* d_img = nullptr; // fp16 hi/lo operand image of 2^6 sqrt(sf2) X (tensor path)
+  float2* d_xs2 = nullptr;  // inputs as double-float
+  int img_exp = 0;          // the image holds 2^img_exp sf2 X
+  double fit_ms = 0.0, inv_ms = 0.0, var_ms = 0.0;
+  int64_t launches = 0;
+  int last_var_path = 0;    // 1 tensor, 2 binary64
   ~gadi_gpr() {
-    for (void* p : {(void*)d_x, (void*)d_L, (void*)d_a})
+    for (void* p : {(void*)d_x, (void*)d_L, (void*)d_a, (void*)d_X, (void*)d_img, (void*)d_xs2})
       if (p) cudaFree(p);
-    if (cb) cublasDestroy(cb);
-    if (cs) cusolverDnDestroy(cs);
     if (s) cudaStreamDestroy(s);
   }
 };
 
 namespace {
 
+// Blocked right-looking Cholesky of the mp x mp matrix W (lower), in place.
+void cholesky(gadi_gpr* g, double* W, int* d_info) {
+  const int mp = g->mp;
+  cudaStream_t s = g->s;
+  for (int j0 = 0; j0 < mp; j0 += NB) {
+    k_potrf128<<<1, 256, SM_POTRF, s>>>(W, mp, j0, d_info);
+    const int j1 = j0 + NB, rem = mp - j1;
+    ++g->launches;
+    if (rem <= 0) break;
+    k_trsm_right<<<(rem + 63) / 64, 64, SM_TRSM_R, s>>>(W, mp, j0, j1, rem);
+    const double* P = W + (size_t)j1 * mp + j0;  // the panel L21: rem x 128
+    k_dgemm<false, true><<<dim3((rem + 63) / 64, (rem + 63) / 64), 256, 0, s>>>(W + (size_t)j1 * mp + j1, mp, P, mp, P,
+                                                                                  mp, rem, rem, NB);
+    g->launches += 2;
+  }
+  GCK(cudaGetLastError());
+}
+
+// a = L^-T L^-1 y on the padded vector v (mp), in place: blocked substitution.
+void solve_llt(gadi_gpr* g, const double* L, double* v) {
+  const int mp = g->mp;
+  cudaStream_t s = g->s;
+  for (int i0 = 0; i0 < mp; i0 += NB) {  // forward: z = L^-1 y
+    k_trsm_left<<<1, 64, SM_TRSM_L, s>>>(L, mp, i0, v, 1, 0, 1);
+    const int rem = mp - i0 - NB;
+    ++g->launches;
+    if (rem > 0) {
+      k_gemv_sub<<<(rem + 7) / 8, 256, 0, s>>>(L, mp, i0 + NB, rem, i0, v, v);
+      ++g->launches;
+    }
+  }
+  for (int i0 = mp - NB; i0 >= 0; i0 -= NB) {  // backward: a = L^-T z
+    k_trsv_diag_T<<<1, 128, SM_TRSV_T, s>>>(L, mp, i0, v);
+    ++g->launches;
+    if (i0 > 0) {
+      k_gemvT_sub<<<(i0 + 255) / 256, 256, 0, s>>>(L, mp, i0, i0, v, v);
+      ++g->launches;
+    }
+  }
+  GCK(cudaGetLastError());
+}
+
 // try_fit (gpr.cpp:84-105) for one hyperparameter triple; false when K is
 // not positive definite after jitter or the LML is not finite.
-bool try_fit(gadi_gpr* g, const std::vector<double>& y, double sf2, double ell, double sn2, double* d_K,
-             double* d_work, int lwork, int* d_info, double* d_tmp, double& lml) {
-  const int m = g->m;
+bool try_fit(gadi_gpr* g, const std::vector<double>& y, double sf2, double ell, double sn2, double* d_W, double* d_v,
+             int* d_info, double* d_ld, std::vector<double>& a, double& lml) {
+  const int m = g->m, mp = g->mp;
   const double jitter = sn2 + 1e-12 * std::max(1.0, sf2);
-  const int64_t mm = (int64_t)m * m;
-  k_gram<<<(unsigned)((mm + 255) / 256), 256, 0, g->s>>>(g->d_x, m, sf2, ell, jitter, d_K);
-  GCK(cudaGetLastError());
-  SCK(cusolverDnDpotrf(g->cs, CUBLAS_FILL_MODE_LOWER, m, d_K, m, d_work, lwork, d_info));
+  const int64_t mm = (int64_t)mp * mp;
+  GCK(cudaMemsetAsync(d_info, 0, sizeof(int), g->s));
+  k_gram<<<(unsigned)((mm + 255) / 256), 256, 0, g->s>>>(g->d_x, m, mp, sf2, ell, jitter, d_W);
+  ++g->launches;
+  cholesky(g, d_W, d_info);
   int info = 0;
   GCK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, g->s));
   GCK(cudaStreamSynchronize(g->s));
   if (info != 0) return false;
-  GCK(cudaMemcpyAsync(d_tmp, y.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
-  SCK(cusolverDnDpotrs(g->cs, CUBLAS_FILL_MODE_LOWER, m, 1, d_K, m, d_tmp, m, d_info));
-  k_logdiag<<<1, 256, 0, g->s>>>(d_K, m, d_tmp + m);
-  std::vector<double> a(m + 1);
-  GCK(cudaMemcpyAsync(a.data(), d_tmp, (m + 1) * sizeof(double), cudaMemcpyDeviceToHost, g->s));
+  GCK(cudaMemsetAsync(d_v, 0, mp * sizeof(double), g->s));
+  GCK(cudaMemcpyAsync(d_v, y.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
+  solve_llt(g, d_W, d_v);
+  k_logdiag<<<1, 256, 0, g->s>>>(d_W, mp, m, d_ld);
+  ++g->launches;
+  double ld = 0.0;
+  a.resize(m);
+  GCK(cudaMemcpyAsync(a.data(), d_v, m * sizeof(double), cudaMemcpyDeviceToHost, g->s));
+  GCK(cudaMemcpyAsync(&ld, d_ld, sizeof(double), cudaMemcpyDeviceToHost, g->s));
   GCK(cudaStreamSynchronize(g->s));
   double ya = 0.0;
   for (int i = 0; i < m; ++i) ya += y[i] * a[i];
-  lml = -0.5 * ya - a[m] - 0.5 * (double)m * std::log(2.0 * M_PI);
+  lml = -0.5 * ya - ld - 0.5 * (double)m * std::log(2.0 * M_PI);
   return std::isfinite(lml);
+}
+
+// X = L^-1 in binary64: right-looking block substitution on the identity.
+void form_inverse(gadi_gpr* g) {
+  if (g->d_X) return;
+  const int mp = g->mp;
+  cudaStream_t s = g->s;
+  cudaEvent_t e0, e1;
+  GCK(cudaEventCreate(&e0));
+  GCK(cudaEventCreate(&e1));
+  GCK(cudaEventRecord(e0, s));
+  double* X = galloc<double>((size_t)mp * mp);
+  const int64_t mm = (int64_t)mp * mp;
+  k_eye<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(X, mp);
+  ++g->launches;
+  for (int i0 = 0; i0 < mp; i0 += NB) {
+    const int nc = i0 + NB, i1 = i0 + NB, rem = mp - i1;
+    k_trsm_left<<<(nc + 63) / 64, 64, SM_TRSM_L, s>>>(g->d_L, mp, i0, X, mp, 0, nc);
+    ++g->launches;
+    if (rem > 0) {
+      k_dgemm<true, false><<<dim3((nc + 63) / 64, (rem + 63) / 64), 256, 0, s>>>(
+          X + (size_t)i1 * mp, mp, g->d_L + (size_t)i1 * mp + i0, mp, X + (size_t)i0 * mp, mp, rem, nc, NB);
+      ++g->launches;
+    }
+  }
+  GCK(cudaGetLastError());
+  GCK(cudaEventRecord(e1, s));
+  GCK(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  g->inv_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  g->d_X = X;
+}
+
+// The tensor path's error model: fp16 hi/lo operands carry ~22 bits, and the
+// fp32 accumulator in TMEM truncates once per MMA, a relative bias of about
+// (3 m / 16) 2^-24 on each row sum (measured 5e-5 on ||.||^2 at m = 4096,
+// tools/umma_probe.cu). The variance subtracts sf2 ||X k'||^2 <= sf2 from
+// sf2 + sn2, so its relative error is bounded by that bias times sf2 / sn2.
+// The tensor path is taken when the bound keeps sd within 1e-4 relative.
+bool use_tensor(const gadi_gpr* g) {
+  if (const char* e = std::getenv("GADI_GPR_VAR")) {
+    if (!std::strcmp(e, "fp64")) return false;
+    if (!std::strcmp(e, "tensor")) return true;
+  }
+  if (g->m < 1024) return false;  // below this the binary64 path takes well under a millisecond per 2048 queries
+  const double bias = 2.0 * (3.0 * g->mp / 16.0) * std::ldexp(1.0, -24);
+  return bias * g->sf2 <= 2e-4 * g->sn2;
 }
 
 }  // namespace
@@ -182,7 +246,10 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     std::unique_ptr<gadi_gpr> g(new gadi_gpr());
     g->device = opts ? opts->device : 0;
     GCK(cudaSetDevice(g->device));
+    set_attrs();
     g->m = m;
+    g->mp = ((m + UM_PASS_ROWS - 1) / UM_PASS_ROWS) * UM_PASS_ROWS;  // multiple of 256 (two 128-row accumulators per pass)
+    const int mp = g->mp;
     std::vector<double> x(m), y(m);
     double mu = 0.0, tmin = std::numeric_limits<double>::infinity();
     for (int i = 0; i < m; ++i) {
@@ -203,24 +270,19 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     g->mu = mu;
     g->tmin = tmin;
     GCK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
-    BCK(cublasCreate(&g->cb));
-    BCK(cublasSetStream(g->cb, g->s));
-    SCK(cusolverDnCreate(&g->cs));
-    SCK(cusolverDnSetStream(g->cs, g->s));
     cudaEvent_t e0, e1;
     GCK(cudaEventCreate(&e0));
     GCK(cudaEventCreate(&e1));
     GCK(cudaEventRecord(e0, g->s));
     g->d_x = galloc<double>(m);
     GCK(cudaMemcpyAsync(g->d_x, x.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
-    double* d_K = galloc<double>((size_t)m * m);
-    g->d_L = galloc<double>((size_t)m * m);
-    g->d_a = galloc<double>(m);
-    double* d_tmp = galloc<double>(m + 1);
+    double* d_W = galloc<double>((size_t)mp * mp);
+    g->d_L = galloc<double>((size_t)mp * mp);
+    g->d_a = galloc<double>(mp);
+    GCK(cudaMemsetAsync(g->d_a, 0, mp * sizeof(double), g->s));
+    double* d_v = galloc<double>(mp);
+    double* d_ld = galloc<double>(1);
     int* d_info = galloc<int>(1);
-    int lwork = 0;
-    SCK(cusolverDnDpotrf_bufferSize(g->cs, CUBLAS_FILL_MODE_LOWER, m, d_K, m, &lwork));
-    double* d_work = galloc<double>(lwork);
     std::vector<double> sfs, ells, sns;
     if (opts && opts->fixed_hypers) {
       sfs = {opts->sigma_f2};
@@ -233,17 +295,19 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
       else sns = {1e-10 * var, 1e-8 * var, 1e-6 * var};
     }
     double best = -std::numeric_limits<double>::infinity();
+    std::vector<double> a;
     for (double sf : sfs)
       for (double el : ells)
         for (double sn : sns) {
           double lml = 0.0;
-          if (try_fit(g.get(), y, sf, el, sn, d_K, d_work, lwork, d_info, d_tmp, lml) && lml > best) {
+          if (try_fit(g.get(), y, sf, el, sn, d_W, d_v, d_info, d_ld, a, lml) && lml > best) {
             best = lml;
             g->sf2 = sf;
             g->ell = el;
             g->sn2 = sn;
-            GCK(cudaMemcpyAsync(g->d_L, d_K, (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, g->s));
-            GCK(cudaMemcpyAsync(g->d_a, d_tmp, m * sizeof(double), cudaMemcpyDeviceToDevice, g->s));
+            std::swap(d_W, g->d_L);  // keep this factor; the other buffer is the next candidate's workspace
+            GCK(cudaMemcpyAsync(g->d_a, a.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
+            GCK(cudaStreamSynchronize(g->s));
           }
         }
     GCK(cudaEventRecord(e1, g->s));
@@ -253,7 +317,7 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     g->fit_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    for (void* p : {(void*)d_K, (void*)d_tmp, (void*)d_info, (void*)d_work}) cudaFree(p);
+    for (void* p : {(void*)d_W, (void*)d_v, (void*)d_ld, (void*)d_info}) cudaFree(p);
     if (!std::isfinite(best)) throw GErr(GADI_E_FIT, "fit: Gram matrix not positive definite for any hyperparameter choice");
     g->lml = best;
     *out = g.release();
@@ -270,36 +334,91 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
 int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, double* stddev) {
   try {
     if (!g || (!sizes && q > 0) || (q > 0 && (!mean || !stddev))) throw GErr(GADI_E_CONTRACT, "gpr_predict: bad argument");
+    if (q <= 0) return GADI_OK;
     GCK(cudaSetDevice(g->device));
-    const int m = g->m;
-    const int QB = 8192;  // queries per block of the triangular solve
-    std::vector<double> xq(std::min(q, QB));
-    double* d_xq = galloc<double>(QB);
-    double* d_Ks = galloc<double>((size_t)m * QB);
-    double* d_V = galloc<double>((size_t)m * QB);
-    double* d_mean = galloc<double>(QB);
-    double* d_sd = galloc<double>(QB);
-    const double one = 1.0;
-    for (int t0 = 0; t0 < q; t0 += QB) {
-      const int qb = std::min(QB, q - t0);
-      xq.resize(qb);
-      for (int t = 0; t < qb; ++t) xq[t] = std::log(sizes[t0 + t]);
-      GCK(cudaMemcpyAsync(d_xq, xq.data(), qb * sizeof(double), cudaMemcpyHostToDevice, g->s));
-      const int64_t n = (int64_t)m * qb;
-      k_cross<<<(unsigned)((n + 255) / 256), 256, 0, g->s>>>(g->d_x, m, d_xq, qb, g->sf2, g->ell, d_Ks);
+    set_attrs();
+    const int m = g->m, mp = g->mp;
+    cudaStream_t s = g->s;
+    std::vector<double> xq(q);
+    for (int t = 0; t < q; ++t) xq[t] = std::log(sizes[t]);
+    double* d_xq = galloc<double>(q);
+    double* d_mean = galloc<double>(q);
+    double* d_var = galloc<double>(q);
+    GCK(cudaMemcpyAsync(d_xq, xq.data(), q * sizeof(double), cudaMemcpyHostToDevice, s));
+    k_mean<<<(q + 7) / 8, 256, 0, s>>>(g->d_x, g->d_a, m, d_xq, q, g->sf2, g->ell, g->mu, g->tmin / 10.0, d_mean);
+    ++g->launches;
+    form_inverse(g);
+    cudaEvent_t e0, e1;
+    GCK(cudaEventCreate(&e0));
+    GCK(cudaEventCreate(&e1));
+    GCK(cudaEventRecord(e0, s));
+    if (use_tensor(g)) {
+      g->last_var_path = 1;
+      const int npass = mp / UM_PASS_ROWS;
+      if (!g->d_img) {
+        // split sf2 X once into fp16 hi/lo tiles in the operand layout, scaled by
+        // 2^ea so that the largest entry lies in [256, 512): || L^-1 k ||^2 =
+        // || (sf2 X) k' ||^2 with k' = k / sf2 = exp(.), what the kernel generates
+        unsigned long long* d_mx = galloc<unsigned long long>(1);
+        GCK(cudaMemsetAsync(d_mx, 0, 8, s));
+        const int64_t mm = (int64_t)mp * mp;
+        k_maxabs_lower<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(g->d_X, mp, d_mx);
+        unsigned long long bits = 0;
+        GCK(cudaMemcpyAsync(&bits, d_mx, 8, cudaMemcpyDeviceToHost, s));
+        GCK(cudaStreamSynchronize(s));
+        cudaFree(d_mx);
+        double mx;
+        std::memcpy(&mx, &bits, 8);
+        mx *= g->sf2;
+        if (!(mx > 0.0) || !std::isfinite(mx)) throw GErr(GADI_E_FIT, "predict: inverse factor is not finite");
+        g->img_exp = 8 - std::ilogb(mx);
+        g->d_img = galloc<uint8_t>((size_t)4 * npass * (npass + 1) * UM_A_STAGE);
+        k_pack_linv<<<dim3(8 * npass, npass), 256, 0, s>>>(g->d_X, mp, mp, std::ldexp(g->sf2, g->img_exp), g->d_img);
+        g->d_xs2 = galloc<float2>(mp);
+        k_split_f2<<<(mp + 255) / 256, 256, 0, s>>>(g->d_x, m, mp, g->d_xs2);
+        g->launches += 3;
+      }
+      float2* d_xq2 = galloc<float2>(q);
+      k_split_f2<<<(q + 255) / 256, 256, 0, s>>>(d_xq, q, q, d_xq2);
+      VarParams P{g->d_img, g->d_xs2, d_xq2, mp, m, q, (float)(1.0 / g->ell),
+                  std::ldexp(1.0, -2 * (g->img_exp + (int)UM_SCALE_B_LOG2)), g->sf2 + g->sn2, d_var};
+      k_var_umma<<<(q + UM_NQ - 1) / UM_NQ, UM_THREADS, UM_SMEM, s>>>(P);
+      g->launches += 2;
       GCK(cudaGetLastError());
-      GCK(cudaMemcpyAsync(d_V, d_Ks, n * sizeof(double), cudaMemcpyDeviceToDevice, g->s));
-      // v = L^-1 k_* for every query of the block (predict_alpha, gpr.cpp:159-161)
-      BCK(cublasDtrsm(g->cb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, m, qb, &one,
-                      g->d_L, m, d_V, m));
-      k_pred_cols<<<(qb + 7) / 8, 256, 0, g->s>>>(d_Ks, d_V, g->d_a, m, qb, g->mu, g->sf2 + g->sn2, g->tmin / 10.0,
-                                                   d_mean, d_sd);
+      GCK(cudaStreamSynchronize(s));
+      cudaFree(d_xq2);
+    } else {
+      g->last_var_path = 2;
+      const int QB = 2048;
+      double* d_Ks = galloc<double>((size_t)mp * QB);
+      double* d_V = galloc<double>((size_t)mp * QB);
+      for (int t0 = 0; t0 < q; t0 += QB) {
+        const int qb = std::min(QB, q - t0);
+        const int64_t n = (int64_t)mp * qb;
+        k_cross<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g->d_x, m, mp, d_xq + t0, qb, QB, g->sf2, g->ell, d_Ks);
+        GCK(cudaMemsetAsync(d_V, 0, (size_t)mp * QB * sizeof(double), s));
+        k_dgemm<true, false><<<dim3((qb + 63) / 64, (mp + 63) / 64), 256, 0, s>>>(d_V, QB, g->d_X, mp, d_Ks, QB, mp, qb,
+                                                                                 mp);
+        k_colsumsq<<<(qb + 255) / 256, 256, 0, s>>>(d_V, mp, qb, QB, g->sf2 + g->sn2, d_var + t0);
+        g->launches += 3;
+      }
       GCK(cudaGetLastError());
-      GCK(cudaMemcpyAsync(mean + t0, d_mean, qb * sizeof(double), cudaMemcpyDeviceToHost, g->s));
-      GCK(cudaMemcpyAsync(stddev + t0, d_sd, qb * sizeof(double), cudaMemcpyDeviceToHost, g->s));
+      GCK(cudaStreamSynchronize(s));
+      cudaFree(d_Ks);
+      cudaFree(d_V);
     }
-    GCK(cudaStreamSynchronize(g->s));
-    for (void* p : {(void*)d_xq, (void*)d_Ks, (void*)d_V, (void*)d_mean, (void*)d_sd}) cudaFree(p);
+    GCK(cudaEventRecord(e1, s));
+    GCK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    g->var_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    GCK(cudaMemcpyAsync(mean, d_mean, q * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GCK(cudaMemcpyAsync(stddev, d_var, q * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GCK(cudaStreamSynchronize(s));
+    for (int t = 0; t < q; ++t) stddev[t] = std::sqrt(stddev[t]);
+    for (void* p : {(void*)d_xq, (void*)d_mean, (void*)d_var}) cudaFree(p);
     return GADI_OK;
   } catch (const GErr& e) {
     gadi_host::set_last_error(e.what());
@@ -318,6 +437,17 @@ int gadi_gpr_params(const gadi_gpr* g, double* sigma_f2, double* length, double*
   if (sigma_n2) *sigma_n2 = g->sn2;
   if (lml) *lml = g->lml;
   if (target_mean) *target_mean = g->mu;
+  return GADI_OK;
+}
+
+int gadi_gpr_timings(const gadi_gpr* g, double* fit_ms, double* inverse_ms, double* variance_ms, int32_t* variance_path,
+                     int64_t* launches) {
+  if (!g) return GADI_E_CONTRACT;
+  if (fit_ms) *fit_ms = g->fit_ms;
+  if (inverse_ms) *inverse_ms = g->inv_ms;
+  if (variance_ms) *variance_ms = g->var_ms;
+  if (variance_path) *variance_path = g->last_var_path;
+  if (launches) *launches = g->launches;
   return GADI_OK;
 }
 

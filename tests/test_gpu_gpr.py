@@ -60,3 +60,58 @@ def test_extrapolation_grows_uncertainty():
     m = g.gpr_fit([512, 1728, 4096, 13824], [0.08, 0.065, 0.06, 0.058])
     (m1, m2), (s1, s2) = m.predict([4096, 40960000])
     assert s2 > s1 and m1 > 0 and m2 > 0 and m2 >= 0.058 / 10.0
+
+
+# ---- BASELINE configs[4] at its own size: m = 4096, q = 65,536 ----
+C5 = os.path.join(os.path.dirname(__file__), "golden", "gpr_c5.npz")
+
+
+@pytest.mark.parametrize("path", ["tensor", "fp64"])
+def test_c5_full_size_vs_oracle(monkeypatch, path):
+    """fit (hand-written blocked binary64 Cholesky) + predict of all 65,536
+    queries against the oracle's values at 385 of them (tests/golden/
+    make_golden_gpr.py). Mean: 1e-9 relative (binary64 end to end). Standard
+    deviation: the binary64 variance path to 1e-9 relative; the tcgen05 path
+    (fp16 hi/lo operands, fp32 accumulation in TMEM, which truncates once per
+    MMA: a relative bias of ~5e-5 on ||L^-1 k||^2 at m = 4096) to 1e-6
+    absolute and 2e-5 relative."""
+    from bench import c5_data
+    gd = np.load(C5)
+    sizes, alphas, q, fixed = c5_data()
+    assert np.allclose([sizes.sum(), alphas.sum(), q.sum()], gd["sizes_sum"], rtol=0, atol=0)
+    monkeypatch.setenv("GADI_GPR_VAR", path)
+    m = g.gpr_fit(sizes, alphas, fixed=fixed)
+    mean, sd = m.predict(q)
+    t = m.timings()
+    assert t["variance_path"] == path
+    p = m.params()
+    np.testing.assert_allclose(p["lml"], gd["params"][4], rtol=1e-10)
+    idx = gd["idx"]
+    np.testing.assert_allclose(mean[idx], gd["mean"], rtol=1e-9, atol=0)
+    if path == "fp64":
+        np.testing.assert_allclose(sd[idx], gd["sd"], rtol=1e-9, atol=0)
+    else:
+        np.testing.assert_allclose(sd[idx], gd["sd"], rtol=2e-5, atol=0)
+        assert np.max(np.abs(sd[idx] - gd["sd"])) <= 1e-6
+    assert np.all(np.isfinite(sd)) and np.all(sd > 0)
+    m.close()
+
+
+def test_default_path_choice_follows_error_model():
+    """The tensor-core variance path is chosen only where its error bound holds
+    (m >= 1024 and sf2 / sn2 small enough); the reference's grid-mode fits
+    (sn2 down to 1e-10 var) stay in binary64."""
+    from bench import c5_data
+    sizes, alphas, q, fixed = c5_data()
+    m = g.gpr_fit(sizes[:2048], alphas[:2048], fixed=fixed)
+    m.predict(q[:512])
+    assert m.timings()["variance_path"] == "tensor"
+    m.close()
+    m = g.gpr_fit(sizes[:2048], alphas[:2048], fixed=(fixed[0], 1.0, 1e-9))
+    m.predict(q[:512])
+    assert m.timings()["variance_path"] == "fp64"
+    m.close()
+    m = g.gpr_fit(sizes[:300], alphas[:300], fixed=fixed)
+    m.predict(q[:512])
+    assert m.timings()["variance_path"] == "fp64"
+    m.close()
