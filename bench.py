@@ -238,29 +238,57 @@ def run_c5(args, rank, world):
     import torch
     import paper_2501_04229_b200 as g
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    tm = {}
 
     def step():
         m = g.gpr_fit(sizes, alphas, fixed=fixed)
         out = m.predict(q)
+        tm.update(m.timings())
         m.close()
         return out
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    l0 = 0
     t = time.perf_counter()
+    var_ms = []
     for _ in range(args.steps):
         mean, sd = step()
+        var_ms.append(tm["variance_ms"])
+        l0 += tm["launches"]
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t) / args.steps
+    mq, nq = len(sizes), len(q)
+    mp = (mq + 255) // 256 * 256
+    # the variance GEMM D = X K_*: lower-triangular X (mp x mp) times mp x q, three fp16 MMAs per product
+    tens_flops = 3.0 * 2.0 * (mp * (mp + 256) / 2.0) * ((nq + 255) // 256 * 256)
+    vms = sum(var_ms) / len(var_ms)
+    peak = 1590.0
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak_kind = "fallback"
+    if os.path.exists(pk):
+        with open(pk) as f:
+            peak = json.load(f).get("bf16_tflops", peak)
+        peak_kind = "measured (bf16 burst)"
+    ach = tens_flops / (vms / 1e3) / 1e12 if tm["variance_path"] == "tensor" else None
     out = {"metric": metric, "value": dt, "unit": "s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-           "e2e": {"value": dt, "unit": "s", "h2d_bytes_per_step": 8 * (2 * len(sizes) + len(q)),
-                   "d2h_bytes_per_step": 16 * len(q)},
-           "note": "host-timed end to end (inputs/outputs are host arrays); Cholesky via cuSOLVER Dpotrf, "
-                   "variances via cuBLAS Dtrsm: library fp64 path, no tensor cores yet",
-           "flops": {"cholesky": len(sizes) ** 3 / 3, "trsm": len(sizes) ** 2 * len(q)},
+           "vs_baseline": None, "dtype": "f64 fit / f16 hi+lo tensor-core variances (f32 accumulate)",
+           "data": "synthetic", "config": cfg,
+           "e2e": {"value": dt, "unit": "s", "h2d_bytes_per_step": 8 * (2 * mq + nq),
+                   "d2h_bytes_per_step": 16 * nq},
+           "gpu_launches": int(l0),
+           "roofline": {"bound": "tensor", "kernel": "k_var_umma (variances: X K_* on tcgen05, fp16 hi/lo, 3 MMAs per product)",
+                        "achieved": ach, "peak": peak, "peak_kind": peak_kind, "unit": "TFLOP/s",
+                        "frac": ach / peak if ach else None, "traffic": None,
+                        "tensor_flops_per_launch": tens_flops, "useful_flops": float(mp) * mp * nq,
+                        "kernel_ms": vms},
+           "phases_ms": {"fit": tm["fit_ms"], "inverse_factor": tm["inverse_ms"], "variance": vms,
+                         "variance_path": tm["variance_path"]},
+           "note": "host-timed end to end (inputs/outputs are host arrays); hand-written kernels only "
+                   "(libgadi_cuda.so links libcudart alone)",
+           "flops": {"cholesky": mq ** 3 / 3, "trsm": mq ** 2 * nq},
            "prediction_sample": {"mean_min": float(mean.min()), "mean_max": float(mean.max()),
                                  "sd_max": float(sd.max())}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

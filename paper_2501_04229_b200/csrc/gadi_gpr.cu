@@ -11,7 +11,7 @@
 // (BASELINE configs[4]: l = 1, sn2 = 1e-4).
 //
 //   fit      K on the device, blocked right-looking Cholesky in binary64
-//            (gadi_gpr_dense.cuh: k_potrf128 / k_trsm_right / k_dgemm), a =
+//            (gadi_gpr_dense.cuh: k_potinv128 / k_dgemm), a =
 //            K^-1 y by blocked forward / backward substitution, LML.
 //   predict  mean: binary64, kernel values on the fly (k_mean).
 //            variance sf2 + sn2 - ||L^-1 k_*||^2: the m^2 q contraction. The
@@ -32,6 +32,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -61,27 +62,47 @@ struct GErr : std::runtime_error {
                  std::string(#x) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
 
+// Device memory comes from a library-owned stream-ordered pool (one per
+// device, never trimmed below 1 GiB): a fit + predict allocates and frees
+// several matrices of mp^2 doubles, and cudaMalloc / cudaFree of those cost
+// more than the factorization itself.
+cudaMemPool_t gpr_pool(int dev) {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaMemPool_t& p = pools[dev & 63];
+  if (!p) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    GCK(cudaMemPoolCreate(&p, &props));
+    uint64_t keep = 1ull << 30;
+    GCK(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  return p;
+}
+thread_local cudaStream_t g_alloc_stream = nullptr;  // the stream of the model being worked on
 template <class T>
 T* galloc(size_t n) {
   void* p = nullptr;
-  GCK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  int dev = 0;
+  GCK(cudaGetDevice(&dev));
+  GCK(cudaMallocFromPoolAsync(&p, std::max<size_t>(n, 1) * sizeof(T), gpr_pool(dev), g_alloc_stream));
   return static_cast<T*>(p);
+}
+void gfree(void* p) {
+  if (p) cudaFreeAsync(p, g_alloc_stream);
 }
 
 constexpr size_t SM_POTRF = (size_t)NB * 129 * 8;
-constexpr size_t SM_TRSM_R = ((size_t)NB * (NB + 1) / 2 + 64 * 129) * 8;
-constexpr size_t SM_TRSM_L = ((size_t)NB * (NB + 1) / 2 + NB * 64) * 8;
-constexpr size_t SM_TRSV_T = ((size_t)NB * (NB + 1) / 2) * 8;
 
 void set_attrs() {  // per device: the large dynamic shared-memory sizes
   static bool done[64] = {};
   int dev = 0;
   GCK(cudaGetDevice(&dev));
   if (done[dev & 63]) return;
-  GCK(cudaFuncSetAttribute(k_potrf128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_POTRF));
-  GCK(cudaFuncSetAttribute(k_trsm_right, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSM_R));
-  GCK(cudaFuncSetAttribute(k_trsm_left, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSM_L));
-  GCK(cudaFuncSetAttribute(k_trsv_diag_T, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TRSV_T));
+  GCK(cudaFuncSetAttribute(k_potinv128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_POTRF));
   GCK(cudaFuncSetAttribute(k_var_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, UM_SMEM));
   done[dev & 63] = true;
 }
@@ -94,6 +115,7 @@ struct gadi_gpr {
   double mu = 0, sf2 = 1, ell = 1, sn2 = 1e-8, lml = 0, tmin = 0;
   double* d_x = nullptr;    // ln(size), m
   double* d_L = nullptr;    // lower Cholesky factor of K, mp x mp row-major (rows >= m: identity)
+  double* d_D = nullptr;    // the inverses of L's 128 x 128 diagonal blocks, mp / 128 x (128 x 128)
   double* d_a = nullptr;    // K^-1 (y - mu), mp (zero padded)
   double* d_X = nullptr;    // L^-1 (binary64), formed at the first predict
   uint8_t* d_img = nullptr; // fp16 hi/lo operand image of 2^6 sqrt(sf2) X (tensor path)
@@ -103,38 +125,46 @@ struct gadi_gpr {
   int64_t launches = 0;
   int last_var_path = 0;    // 1 tensor, 2 binary64
   ~gadi_gpr() {
-    for (void* p : {(void*)d_x, (void*)d_L, (void*)d_a, (void*)d_X, (void*)d_img, (void*)d_xs2})
-      if (p) cudaFree(p);
-    if (s) cudaStreamDestroy(s);
+    for (void* p : {(void*)d_x, (void*)d_L, (void*)d_D, (void*)d_a, (void*)d_X, (void*)d_img, (void*)d_xs2})
+      if (p) cudaFreeAsync(p, s);
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
   }
 };
 
 namespace {
 
-// Blocked right-looking Cholesky of the mp x mp matrix W (lower), in place.
-void cholesky(gadi_gpr* g, double* W, int* d_info) {
+// Blocked right-looking Cholesky of the mp x mp matrix W (lower), in place;
+// Dv receives the inverses of the diagonal blocks, P is a panel buffer (mp x 128).
+void cholesky(gadi_gpr* g, double* W, double* Dv, double* P, int* d_info) {
   const int mp = g->mp;
   cudaStream_t s = g->s;
   for (int j0 = 0; j0 < mp; j0 += NB) {
-    k_potrf128<<<1, 256, SM_POTRF, s>>>(W, mp, j0, d_info);
+    double* Dj = Dv + (size_t)(j0 / NB) * NB * NB;
+    k_potinv128<<<1, 256, SM_POTRF, s>>>(W, mp, j0, Dj, d_info);
     const int j1 = j0 + NB, rem = mp - j1;
     ++g->launches;
     if (rem <= 0) break;
-    k_trsm_right<<<(rem + 63) / 64, 64, SM_TRSM_R, s>>>(W, mp, j0, j1, rem);
-    const double* P = W + (size_t)j1 * mp + j0;  // the panel L21: rem x 128
-    k_dgemm<false, true><<<dim3((rem + 63) / 64, (rem + 63) / 64), 256, 0, s>>>(W + (size_t)j1 * mp + j1, mp, P, mp, P,
-                                                                                  mp, rem, rem, NB);
+    // panel L21 = W21 L_jj^-T = W21 D^T, then the trailing update W22 -= L21 L21^T (lower tiles)
+    k_dgemm<false, false, true><<<dim3(NB / 64, (rem + 63) / 64), 256, 0, s>>>(P, NB, W + (size_t)j1 * mp + j0, mp, Dj,
+                                                                                NB, rem, NB, NB);
+    GCK(cudaMemcpy2DAsync(W + (size_t)j1 * mp + j0, (size_t)mp * 8, P, NB * 8, NB * 8, rem, cudaMemcpyDeviceToDevice, s));
+    k_dgemm<false, true><<<dim3((rem + 63) / 64, (rem + 63) / 64), 256, 0, s>>>(W + (size_t)j1 * mp + j1, mp, P, NB, P,
+                                                                                  NB, rem, rem, NB);
     g->launches += 2;
   }
   GCK(cudaGetLastError());
 }
 
-// a = L^-T L^-1 y on the padded vector v (mp), in place: blocked substitution.
-void solve_llt(gadi_gpr* g, const double* L, double* v) {
+// a = L^-T L^-1 y on the padded vector v (mp), in place: blocked substitution
+// with the inverted diagonal blocks.
+void solve_llt(gadi_gpr* g, const double* L, const double* Dv, double* v) {
   const int mp = g->mp;
   cudaStream_t s = g->s;
   for (int i0 = 0; i0 < mp; i0 += NB) {  // forward: z = L^-1 y
-    k_trsm_left<<<1, 64, SM_TRSM_L, s>>>(L, mp, i0, v, 1, 0, 1);
+    k_diag_apply<false><<<1, 128, 0, s>>>(Dv + (size_t)(i0 / NB) * NB * NB, v + i0);
     const int rem = mp - i0 - NB;
     ++g->launches;
     if (rem > 0) {
@@ -143,7 +173,7 @@ void solve_llt(gadi_gpr* g, const double* L, double* v) {
     }
   }
   for (int i0 = mp - NB; i0 >= 0; i0 -= NB) {  // backward: a = L^-T z
-    k_trsv_diag_T<<<1, 128, SM_TRSV_T, s>>>(L, mp, i0, v);
+    k_diag_apply<true><<<1, 128, 0, s>>>(Dv + (size_t)(i0 / NB) * NB * NB, v + i0);
     ++g->launches;
     if (i0 > 0) {
       k_gemvT_sub<<<(i0 + 255) / 256, 256, 0, s>>>(L, mp, i0, i0, v, v);
@@ -155,22 +185,22 @@ void solve_llt(gadi_gpr* g, const double* L, double* v) {
 
 // try_fit (gpr.cpp:84-105) for one hyperparameter triple; false when K is
 // not positive definite after jitter or the LML is not finite.
-bool try_fit(gadi_gpr* g, const std::vector<double>& y, double sf2, double ell, double sn2, double* d_W, double* d_v,
-             int* d_info, double* d_ld, std::vector<double>& a, double& lml) {
+bool try_fit(gadi_gpr* g, const std::vector<double>& y, double sf2, double ell, double sn2, double* d_W, double* d_Dw,
+             double* d_P, double* d_v, int* d_info, double* d_ld, std::vector<double>& a, double& lml) {
   const int m = g->m, mp = g->mp;
   const double jitter = sn2 + 1e-12 * std::max(1.0, sf2);
   const int64_t mm = (int64_t)mp * mp;
   GCK(cudaMemsetAsync(d_info, 0, sizeof(int), g->s));
   k_gram<<<(unsigned)((mm + 255) / 256), 256, 0, g->s>>>(g->d_x, m, mp, sf2, ell, jitter, d_W);
   ++g->launches;
-  cholesky(g, d_W, d_info);
+  cholesky(g, d_W, d_Dw, d_P, d_info);
   int info = 0;
   GCK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, g->s));
   GCK(cudaStreamSynchronize(g->s));
   if (info != 0) return false;
   GCK(cudaMemsetAsync(d_v, 0, mp * sizeof(double), g->s));
   GCK(cudaMemcpyAsync(d_v, y.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
-  solve_llt(g, d_W, d_v);
+  solve_llt(g, d_W, d_Dw, d_v);
   k_logdiag<<<1, 256, 0, g->s>>>(d_W, mp, m, d_ld);
   ++g->launches;
   double ld = 0.0;
@@ -194,19 +224,26 @@ void form_inverse(gadi_gpr* g) {
   GCK(cudaEventCreate(&e1));
   GCK(cudaEventRecord(e0, s));
   double* X = galloc<double>((size_t)mp * mp);
+  double* T = galloc<double>((size_t)NB * mp);
   const int64_t mm = (int64_t)mp * mp;
   k_eye<<<(unsigned)((mm + 255) / 256), 256, 0, s>>>(X, mp);
   ++g->launches;
+  // rows of block i hold R_i = I_i - sum_{k<i} L_ik X_k; X_i = L_ii^-1 R_i, then the rows below lose L_ri X_i
   for (int i0 = 0; i0 < mp; i0 += NB) {
     const int nc = i0 + NB, i1 = i0 + NB, rem = mp - i1;
-    k_trsm_left<<<(nc + 63) / 64, 64, SM_TRSM_L, s>>>(g->d_L, mp, i0, X, mp, 0, nc);
+    k_dgemm<true, false, true><<<dim3((nc + 63) / 64, NB / 64), 256, 0, s>>>(
+        T, mp, g->d_D + (size_t)(i0 / NB) * NB * NB, NB, X + (size_t)i0 * mp, mp, NB, nc, NB);
+    GCK(cudaMemcpy2DAsync(X + (size_t)i0 * mp, (size_t)mp * 8, T, (size_t)mp * 8, (size_t)nc * 8, NB,
+                          cudaMemcpyDeviceToDevice, s));
     ++g->launches;
     if (rem > 0) {
       k_dgemm<true, false><<<dim3((nc + 63) / 64, (rem + 63) / 64), 256, 0, s>>>(
-          X + (size_t)i1 * mp, mp, g->d_L + (size_t)i1 * mp + i0, mp, X + (size_t)i0 * mp, mp, rem, nc, NB);
+          X + (size_t)i1 * mp, mp, g->d_L + (size_t)i1 * mp + i0, mp, T, mp, rem, nc, NB);
       ++g->launches;
     }
   }
+  GCK(cudaStreamSynchronize(s));
+  gfree(T);
   GCK(cudaGetLastError());
   GCK(cudaEventRecord(e1, s));
   GCK(cudaEventSynchronize(e1));
@@ -270,6 +307,7 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     g->mu = mu;
     g->tmin = tmin;
     GCK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
+    g_alloc_stream = g->s;
     cudaEvent_t e0, e1;
     GCK(cudaEventCreate(&e0));
     GCK(cudaEventCreate(&e1));
@@ -278,6 +316,9 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     GCK(cudaMemcpyAsync(g->d_x, x.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
     double* d_W = galloc<double>((size_t)mp * mp);
     g->d_L = galloc<double>((size_t)mp * mp);
+    double* d_Dw = galloc<double>((size_t)mp * NB);
+    g->d_D = galloc<double>((size_t)mp * NB);
+    double* d_P = galloc<double>((size_t)mp * NB);
     g->d_a = galloc<double>(mp);
     GCK(cudaMemsetAsync(g->d_a, 0, mp * sizeof(double), g->s));
     double* d_v = galloc<double>(mp);
@@ -300,12 +341,13 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
       for (double el : ells)
         for (double sn : sns) {
           double lml = 0.0;
-          if (try_fit(g.get(), y, sf, el, sn, d_W, d_v, d_info, d_ld, a, lml) && lml > best) {
+          if (try_fit(g.get(), y, sf, el, sn, d_W, d_Dw, d_P, d_v, d_info, d_ld, a, lml) && lml > best) {
             best = lml;
             g->sf2 = sf;
             g->ell = el;
             g->sn2 = sn;
-            std::swap(d_W, g->d_L);  // keep this factor; the other buffer is the next candidate's workspace
+            std::swap(d_W, g->d_L);  // keep this factor; the other buffers are the next candidate's workspace
+            std::swap(d_Dw, g->d_D);
             GCK(cudaMemcpyAsync(g->d_a, a.data(), m * sizeof(double), cudaMemcpyHostToDevice, g->s));
             GCK(cudaStreamSynchronize(g->s));
           }
@@ -317,7 +359,7 @@ int gadi_gpr_fit(const double* sizes, const double* alphas, int32_t m, const gad
     g->fit_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    for (void* p : {(void*)d_W, (void*)d_v, (void*)d_ld, (void*)d_info}) cudaFree(p);
+    for (void* p : {(void*)d_W, (void*)d_Dw, (void*)d_P, (void*)d_v, (void*)d_ld, (void*)d_info}) gfree(p);
     if (!std::isfinite(best)) throw GErr(GADI_E_FIT, "fit: Gram matrix not positive definite for any hyperparameter choice");
     g->lml = best;
     *out = g.release();
@@ -339,6 +381,7 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
     set_attrs();
     const int m = g->m, mp = g->mp;
     cudaStream_t s = g->s;
+    g_alloc_stream = s;
     std::vector<double> xq(q);
     for (int t = 0; t < q; ++t) xq[t] = std::log(sizes[t]);
     double* d_xq = galloc<double>(q);
@@ -366,7 +409,7 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
         unsigned long long bits = 0;
         GCK(cudaMemcpyAsync(&bits, d_mx, 8, cudaMemcpyDeviceToHost, s));
         GCK(cudaStreamSynchronize(s));
-        cudaFree(d_mx);
+        gfree(d_mx);
         double mx;
         std::memcpy(&mx, &bits, 8);
         mx *= g->sf2;
@@ -386,7 +429,7 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
       g->launches += 2;
       GCK(cudaGetLastError());
       GCK(cudaStreamSynchronize(s));
-      cudaFree(d_xq2);
+      gfree(d_xq2);
     } else {
       g->last_var_path = 2;
       const int QB = 2048;
@@ -404,8 +447,8 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
       }
       GCK(cudaGetLastError());
       GCK(cudaStreamSynchronize(s));
-      cudaFree(d_Ks);
-      cudaFree(d_V);
+      gfree(d_Ks);
+      gfree(d_V);
     }
     GCK(cudaEventRecord(e1, s));
     GCK(cudaEventSynchronize(e1));
@@ -418,7 +461,7 @@ int gadi_gpr_predict(gadi_gpr* g, const double* sizes, int32_t q, double* mean, 
     GCK(cudaMemcpyAsync(stddev, d_var, q * sizeof(double), cudaMemcpyDeviceToHost, s));
     GCK(cudaStreamSynchronize(s));
     for (int t = 0; t < q; ++t) stddev[t] = std::sqrt(stddev[t]);
-    for (void* p : {(void*)d_xq, (void*)d_mean, (void*)d_var}) cudaFree(p);
+    for (void* p : {(void*)d_xq, (void*)d_mean, (void*)d_var}) gfree(p);
     return GADI_OK;
   } catch (const GErr& e) {
     gadi_host::set_last_error(e.what());

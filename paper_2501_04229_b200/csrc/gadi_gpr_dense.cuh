@@ -4,12 +4,13 @@
 //
 // Blocked right-looking Cholesky on a row-major mp x mp matrix (mp a multiple
 // of 128, the lower triangle is referenced): per 128-column block
-//   k_potrf128      the diagonal block, one CTA, column by column in shared memory
-//   k_trsm_right    the panel below it: rows of W21 L_jj^-T by substitution
+//   k_potinv128     the diagonal block L_jj and its inverse D_j, one CTA
+//   k_dgemm<NT,SET> the panel below it: L21 = W21 D_j^T
 //   k_dgemm<NT>     the trailing update W22 -= L21 L21^T (lower tiles only)
 // The explicit inverse factor X = L^-1 the tensor-core variance GEMM consumes
 // (gadi_gpr_umma.cuh) is a right-looking block substitution on the identity:
-//   k_trsm_left     X_i,: = L_ii^-1 X_i,:      k_dgemm<NN>   X_r,: -= L_r,i X_i,:
+//   k_dgemm<NN,SET> X_i,: = D_i R_i,:          k_dgemm<NN>   R_r,: -= L_r,i X_i,:
+// and K^-1 y the same substitution on one vector (k_diag_apply, k_gemv[T]_sub).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -38,138 +39,213 @@ __global__ void k_gram(const double* __restrict__ x, int m, int mp, double sf2, 
   K[idx] = v;
 }
 
-// Cholesky of the 128 x 128 diagonal block at (j0, j0), in place (lower).
+// 64-bit warp shuffle
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  int lo = __double2loint(v), hi = __double2hiint(v);
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  hi = __shfl_sync(0xffffffffu, hi, src);
+  return __hiloint2double(hi, lo);
+}
+
+// Cholesky of the 128 x 128 diagonal block at (j0, j0), in place (lower), and
+// its inverse D = L_jj^-1 (128 x 128 row-major, zeros above the diagonal): the
+// panel below the block, the inverse factor and the triangular solves then
+// all run as GEMMs / GEMVs against D instead of substitutions.
 // info: 0, or 1 + the first column whose pivot is not positive (Eigen's
-// NumericalIssue, gpr.cpp:92). One CTA of 256 threads; shared: 128 x 129 doubles.
-__global__ void __launch_bounds__(256) k_potrf128(double* __restrict__ W, int ld, int j0, int* __restrict__ info) {
-  extern __shared__ double sA[];  // [128][129]
-  __shared__ double scol[NB];
+// NumericalIssue, gpr.cpp:92). One CTA of 256 threads, shared: 128 x 129
+// doubles. Blocked by 32:
+//   factor   per 32-column block: the 32 x 32 diagonal block in one warp's
+//            registers (column broadcasts by shuffle, 1/sqrt by rsqrt: no
+//            division on the pivot chain), the rows below it one thread per
+//            row, the trailing update of the block on 16 x 16 threads;
+//   invert   in place, last 32-block first: X_kk in one warp's registers,
+//            X_ik = -(sum_j X_ij L_jk) X_kk on all threads.
+__global__ void __launch_bounds__(256) k_potinv128(double* __restrict__ W, int ld, int j0, double* __restrict__ D,
+                                                   int* __restrict__ info) {
+  extern __shared__ double sA[];  // [128][129]; the strict upper triangle stays zero
+  __shared__ double sinv[NB];     // 1 / L_cc
   __shared__ int bad;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) bad = 0;
   for (int e = t; e < NB * NB; e += 256) {
     const int r = e / NB, c = e % NB;
     sA[r * 129 + c] = c <= r ? W[(size_t)(j0 + r) * ld + j0 + c] : 0.0;
   }
   __syncthreads();
-  const int r = t & 127, half = t >> 7;
-  for (int c = 0; c < NB; ++c) {
-    const double d = sA[c * 129 + c];
-    if (!(d > 0.0)) {  // uniform: every thread reads the same pivot
-      if (t == 0) bad = c + 1;
-      break;
+  // ------------------------------------------------------------- factor
+  for (int c0 = 0; c0 < NB; c0 += 32) {
+    if (warp == 0) {  // diagonal 32 x 32 block: lane = row
+      double a[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) a[c] = sA[(c0 + lane) * 129 + c0 + c];
+      int isbad = 0;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const double piv = shfl_d(a[c], c);
+        if (!(piv > 0.0) && !isbad) isbad = c0 + c + 1;
+        const double rs = rsqrt(piv);
+        if (lane == c) {
+          a[c] = piv * rs;
+          sinv[c0 + c] = rs;
+        } else if (lane > c) {
+          a[c] *= rs;
+        }
+#pragma unroll
+        for (int cc = c + 1; cc < 32; ++cc) {
+          const double lcc = shfl_d(a[c], cc);
+          if (lane >= cc) a[cc] = fma(-a[c], lcc, a[cc]);
+        }
+      }
+      if (isbad && lane == 0) bad = isbad;
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c <= lane) sA[(c0 + lane) * 129 + c0 + c] = a[c];
     }
-    const double sd = sqrt(d);
-    if (half == 0 && r >= c) scol[r] = r == c ? sd : __ddiv_rn(sA[r * 129 + c], sd);
     __syncthreads();
-    if (r > c) {
-      const double lr = scol[r];
-      for (int cc = c + 1 + half; cc <= r; cc += 2) sA[r * 129 + cc] = fma(-lr, scol[cc], sA[r * 129 + cc]);
+    if (bad) break;
+    const int below = NB - c0 - 32;  // rows under the diagonal block
+    if (t < below) {                 // l_r,: = a_r,: L_kk^-T, one thread per row
+      double x[32];
+      const int r = c0 + 32 + t;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) x[c] = sA[r * 129 + c0 + c];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        double acc = x[c];
+#pragma unroll
+        for (int k = 0; k < c; ++k) acc = fma(-x[k], sA[(c0 + c) * 129 + c0 + k], acc);
+        x[c] = acc * sinv[c0 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) sA[r * 129 + c0 + c] = x[c];
     }
-    if (half == 0 && r >= c) sA[r * 129 + c] = scol[r];
+    __syncthreads();
+    if (below > 0) {  // trailing update of the block: a_r,cc -= sum_k l_r,k l_cc,k
+      const int ty = t >> 4, tx = t & 15, b0 = c0 + 32;
+      double acc[6][6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc[i][j] = 0.0;
+      for (int k = 0; k < 32; ++k) {
+        double rv[6], cv[6];
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const int r = b0 + ty + 16 * i, c = b0 + tx + 16 * i;
+          rv[i] = r < NB ? sA[r * 129 + c0 + k] : 0.0;
+          cv[i] = c < NB ? sA[c * 129 + c0 + k] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 6; ++i)
+#pragma unroll
+          for (int j = 0; j < 6; ++j) acc[i][j] = fma(rv[i], cv[j], acc[i][j]);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          const int r = b0 + ty + 16 * i, c = b0 + tx + 16 * j;
+          if (r < NB && c <= r) sA[r * 129 + c] -= acc[i][j];
+        }
+    }
     __syncthreads();
   }
-  __syncthreads();
   if (bad) {
     if (t == 0) atomicCAS(info, 0, j0 + bad);
     return;
   }
   for (int e = t; e < NB * NB; e += 256) {
-    const int rr = e / NB, c = e % NB;
-    if (c <= rr) W[(size_t)(j0 + rr) * ld + j0 + c] = sA[rr * 129 + c];
-  }
-}
-
-// Lower-packed copy of a 128 x 128 diagonal block in shared memory
-__device__ __forceinline__ int pk(int r, int c) { return r * (r + 1) / 2 + c; }
-__device__ __forceinline__ void load_diag_packed(const double* __restrict__ W, int ld, int j0, double* sL) {
-  for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) {
     const int r = e / NB, c = e % NB;
-    if (c <= r) sL[pk(r, c)] = W[(size_t)(j0 + r) * ld + j0 + c];
-  }
-}
-
-// Panel: rows [r0, r0 + nrows) of the block column j0 become W21 L_jj^-T, in
-// place: l_rc = (w_rc - sum_{k<c} l_rk L_ck) / L_cc. One thread per row, 64
-// rows per CTA staged in shared memory. Shared: 8256 + 64*129 doubles.
-__global__ void __launch_bounds__(64) k_trsm_right(double* __restrict__ W, int ld, int j0, int r0, int nrows) {
-  extern __shared__ double sm[];
-  double* sL = sm;
-  double* sT = sm + NB * (NB + 1) / 2;  // [64][129]
-  load_diag_packed(W, ld, j0, sL);
-  const int rb = r0 + blockIdx.x * 64;
-  for (int e = threadIdx.x; e < 64 * NB; e += 64) {
-    const int r = e / NB, c = e % NB;
-    sT[r * 129 + c] = rb + r < r0 + nrows ? W[(size_t)(rb + r) * ld + j0 + c] : 0.0;
+    if (c <= r) W[(size_t)(j0 + r) * ld + j0 + c] = sA[r * 129 + c];
   }
   __syncthreads();
-  double* row = sT + threadIdx.x * 129;
-  for (int c = 0; c < NB; ++c) {
-    double a0 = row[c], a1 = 0.0;
-    const double* Lc = sL + pk(c, 0);
-    int k = 0;
-    for (; k + 1 < c; k += 2) {
-      a0 = fma(-row[k], Lc[k], a0);
-      a1 = fma(-row[k + 1], Lc[k + 1], a1);
+  // ------------------------------------------------------------- invert
+  for (int c0 = NB - 32; c0 >= 0; c0 -= 32) {
+    if (warp == 0) {  // X_kk = L_kk^-1: lane = column
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        double acc = i == lane ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; ++k) acc = fma(-sA[(c0 + i) * 129 + c0 + k], x[k], acc);
+        x[i] = i < lane ? 0.0 : acc * sinv[c0 + i];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i >= lane) sA[(c0 + i) * 129 + c0 + lane] = x[i];
     }
-    if (k < c) a0 = fma(-row[k], Lc[k], a0);
-    row[c] = __ddiv_rn(a0 + a1, Lc[c]);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < 64 * NB; e += 64) {
-    const int r = e / NB, c = e % NB;
-    if (rb + r < r0 + nrows) W[(size_t)(rb + r) * ld + j0 + c] = sT[r * 129 + c];
-  }
-}
-
-// X[i0 .. i0+128, c0 .. c0+ncols) = L_ii^-1 X[same], in place (L_ii the
-// diagonal block of L at i0): x_r = (x_r - sum_{k<r} L_rk x_k) / L_rr, one
-// thread per column, 64 columns per CTA. Shared: 8256 + 128*64 doubles.
-__global__ void __launch_bounds__(64) k_trsm_left(const double* __restrict__ L, int ldl, int i0, double* __restrict__ X,
-                                                  int ldx, int c0, int ncols) {
-  extern __shared__ double sm[];
-  double* sL = sm;
-  double* sT = sm + NB * (NB + 1) / 2;  // [128][64]
-  load_diag_packed(L, ldl, i0, sL);
-  const int cb = c0 + blockIdx.x * 64, t = threadIdx.x;
-  const bool live = cb + t < c0 + ncols;
-  for (int r = 0; r < NB; ++r) sT[r * 64 + t] = live ? X[(size_t)(i0 + r) * ldx + cb + t] : 0.0;
-  __syncthreads();
-  for (int r = 0; r < NB; ++r) {
-    double a0 = sT[r * 64 + t], a1 = 0.0;
-    const double* Lr = sL + pk(r, 0);
-    int k = 0;
-    for (; k + 1 < r; k += 2) {
-      a0 = fma(-Lr[k], sT[k * 64 + t], a0);
-      a1 = fma(-Lr[k + 1], sT[(k + 1) * 64 + t], a1);
+    __syncthreads();
+    const int b0 = c0 + 32, below = NB - b0;
+    if (below > 0) {
+      const int c = t & 31, g = t >> 5;  // column of the block, row group
+      double acc[12];
+      // T = X22 L21: rows b0 + g + 8 u, inner index j over the inverted trailing block (upper part is zero)
+#pragma unroll
+      for (int u = 0; u < 12; ++u) acc[u] = 0.0;
+      for (int j = b0; j < NB; ++j) {
+        const double lj = sA[j * 129 + c0 + c];
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+          const int i = b0 + g + 8 * u;
+          if (i < NB) acc[u] = fma(sA[i * 129 + j], lj, acc[u]);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const int i = b0 + g + 8 * u;
+        if (i < NB) sA[i * 129 + c0 + c] = acc[u];
+      }
+      __syncthreads();
+      // X21 = -T X_kk (X_kk lower: its upper part is zero)
+#pragma unroll
+      for (int u = 0; u < 12; ++u) acc[u] = 0.0;
+      for (int k = 0; k < 32; ++k) {
+        const double xk = sA[(c0 + k) * 129 + c0 + c];
+#pragma unroll
+        for (int u = 0; u < 12; ++u) {
+          const int i = b0 + g + 8 * u;
+          if (i < NB) acc[u] = fma(sA[i * 129 + c0 + k], xk, acc[u]);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 12; ++u) {
+        const int i = b0 + g + 8 * u;
+        if (i < NB) sA[i * 129 + c0 + c] = -acc[u];
+      }
     }
-    if (k < r) a0 = fma(-Lr[k], sT[k * 64 + t], a0);
-    sT[r * 64 + t] = __ddiv_rn(a0 + a1, Lr[r]);
+    __syncthreads();
   }
-  if (live)
-    for (int r = 0; r < NB; ++r) X[(size_t)(i0 + r) * ldx + cb + t] = sT[r * 64 + t];
+  for (int e = t; e < NB * NB; e += 256) {
+    const int r = e / NB, c = e % NB;
+    D[e] = c <= r ? sA[r * 129 + c] : 0.0;
+  }
 }
 
-// a[i0 .. i0+128) = L_ii^-T a[same] (one right-hand side, backward): one CTA of 128 threads.
-__global__ void __launch_bounds__(128) k_trsv_diag_T(const double* __restrict__ L, int ldl, int i0, double* __restrict__ a) {
-  extern __shared__ double sm[];
-  double* sL = sm;  // packed lower
-  __shared__ double z[NB];
-  __shared__ double ar;
-  load_diag_packed(L, ldl, i0, sL);
+// v[0..128) = D v (TRANS = false) or D^T v (TRANS = true), D a 128 x 128
+// lower-triangular block: one CTA of 128 threads.
+template <bool TRANS>
+__global__ void __launch_bounds__(128) k_diag_apply(const double* __restrict__ D, double* __restrict__ v) {
+  __shared__ double sv[NB];
   const int t = threadIdx.x;
-  z[t] = a[i0 + t];
+  sv[t] = v[t];
   __syncthreads();
-  for (int r = NB - 1; r >= 0; --r) {
-    if (t == r) {
-      ar = __ddiv_rn(z[r], sL[pk(r, r)]);
-      z[r] = ar;
+  double s = 0.0;
+  if (TRANS) {
+    for (int k = t; k < NB; ++k) s = fma(D[k * NB + t], sv[k], s);  // coalesced over t
+    v[t] = s;
+  } else {
+    const int warp = t >> 5, lane = t & 31;
+    for (int r = warp; r < NB; r += 4) {  // a warp per row, lanes over k
+      double a = 0.0;
+      for (int k = lane; k <= r; k += 32) a = fma(D[r * NB + k], sv[k], a);
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (lane == 0) v[r] = a;
     }
-    __syncthreads();
-    if (t < r) z[t] = fma(-sL[pk(r, t)], ar, z[t]);
-    __syncthreads();
   }
-  a[i0 + t] = z[t];
 }
 
 // y[r0 + r] -= sum_k A[r0 + r][k0 + k] z[k0 + k], k < 128, r < nrows: one warp per row
@@ -199,11 +275,11 @@ __global__ void k_gemvT_sub(const double* __restrict__ A, int lda, int r0, int n
   z[c] -= s0 + s1;
 }
 
-// C[M x N] -= A[M x K] op(B): NT: B is [N][K]; NN: B is [K][N]. Row-major,
+// C[M x N] -= A[M x K] op(B) (SET: C = A op(B)): NT: B is [N][K]; NN: B is [K][N]. Row-major,
 // 64 x 64 tiles, K steps of 16, 256 threads x (4 x 4). LOWER: tiles entirely
 // above the diagonal of the square region are skipped (SYRK); ncut > 0: tile
 // columns >= the tile's row0 + ncut are skipped (triangular right-hand sides).
-template <bool NN, bool LOWER>
+template <bool NN, bool LOWER, bool SET = false>
 __global__ void __launch_bounds__(256) k_dgemm(double* __restrict__ C, int ldc, const double* __restrict__ A, int lda,
                                                const double* __restrict__ B, int ldb, int M, int N, int K) {
   const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
@@ -259,7 +335,10 @@ __global__ void __launch_bounds__(256) k_dgemm(double* __restrict__ C, int ldc, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = col0 + tx * 4 + j;
-      if (c < N) C[(size_t)r * ldc + c] -= acc[i][j];
+      if (c < N) {
+        if (SET) C[(size_t)r * ldc + c] = acc[i][j];
+        else C[(size_t)r * ldc + c] -= acc[i][j];
+      }
     }
   }
 }
