@@ -449,10 +449,14 @@ def main():
         solve_s, e2e_s = t.tolist()
     peak, peak_kind = load_peaks()
     # inner CG sweep: B_CG = 11 N s_r bytes per iteration; a
-    # sparse H adds nnz(H) (s_r value + 4 index) + 4 (N+1) row bytes per SpMV
+    # sparse H adds, per SpMV, nnz(H) (s_r value + index) + the row lengths. The
+    # index is what the SELL image stores: a 2-byte column offset when the band
+    # is below 2^15 (configs[3]: +-4096), else a 4-byte column; row lengths are
+    # 2 bytes per row (SURVEY's 6 B/nnz int32-CSR figure would overstate it)
     bytes_it = 11 * N * wl["s_r"]
     if band:
-        bytes_it += sysx.nnz()[1] * (wl["s_r"] + 4) + 4 * (N + 1)
+        idx_bytes = 2 if wl["band"] < 32768 else 4
+        bytes_it += sysx.nnz()[1] * (wl["s_r"] + idx_bytes) + 2 * N
     cg_gbs = bytes_it * h_it / (h_ms / 1e3) / 1e9 if h_ms > 0 else None
     roof_kernel = ("inner CG iteration (p-update, SELL spmv + p.q, axpys + dots)" if band
                    else "inner CG iteration (spmv+p-update, axpys+dots)")

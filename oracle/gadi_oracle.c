@@ -445,6 +445,13 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
   rounded_values(A0, fmt, &A, vb);
   const double target = eps * stop_norm;
   const int m = restart > 1 ? restart : 1;
+  /* The GADI_ACCUM_FP32 extension mode (af != fmt; not in the reference) runs the
+   * Arnoldi step as the device's fused passes do: classical Gram-Schmidt (all
+   * dots of a step from the same w, then ONE update pass w -= sum h_i v_i in af
+   * with a single rounding to fmt) and unscaled norms sqrt(dot(w, w)) in af.
+   * The reference's modified Gram-Schmidt and max-scaled norm2
+   * (inner_solver.cpp:121-126) stay as they are for af == fmt. */
+  const int fused = af != fmt && !getenv("ORC_GMRES_MGS");
   double* V = (double*)malloc((size_t)(m + 1) * (size_t)n * 8);
   double* r = (double*)malloc((size_t)n * 8);
   double* w = (double*)malloc((size_t)n * 8);
@@ -462,7 +469,7 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
       status = GADI_INNER_OVERFLOW;
       break;
     }
-    const double beta = orc_norm2(r, n, af);
+    const double beta = fused ? R(sqrt(orc_dot(r, r, n, af)), af) : orc_norm2(r, n, af);
     if (orc_norm2_64(r, n) <= target) {
       status = GADI_INNER_CONVERGED;
       break;
@@ -478,12 +485,23 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
     int j = 0, happy = 0;
     for (; j < m && total < max_inner; ++j, ++total) {
       matvec_s(&A, V + (size_t)j * n, af, fmt, w);
-      for (int i = 0; i <= j; ++i) {
-        const double h = orc_dot(w, V + (size_t)i * n, n, af);
-        HC(i, j) = h;
-        axpy_s(-h, V + (size_t)i * n, w, n, af, fmt, w);
+      double h1;
+      if (fused) { /* classical Gram-Schmidt: every h_ij from the same w, one update pass */
+        for (int i = 0; i <= j; ++i) HC(i, j) = orc_dot(w, V + (size_t)i * n, n, af);
+        for (int64_t e = 0; e < n; ++e) {
+          double acc = w[e];
+          for (int i = 0; i <= j; ++i) acc = R(acc + R(-HC(i, j) * V[(size_t)i * n + e], af), af);
+          w[e] = R(acc, fmt);
+        }
+        h1 = R(sqrt(orc_dot(w, w, n, af)), af);
+      } else {
+        for (int i = 0; i <= j; ++i) {
+          const double h = orc_dot(w, V + (size_t)i * n, n, af);
+          HC(i, j) = h;
+          axpy_s(-h, V + (size_t)i * n, w, n, af, fmt, w);
+        }
+        h1 = orc_norm2(w, n, af);
       }
-      const double h1 = orc_norm2(w, n, af);
       HC(j + 1, j) = h1;
       if (!isfinite(h1)) {
         status = GADI_INNER_OVERFLOW;

@@ -637,7 +637,14 @@ int gadi_cuda_destroy(gadi_handle* h) {
   for (cudaEvent_t ev : {h->ev0, h->ev1, h->evA, h->evB, h->evC})
     if (ev) cudaEventDestroy(ev);
   for (auto ev : h->ring) cudaEventDestroy(ev);
-  if (h->stream) cudaStreamDestroy(h->stream);
+  if (h->stream) {
+    cudaStreamSynchronize(h->stream);
+    cudaStreamDestroy(h->stream);
+  }
+  try {
+    engine_pool_trim(h->device);  // unused work-vector memory back to the device (other live handles keep theirs)
+  } catch (...) {
+  }
   delete h;
   return GADI_OK;
 }

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/gadi_cuda.h"
@@ -217,11 +218,7 @@ inline bool make_st25(int64_t n, int tsize, int nin, St25Geo& g, int64_t target_
 
 template <class P, int CPT>
 inline void launch_st25_cpt(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
-  static bool attr = false;  // one attribute call per instantiation
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_st25<P, CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  smem_attr(k_st25<P, CPT>, 200 * 1024);  // per device, once (monotonic cap, locked)
   k_st25<P, CPT><<<g.nblk, g.threads, g.smem, s>>>(pol, g, rd, st);
 }
 template <class P>
@@ -252,23 +249,27 @@ inline bool make_st25h(int64_t n, int nin, St25Geo& g, int64_t i0, int64_t i1) {
 
 template <class P, int CPT, int MINB>
 inline void launch_st25h_cpt(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_st25h<P, CPT, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  // persistent CTAs: as many as are resident at once (cached per shape)
-  static size_t c_smem = 0;
-  static int c_threads = 0, c_res = 0;
-  if (c_smem != g.smem || c_threads != g.threads) {
-    int dev = 0, sms = 0, per = 0;
+  smem_attr(k_st25h<P, CPT, MINB>, 200 * 1024);
+  // persistent CTAs: as many as are resident at once, cached per (device,
+  // shared memory, threads) under a lock (handles on several devices, and the
+  // training-set probe threads, launch concurrently)
+  int c_res = 0;
+  {
+    static std::mutex mu;
+    static std::map<std::tuple<int, size_t, int>, int> cache;
+    int dev = 0;
     CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_st25h<P, CPT, MINB>, g.threads, g.smem));
-    c_smem = g.smem;
-    c_threads = g.threads;
-    c_res = std::max(1, per) * sms;
-    if (const char* e = std::getenv("GADI_ST25H_GRID")) c_res = std::max(1, std::atoi(e));  // tuning knob
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find({dev, g.smem, g.threads});
+    if (it == cache.end()) {
+      int sms = 0, per = 0;
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_st25h<P, CPT, MINB>, g.threads, g.smem));
+      int res = std::max(1, per) * sms;
+      if (const char* e = std::getenv("GADI_ST25H_GRID")) res = std::max(1, std::atoi(e));  // tuning knob
+      it = cache.emplace(std::make_tuple(dev, g.smem, g.threads), res).first;
+    }
+    c_res = it->second;
   }
   const int grid = std::min(g.nblk, c_res);
   k_st25h<P, CPT, MINB><<<grid, g.threads, g.smem, s>>>(pol, g, rd, st);
@@ -689,6 +690,28 @@ struct EngineBase {
 
 namespace gadi_host {
 
+// The engines' work vectors come from a library-owned stream-ordered pool per
+// device (the process's default pool and its attributes are left alone). It
+// keeps what a solve used for the next one; gadi_cuda_destroy trims it to 256 MB
+// (engine_pool_trim) so a destroyed C3-sized engine does not hold its GBs.
+inline cudaMemPool_t engine_pool(int dev) {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaMemPool_t& p = pools[dev & 63];
+  if (!p) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    CK(cudaMemPoolCreate(&p, &props));
+    uint64_t keep = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  return p;
+}
+inline void engine_pool_trim(int dev) { cudaMemPoolTrimTo(engine_pool(dev), (size_t)256 << 20); }  // keep 256 MB for the next small handle
+
 template <class Op, class T, class C>
 struct Engine final : EngineBase {
   gadi_handle* h;
@@ -721,16 +744,8 @@ struct Engine final : EngineBase {
   // gadi_ir_solve does (solver.cpp:75) -- costs no cudaMalloc/cudaFree and no
   // device-wide synchronisation.
   T* salloc(int64_t n) {
-    static std::once_flag once[64];
-    std::call_once(once[h->device & 63], [&] {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, h->device) == cudaSuccess) {
-        uint64_t keep = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-    });
     T* p = nullptr;
-    CK(cudaMallocAsync((void**)&p, (size_t)n * sizeof(T), h->stream));
+    CK(cudaMallocFromPoolAsync((void**)&p, (size_t)n * sizeof(T), engine_pool(h->device), h->stream));
     return p;
   }
 

@@ -813,7 +813,7 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
     f->kl = f->ku = h->n > 1 ? h->n * h->n : 0;  // the i-1 / i+1 neighbours
   } else {  // lower/upper_bandwidth of the union pattern (sparse.cpp:142-154)
     unsigned long long* bw = nullptr;
-    CK(cudaMallocAsync((void**)&bw, 16, h->stream));
+    CK(cudaMallocFromPoolAsync((void**)&bw, 16, engine_pool(f->device), h->stream));
     CK(cudaMemsetAsync(bw, 0, 16, h->stream));
     const auto pt = h->part(which);  // the operator's own pattern (the HSS union, or an explicit M / N)
     k_bandwidths<<<(unsigned)((h->N + 255) / 256), 256, 0, h->stream>>>(h->N, pt.rp, pt.ci, bw);
@@ -829,16 +829,16 @@ LuFactor* lu_factor_build(gadi_handle* h, int which, double alpha, int ur, int* 
   const size_t es = ur == GADI_DOUBLE ? 8 : 4;
   cudaStream_t s = h->stream;
   // stream-ordered allocations: concurrent handles (gadi_train.cu) never wait on each other here
-  CK(cudaMallocAsync(&f->ab, (size_t)f->ldab * (size_t)f->N * es, s));
+  CK(cudaMallocFromPoolAsync(&f->ab, (size_t)f->ldab * (size_t)f->N * es, engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->ab, 0, (size_t)f->ldab * (size_t)f->N * es, s));
-  CK(cudaMallocAsync((void**)&f->ipiv, (size_t)f->N * sizeof(int32_t), s));
-  CK(cudaMallocAsync(&f->xw, (size_t)f->N * es, s));
-  CK(cudaMallocAsync((void**)&f->err, 4 * sizeof(int), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->ipiv, (size_t)f->N * sizeof(int32_t), engine_pool(f->device), s));
+  CK(cudaMallocFromPoolAsync(&f->xw, (size_t)f->N * es, engine_pool(f->device), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->err, 4 * sizeof(int), engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
-  CK(cudaMallocAsync((void**)&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->flags, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->flags, 0, (size_t)((f->N + 31) / 32 + 1) * sizeof(unsigned), s));
   f->ticket = f->flags + (f->N + 31) / 32;
-  CK(cudaMallocAsync((void**)&f->xt, (size_t)f->N * 8, s));
+  CK(cudaMallocFromPoolAsync((void**)&f->xt, (size_t)f->N * 8, engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->xt, 0, (size_t)f->N * 8, s));  // epoch 0 on every word
   f->bad = f->err + 2;
   const int64_t ldoff = f->kl + f->ku, N = f->N;
@@ -917,21 +917,21 @@ LuFactor* lu_factor_host_csr(int device, cudaStream_t s, int64_t N, const int64_
     if (!diag) band[(size_t)(i * f->ldab + ldoff)] = hround(alpha, ur);
   }
   const size_t es = ur == GADI_DOUBLE ? 8 : 4;
-  CK(cudaMallocAsync(&f->ab, band.size() * es, s));
+  CK(cudaMallocFromPoolAsync(&f->ab, band.size() * es, engine_pool(f->device), s));
   if (ur == GADI_DOUBLE) {
     CK(cudaMemcpyAsync(f->ab, band.data(), band.size() * 8, cudaMemcpyHostToDevice, s));
   } else {
     std::vector<float> bf(band.begin(), band.end());
     CK(cudaMemcpyAsync(f->ab, bf.data(), bf.size() * 4, cudaMemcpyHostToDevice, s));
   }
-  CK(cudaMallocAsync((void**)&f->ipiv, (size_t)N * sizeof(int32_t), s));
-  CK(cudaMallocAsync(&f->xw, (size_t)N * es, s));
-  CK(cudaMallocAsync((void**)&f->err, 4 * sizeof(int), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->ipiv, (size_t)N * sizeof(int32_t), engine_pool(f->device), s));
+  CK(cudaMallocFromPoolAsync(&f->xw, (size_t)N * es, engine_pool(f->device), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->err, 4 * sizeof(int), engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->err, 0, 4 * sizeof(int), s));
-  CK(cudaMallocAsync((void**)&f->flags, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
+  CK(cudaMallocFromPoolAsync((void**)&f->flags, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->flags, 0, (size_t)((N + 31) / 32 + 1) * sizeof(unsigned), s));
   f->ticket = f->flags + (N + 31) / 32;
-  CK(cudaMallocAsync((void**)&f->xt, (size_t)N * 8, s));
+  CK(cudaMallocFromPoolAsync((void**)&f->xt, (size_t)N * 8, engine_pool(f->device), s));
   CK(cudaMemsetAsync(f->xt, 0, (size_t)N * 8, s));
   f->bad = f->err + 2;
   *status = ur == GADI_DOUBLE ? factor_impl<GADI_DOUBLE>(f.get(), s)
