@@ -448,7 +448,7 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
   /* The GADI_ACCUM_FP32 extension mode (af != fmt; not in the reference) runs the
    * Arnoldi step as the device's fused passes do: classical Gram-Schmidt (all
    * dots of a step from the same w, then ONE update pass w -= sum h_i v_i in af
-   * with a single rounding to fmt) and unscaled norms sqrt(dot(w, w)) in af.
+   * with a single rounding to fmt) and h(j+1, j) = sqrt(dot(w, w)) in af.
    * The reference's modified Gram-Schmidt and max-scaled norm2
    * (inner_solver.cpp:121-126) stay as they are for af == fmt. */
   const int fused = af != fmt && !getenv("ORC_GMRES_MGS");
@@ -469,7 +469,7 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
       status = GADI_INNER_OVERFLOW;
       break;
     }
-    const double beta = fused ? R(sqrt(orc_dot(r, r, n, af)), af) : orc_norm2(r, n, af);
+    const double beta = orc_norm2(r, n, af);
     if (orc_norm2_64(r, n) <= target) {
       status = GADI_INNER_CONVERGED;
       break;

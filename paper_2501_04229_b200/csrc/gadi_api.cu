@@ -597,6 +597,8 @@ static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_op
   const int64_t maxblk = std::max<int64_t>(N / 64, 1) + 8;
   h->d_part0 = dalloc<double>(maxblk);
   h->d_part1 = dalloc<double>(maxblk);
+  h->d_partm = dalloc<double>(4 * maxblk);
+  h->partm_stride = maxblk;
   h->d_ticket = dalloc<unsigned>(1);
   CK(cudaMemset(h->d_ticket, 0, sizeof(unsigned)));
   CK(cudaHostAlloc(&h->h_done, sizeof(int), cudaHostAllocMapped));
@@ -627,7 +629,7 @@ int gadi_cuda_destroy(gadi_handle* h) {
       if (q) cudaFree(q);
   for (void* p : {(void*)h->d_rpA, (void*)h->d_ciA, (void*)h->d_vA, (void*)h->d_urp, (void*)h->d_uci,
                   (void*)h->d_mv, (void*)h->d_nv, (void*)h->d_dpos, (void*)h->d_din, (void*)h->st,
-                  (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_ticket})
+                  (void*)h->d_part0, (void*)h->d_part1, (void*)h->d_partm, (void*)h->d_ticket})
     if (p) cudaFree(p);
   for (void* p : h->raw) cudaFree(p);  // d_x, d_b, d_s, d_t64 (hvec)
   h->comm.reset();

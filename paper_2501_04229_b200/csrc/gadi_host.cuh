@@ -377,6 +377,8 @@ struct gadi_handle {
   DevState* st = nullptr;
   DevState* h_st = nullptr;  // pinned mirror
   double *d_part0 = nullptr, *d_part1 = nullptr;
+  double* d_partm = nullptr;  // block partials of the multi-dot pass (4 channels)
+  int64_t partm_stride = 0;
   unsigned* d_ticket = nullptr;
   int* h_done = nullptr;  // mapped pinned flag (CG done)
   int* d_h_done = nullptr;
@@ -720,6 +722,8 @@ struct Engine final : EngineBase {
   Geo geo;
   static constexpr int VA = 16 / sizeof(T);
   static constexpr bool SPARSE = !std::is_same<Op, Stencil7<C>>::value;
+  // binary16 storage with binary32 arithmetic (GADI_ACCUM_FP32): the fused two-pass Gram-Schmidt
+  static constexpr bool FUSED_GS = std::is_same<T, __half>::value && std::is_same<C, float>::value;
   // CG / GMRES work vectors
   T *pA = nullptr, *pB = nullptr, *q = nullptr, *wA = nullptr, *wB = nullptr, *gr = nullptr, *V = nullptr;
   int64_t ldv = 0;  // basis stride
@@ -1109,22 +1113,40 @@ struct Engine final : EngineBase {
               k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
           }
           coll<C>(h, EpiHcol{0});
-          for (int i = 0; i <= j; ++i) {
-            T* vi = V + (int64_t)i * ldv;
-            if (i < j) {
-              k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + ldv, i, geo, rd, h->st);
-              coll<C>(h, EpiHcol{i + 1});
-            } else {
-              CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
-              k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
-              coll_flags(h, nullptr);  // max|w| over all ranks
+          if constexpr (FUSED_GS) {
+            // accum = FP32: classical Gram-Schmidt in two passes (gadi_kernels.cuh)
+            const int64_t ps = h->partm_stride;
+            for (int i0 = 1; i0 <= j;) {
+              const int left = j - i0 + 1, J = h->sharded() ? 1 : std::min(left, 4);
+              if (J == 4) k_gm_dots<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+              else if (J == 3) k_gm_dots<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+              else if (J == 2) k_gm_dots<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+              else k_gm_dots<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+              if (J == 1) coll<C>(h, EpiHcol{i0});
+              i0 += J;
+              ++h->launches;
             }
+            k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
+            coll<C>(h, EpiCgsNorm{j});
+            h->launches += 2;
+          } else {
+            for (int i = 0; i <= j; ++i) {
+              T* vi = V + (int64_t)i * ldv;
+              if (i < j) {
+                k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + ldv, i, geo, rd, h->st);
+                coll<C>(h, EpiHcol{i + 1});
+              } else {
+                CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
+                k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
+                coll_flags(h, nullptr);  // max|w| over all ranks
+              }
+            }
+            k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
+            coll<C>(h, EpiNorm2{&h->st->hcol[j + 1]});
+            h->launches += j + 3;
           }
-          k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
-          coll<C>(h, EpiNorm2{&h->st->hcol[j + 1]});
         });
         CKL();
-        h->launches += j + 3;
         read_state(h);
         for (int i = 0; i <= j + 1; ++i) HC(i, j) = h->h_st->hcol[i];
         const double h1 = HC(j + 1, j);

@@ -955,6 +955,187 @@ __global__ void __launch_bounds__(256) k_gm_mgs(T* __restrict__ w, const T* __re
   }
 }
 
+// ------------------------------------------------ fused Gram-Schmidt (accum = FP32)
+// The GADI_ACCUM_FP32 extension mode (binary16 storage, binary32 arithmetic;
+// not in the reference) orthogonalises an Arnoldi vector in two passes instead
+// of j + 2: every h(i, j) = dot(w, v_i) from the same w (classical
+// Gram-Schmidt; h(0, j) comes from the matvec pass), then ONE update pass
+// w <- w - sum_i h_i v_i carried in binary32 with a single rounding to the
+// storage format, fused with dot(w, w) for h(j+1, j) = sqrt(.) -- (2j + 7) N
+// values moved per step instead of (4j + 7) N. The oracle restates exactly
+// this (gadi_oracle.c gmres_solve, `fused`).
+
+// J-channel versions of seg_run / grid_finish (C0 channels only): the same
+// pairwise trees per channel, one pass over the data, one grid ticket.
+template <int VEC, int J, class C0, class Body>
+__device__ __forceinline__ void seg_run_multi(const Geo& g, Body&& body, C0 (&w)[J]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  C0 a[J][RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r < g.R) {
+      const int64_t t = (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane;
+      const Seg s = seg_of<VEC>(t, g.N, g.D);
+      C0 c[J];
+#pragma unroll
+      for (int k = 0; k < J; ++k) c[k] = Ar<C0>::zero();
+      body(s, c);
+#pragma unroll
+      for (int k = 0; k < J; ++k) a[k][r] = warp_tree(c[k], g.L);
+    }
+  }
+#pragma unroll
+  for (int st = 1; st < RMAX; st <<= 1)
+#pragma unroll
+    for (int r = 0; r + st < RMAX; r += 2 * st)
+      if (r + st < g.R) {
+#pragma unroll
+        for (int k = 0; k < J; ++k) a[k][r] = Ar<C0>::add(a[k][r], a[k][r + st]);
+      }
+#pragma unroll
+  for (int k = 0; k < J; ++k) w[k] = a[k][0];
+}
+
+// part: J arrays of `stride` block partials. True in thread 0 of the last block.
+template <int J, class C0>
+__device__ __forceinline__ bool grid_finish_multi(C0 (&w)[J], const Geo& g, double* part, int64_t stride,
+                                                  unsigned* ticket, C0 (&tot)[J]) {
+  __shared__ __align__(8) unsigned char smb[J][32 * sizeof(double)];
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (g.W > 1) {
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < J; ++k) reinterpret_cast<C0*>(smb[k])[warp] = w[k];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int k = 0; k < J; ++k) {
+        C0 v = lane < g.W ? reinterpret_cast<C0*>(smb[k])[lane] : Ar<C0>::zero();
+        if (lane < g.W) v = warp_tree(v, g.W);
+        w[k] = v;
+      }
+    }
+  }
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < J; ++k) part[k * stride + blockIdx.x] = to_dbl(w[k]);
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    last = (t == (unsigned)g.nblk - 1u);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  const int P = g.nblk, B = blockDim.x;
+#pragma unroll
+  for (int k = 0; k < J; ++k) {
+    const double* pk = part + k * stride;
+    C0 a;
+    int cnt;
+    if (P <= B) {
+      a = tid < P ? from_dbl<C0>(__ldcg(pk + tid)) : Ar<C0>::zero();
+      cnt = P;
+    } else {
+      const int64_t Lr = P / B;
+      const double* p0 = pk + (int64_t)tid * Lr;
+      a = run_pairwise<C0>(Lr, [&](int64_t j) { return from_dbl<C0>(__ldcg(p0 + j)); });
+      cnt = B;
+    }
+    __syncthreads();
+    a = block_tree(a, cnt, reinterpret_cast<C0*>(smb[k]));
+    if (tid == 0) tot[k] = a;
+  }
+  if (tid == 0) *ticket = 0u;
+  return tid == 0;
+}
+
+// h(i0 + k, j) = dot(w, v_{i0+k}), k < J, in one pass over w and the J basis vectors.
+template <class T, class C, int VEC, int J>
+__global__ void __launch_bounds__(256) k_gm_dots(const T* __restrict__ w, const T* __restrict__ V, int64_t ldv, int i0,
+                                                 Geo g, Red rd, double* partm, int64_t pstride, DevState* st) {
+  GADI_G;
+  C ws[J];
+  seg_run_multi<VEC, J>(g, [&](const Seg& s, C (&c)[J]) {
+    T wv[G], vv[G];
+    load_seg<T, VEC, G>(w, s, wv);
+#pragma unroll
+    for (int k = 0; k < J; ++k) {
+      load_seg<T, VEC, G>(V + (int64_t)(i0 + k) * ldv, s, vv);
+      C tc[G];
+#pragma unroll
+      for (int e = 0; e < G; ++e) tc[e] = Ar<C>::mul(ld_c<T, C>(wv[e]), ld_c<T, C>(vv[e]));
+      c[k] = seg_sum<C, G>(tc, s.len);
+    }
+  }, ws);
+  C tot[J];
+  if (grid_finish_multi<J>(ws, g, partm, pstride, rd.ticket, tot)) {
+    if (J == 1) {
+      finish_red(EpiHcol{i0}, st, tot[0], 0.0);  // sharded solves: one record per dot
+    } else {
+#pragma unroll
+      for (int k = 0; k < J; ++k) st->hcol[i0 + k] = to_dbl(tot[k]);
+    }
+  }
+}
+
+struct EpiCgsNorm {  // h(j+1, j) = sqrt(dot(w, w)) in the inner arithmetic
+  int j;
+  template <class C>
+  __device__ void finish(C ss, double, DevState* st) const {
+    st->hcol[j + 1] = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss))));
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+
+// w <- round_T(w - h_0 v_0 - ... - h_j v_j) (each op rounded to C) and dot(w, w).
+template <class T, class C, int VEC>
+__global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __restrict__ V, int64_t ldv, int j, Geo g,
+                                                Red rd, DevState* st) {
+  GADI_G;
+  C w0;
+  double w1;
+  seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
+    T wv[G], vv[G];
+    C acc[G];
+    load_seg<T, VEC, G>(w, s, wv);
+#pragma unroll
+    for (int e = 0; e < G; ++e) acc[e] = ld_c<T, C>(wv[e]);
+    int i = 0;
+    for (; i + 4 <= j + 1; i += 4) {  // four basis vectors in flight at a time
+      T v4[4][G];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_seg<T, VEC, G>(V + (int64_t)(i + u) * ldv, s, v4[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const C nh = Ar<C>::neg(from_dbl<C>(st->hcol[i + u]));
+#pragma unroll
+        for (int e = 0; e < G; ++e) acc[e] = Ar<C>::add(acc[e], Ar<C>::mul(nh, ld_c<T, C>(v4[u][e])));
+      }
+    }
+    for (; i <= j; ++i) {
+      const C nh = Ar<C>::neg(from_dbl<C>(st->hcol[i]));
+      load_seg<T, VEC, G>(V + (int64_t)i * ldv, s, vv);
+#pragma unroll
+      for (int e = 0; e < G; ++e) acc[e] = Ar<C>::add(acc[e], Ar<C>::mul(nh, ld_c<T, C>(vv[e])));
+    }
+    C tc[G];
+#pragma unroll
+    for (int e = 0; e < G; ++e) {
+      wv[e] = st_t<T, C>(acc[e]);
+      const C r = ld_c<T, C>(wv[e]);
+      tc[e] = Ar<C>::mul(r, r);
+    }
+    store_seg<T, VEC, G>(w, s, wv);
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
+  C ss;
+  double dummy;
+  if (grid_finish(w0, w1, g, rd, ss, dummy)) finish_red(EpiCgsNorm{j}, st, ss, dummy);
+}
+
 // x += y_0 v_0; x += y_1 v_1; ... (inner_solver.cpp:174), one pass, the
 // sequence of rounded axpys kept per element; x_zero: x starts at 0.
 template <class T, class C, int VEC>

@@ -90,9 +90,9 @@ def test_c1_exact_equals_reference(orc, gold, inner):
 # ---- (b) configs[2] stand-ins: r held at 100/(2*513), max_inner 5, accum = FP32
 # gap = |outer(device) - outer(reference, u_r = single)| allowed: the north
 # star's +-1, met at three of the four cells; at n = 64, alpha = 0.2 (the
-# bench's alpha) binary16 storage converges 4 steps EARLIER than the reference's
-# binary32 storage (209 vs 213) -- the measured gap, stated in DESIGN.md.
-@pytest.mark.parametrize("n,alpha,gap", [(32, 0.2, 1), (32, 0.5, 1), (64, 0.3, 1), (64, 0.2, 4)])
+# bench's alpha) binary16 storage converges 3 steps EARLIER than the reference's
+# binary32 storage (210 vs 213) -- the measured gap, stated in DESIGN.md.
+@pytest.mark.parametrize("n,alpha,gap", [(32, 0.2, 1), (32, 0.5, 1), (64, 0.3, 1), (64, 0.2, 3)])
 def test_c3_standin(orc, gold, n, alpha, gap):
     S = g.build_convdiff3d(n, r=R_C3)
     A = orc.convdiff(n, S.t1, S.t2, S.t3)
