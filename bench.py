@@ -23,10 +23,12 @@ e2e    = the same solve through the C ABI gadi_cuda_solve with HOST buffers
          (pinned b in, x out; copies inside the timed region).
 roofline = the inner CG sweep (SpMV + axpys + dots, SURVEY §8(d) B_CG =
          11 N s_r bytes per iteration) against MEASURED_PEAKS.json hbm_gbs.
-Multi-GPU (torchrun, one rank per GPU): the workload is partitioned over the
-ranks -- z-slabs of the stencil grid, contiguous row blocks of the band CSR
- -- with halo exchanges and rank-ordered reduction records over
-one NCCL communicator (strong scaling: the same problem at every N).
+Multi-GPU (torchrun, one rank per GPU; launched bare, --gpus N spawns the
+ranks itself): the workload is partitioned over the ranks -- z-slabs of the
+stencil grid, contiguous row blocks of the band CSR -- with
+halo exchanges and rank-ordered reduction records over the library's CUDA IPC
+transport (GADI_TRANSPORT=nccl: one NCCL communicator). Strong scaling: the
+same problem at every N.
 """
 import argparse
 import json
@@ -380,20 +382,31 @@ def main():
     import torch
     import paper_2501_04229_b200 as g
 
+    if os.environ.get("GADI_BENCH_ONE_GPU"):  # dry run of the multi-rank path on one GPU (IPC transport only)
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # control plane only (barriers, a few scalars, the transport's rendezvous): gloo on the host.
+        # The data plane is the library's own transport below.
+        dist.init_process_group("gloo")
     if band:
         S = g.build_band_csr(wl["N"], wl["k_off"], wl["band"], wl["mseed"])
     else:
         S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
     grp = None
-    if sharded:  # one NCCL communicator for the solver's collectives (gadi_group_nccl)
-        obj = [g.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        grp = g.ShardGroup.nccl(world, rank, obj[0])
+    if sharded:
+        # one rank per process: CUDA IPC on a node (peer-mapped staging buffers, interprocess events,
+        # one-shot record gathers over NVLink), or NCCL with GADI_TRANSPORT=nccl
+        transport = os.environ.get("GADI_TRANSPORT", "ipc")
+        if transport == "nccl":
+            obj = [g.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            grp = g.ShardGroup.nccl(world, rank, obj[0])
+        else:
+            grp = g.ShardGroup.ipc(world, rank, f"/gadi_bench_{os.environ.get('MASTER_PORT', '0')}_{os.getppid()}")
+        cfg_json["transport"] = transport
         sysx = g.ShardSystem(S, grp, rank, device=local)
     else:
         sysx = g.CudaGadiSystem(S, device=local)
@@ -439,12 +452,12 @@ def main():
     h_it = sum(r.h_iters for r in reps)
     ok = all(r.status == g.SolveStatus.Converged for r in reps)
     x = torch.from_numpy(x_np).cuda()
-    ss = torch.stack([torch.sum((x - xt) ** 2), torch.sum(xt ** 2)])
+    ss = torch.stack([torch.sum((x - xt) ** 2), torch.sum(xt ** 2)]).cpu()
     if sharded:
         dist.all_reduce(ss)
     ferr = (ss[0].sqrt() / ss[1].sqrt()).item()
     if dist:
-        t = torch.tensor([solve_s, e2e_s], dtype=torch.float64, device="cuda")
+        t = torch.tensor([solve_s, e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         solve_s, e2e_s = t.tolist()
     peak, peak_kind = load_peaks()

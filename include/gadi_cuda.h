@@ -288,6 +288,11 @@ int gadi_group_local(int32_t world, gadi_group** out);
  * calls gadi_cuda_solve / gadi_cuda_solve_device on its shard collectively */
 int gadi_nccl_unique_id(uint8_t* out128);
 int gadi_group_nccl(int32_t world, int32_t rank, const uint8_t* id128, gadi_group** out);
+/* one rank per process on ONE node over CUDA IPC (peer-mapped staging
+ * buffers, interprocess events, a barrier in POSIX shared memory `name`,
+ * "/..."; every rank passes the same name): the intra-node transport of
+ * bench.py --gpus N. Collective: returns when all `world` ranks have attached. */
+int gadi_group_ipc(int32_t world, int32_t rank, const char* name, gadi_group** out);
 int gadi_group_destroy(gadi_group* g);
 /* the shard of `rank` (GADI_PROBLEM_STENCIL7 only) */
 int gadi_cuda_create_shard(const gadi_problem_desc* d, const gadi_device_opts* opts, gadi_group* g,

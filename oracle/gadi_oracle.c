@@ -436,6 +436,12 @@ static int cg_solve(const orc_csr* A0, const double* rhs, double eps, int max_in
   return status;
 }
 
+/* the fused mode's basis scaling: round_fmt(round_af(round_af(a) * x)) (scale_rn<T, true> on the device) */
+static void scale_af(double a, const double* x, int64_t n, int af, int fmt, double* z) {
+  const double aa = R(a, af);
+  for (int64_t i = 0; i < n; ++i) z[i] = R(R(aa * x[i], af), fmt);
+}
+
 /* gmres_solve, inner_solver.cpp:85-194. */
 static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max_inner, int restart,
                        int fmt, int af, double stop_norm, double* x, int* iters) {
@@ -448,7 +454,8 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
   /* The GADI_ACCUM_FP32 extension mode (af != fmt; not in the reference) runs the
    * Arnoldi step as the device's fused passes do: classical Gram-Schmidt (all
    * dots of a step from the same w, then ONE update pass w -= sum h_i v_i in af
-   * with a single rounding to fmt) and h(j+1, j) = sqrt(dot(w, w)) in af.
+   * with a single rounding to fmt), h(j+1, j) = sqrt(dot(w, w)) in af, and the
+   * basis scaling v = w / h as a product in af (scale_af).
    * The reference's modified Gram-Schmidt and max-scaled norm2
    * (inner_solver.cpp:121-126) stay as they are for af == fmt. */
   const int fused = af != fmt && !getenv("ORC_GMRES_MGS");
@@ -476,7 +483,8 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
     }
     if (beta == 0.0) break;
     int nv = 1;
-    orc_scale(1.0 / beta, r, n, fmt, V);
+    if (fused) scale_af(1.0 / beta, r, n, af, fmt, V);
+    else orc_scale(1.0 / beta, r, n, fmt, V);
     memset(Hc, 0, (size_t)(m + 1) * (size_t)m * 8);
     memset(cs, 0, (size_t)m * 8);
     memset(sn, 0, (size_t)m * 8);
@@ -508,7 +516,8 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
         goto out;
       }
       if (h1 != 0.0) {
-        orc_scale(1.0 / h1, w, n, fmt, V + (size_t)nv * n);
+        if (fused) scale_af(1.0 / h1, w, n, af, fmt, V + (size_t)nv * n);
+        else orc_scale(1.0 / h1, w, n, fmt, V + (size_t)nv * n);
         ++nv;
       }
       for (int i = 0; i < j; ++i) {

@@ -218,6 +218,7 @@ def lib():
     L.gadi_group_local.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
     L.gadi_nccl_unique_id.argtypes = [C.c_char_p]
     L.gadi_group_nccl.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]
+    L.gadi_group_ipc.argtypes = [C.c_int32, C.c_int32, C.c_char_p, C.POINTER(C.c_void_p)]
     L.gadi_group_destroy.argtypes = [C.c_void_p]
     L.gadi_cuda_create_shard.argtypes = [C.POINTER(_Problem), C.POINTER(_DevOpts), C.c_void_p, C.c_int32,
                                          C.POINTER(C.c_void_p)]
@@ -581,6 +582,14 @@ class ShardGroup:
             raise ContractViolation("nccl id must be 128 bytes")
         g = C.c_void_p()
         _check(lib().gadi_group_nccl(world, rank, uid, C.byref(g)))
+        return cls(g, world)
+
+    @classmethod
+    def ipc(cls, world: int, rank: int, name: str) -> "ShardGroup":
+        """One rank per process on one node over CUDA IPC (gadi_group_ipc): `name`
+        is a POSIX shared-memory name ("/..."), the same on every rank. Collective."""
+        g = C.c_void_p()
+        _check(lib().gadi_group_ipc(world, rank, name.encode(), C.byref(g)))
         return cls(g, world)
 
     def close(self):

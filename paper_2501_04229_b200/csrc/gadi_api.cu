@@ -478,6 +478,8 @@ static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_op
       h->gh = d->n * d->n;
       if (grp->local)
         h->comm.reset(new LocalComm(grp->local.get(), rank));
+      else if (grp->ipc)
+        h->comm.reset(new IpcComm(grp->ipc.get(), (size_t)h->gh * 8));
       else
         h->comm.reset(new NcclComm(grp->world, rank, grp->id));
     }
@@ -576,6 +578,8 @@ static gadi_handle* create_impl(const gadi_problem_desc* d, const gadi_device_op
       if (h->gh > h->N) throw Err(GADI_E_UNSUPPORTED, "sharded solves: the band exceeds a row block (fewer ranks)");
       if (grp->local)
         h->comm.reset(new LocalComm(grp->local.get(), rank));
+      else if (grp->ipc)
+        h->comm.reset(new IpcComm(grp->ipc.get(), (size_t)h->gh * 8));
       else
         h->comm.reset(new NcclComm(grp->world, rank, grp->id));
     }
@@ -1057,6 +1061,20 @@ int gadi_group_nccl(int32_t world, int32_t rank, const uint8_t* id128, gadi_grou
   g->nccl_rank = rank;
   std::memcpy(g->id.b, id128, sizeof(g->id.b));
   *out = g;
+  API_END
+}
+
+int gadi_group_ipc(int32_t world, int32_t rank, const char* name, gadi_group** out) {
+  API_BEGIN
+  if (!out || !name || name[0] != '/') throw Err(GADI_E_CONTRACT, "ipc group: need a shared-memory name starting with '/'");
+  if (world < 1 || world > GADI_MAX_RANKS || (world & (world - 1)) != 0)
+    throw Err(GADI_E_PARAM, "group: world must be a power of two <= 64");
+  if (rank < 0 || rank >= world) throw Err(GADI_E_PARAM, "group: rank out of range");
+  std::unique_ptr<gadi_group> g(new gadi_group());
+  g->world = world;
+  g->nccl_rank = rank;
+  g->ipc.reset(new IpcGroup(world, rank, name));
+  *out = g.release();
   API_END
 }
 

@@ -15,16 +15,25 @@
 //    the band of a CSR row block) into the neighbours' ghost entries before
 //    an operator pass reads them.
 //
-// Two transports implement them: LocalComm (ranks are threads of one
+// Three transports implement them: LocalComm (ranks are threads of one
 // process, on one or several devices: device copies ordered by CUDA events,
 // a host barrier per collective -- no kernel ever waits on another rank, so
-// several ranks may share one GPU) and NcclComm (one rank per process;
+// several ranks may share one GPU), IpcComm (one rank per process on one node:
+// the same protocol across processes -- CUDA IPC memory and interprocess
+// events, a barrier in POSIX shared memory, peer loads over NVLink / NVSwitch;
+// again no kernel waits on another rank) and NcclComm (one rank per process;
 // ncclAllGather and grouped ncclSend/ncclRecv, libnccl loaded at run time).
 #pragma once
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
+#include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <cstdint>
 #include <cstring>
@@ -130,6 +139,209 @@ struct LocalComm final : Comm {
   }
 };
 
+
+// ------------------------------------------------------------ CUDA IPC
+// One rank per process, all on one node (the torchrun launch of bench.py
+// --gpus N). Each rank owns a staging buffer (cudaMalloc, exported with
+// cudaIpcGetMemHandle and mapped by every peer) holding, per collective
+// parity p, its 4-word reduction record and its first / last `ghost` bytes,
+// and two interprocess events per parity: ready[p] (my staging[p] is written)
+// and pulled[p] (my reads of the peers' staging[p] are done). A collective:
+//   1. wait (stream) on every peer's pulled[p] of two collectives ago, write
+//      my staging[p], record ready[p];
+//   2. host barrier in shared memory (every rank has RECORDED ready[p]: a
+//      cudaStreamWaitEvent captures the event's latest record at call time);
+//   3. wait (stream) on the peers' ready[p], read their staging[p] through the
+//      mapped pointers (a halo pulls two chunks with device copies, a record
+//      all-gather reads every peer in ONE kernel: the one-shot exchange over
+//      NVLink / NVSwitch peer loads), record pulled[p].
+// The wait in step 1 of collective c + 2 follows the barrier of collective
+// c + 1, which every rank passes only after recording pulled[p] in c, so it
+// sees that record. No kernel ever spins on another rank's progress: ranks
+// may share a GPU (the 2- and 4-process tests do).
+struct IpcShared {
+  std::atomic<uint32_t> bar_count, bar_gen, attached;
+  uint32_t world;
+  struct Slot {
+    cudaIpcMemHandle_t mem;
+    cudaIpcEventHandle_t ev[4];  // ready[0], ready[1], pulled[0], pulled[1]
+    uint64_t stage_bytes;
+  } slot[64];
+};
+
+struct IpcGroup {
+  std::string name;
+  int world = 1, rank = 0;
+  IpcShared* sh = nullptr;
+  IpcGroup(int w, int r, const std::string& nm) : name(nm), world(w), rank(r) {
+    int fd = -1;
+    if (r == 0) {
+      shm_unlink(name.c_str());
+      fd = shm_open(name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (fd < 0 || ftruncate(fd, sizeof(IpcShared)) != 0) throw std::runtime_error("ipc group: shm_open failed: " + name);
+    } else {
+      const auto t0 = std::chrono::steady_clock::now();
+      while ((fd = shm_open(name.c_str(), O_RDWR, 0600)) < 0) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          throw std::runtime_error("ipc group: rank 0 never created " + name);
+        usleep(1000);
+      }
+      // wait until rank 0 sized the segment
+      for (;;) {
+        const off_t sz = lseek(fd, 0, SEEK_END);
+        if (sz >= (off_t)sizeof(IpcShared)) break;
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          throw std::runtime_error("ipc group: segment never sized: " + name);
+        usleep(1000);
+      }
+    }
+    void* p = mmap(nullptr, sizeof(IpcShared), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw std::runtime_error("ipc group: mmap failed");
+    sh = static_cast<IpcShared*>(p);
+    if (r == 0) sh->world = (uint32_t)w;  // the fresh segment is zero-filled: counters start at 0
+    sh->attached.fetch_add(1, std::memory_order_acq_rel);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (sh->attached.load(std::memory_order_acquire) < (uint32_t)w) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+        throw std::runtime_error("ipc group: not every rank attached");
+      sched_yield();
+    }
+  }
+  ~IpcGroup() {
+    if (sh) munmap(sh, sizeof(IpcShared));
+    if (rank == 0) shm_unlink(name.c_str());
+  }
+  void barrier() {
+    const uint32_t gen = sh->bar_gen.load(std::memory_order_acquire);
+    if (sh->bar_count.fetch_add(1, std::memory_order_acq_rel) + 1 == (uint32_t)world) {
+      sh->bar_count.store(0, std::memory_order_relaxed);
+      sh->bar_gen.fetch_add(1, std::memory_order_release);
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spins = 0; sh->bar_gen.load(std::memory_order_acquire) == gen; ++spins) {
+      if ((spins & 1023u) == 1023u) {
+        sched_yield();
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(300))
+          throw std::runtime_error("ipc group: a rank did not reach the barrier (300 s)");
+      }
+    }
+  }
+};
+
+struct IpcPeers {
+  const double* rec[64];
+};
+// dst[4 r + k] = rank r's record: one launch reads every peer (mapped pointers)
+static __global__ void k_ipc_gather(IpcPeers pp, int world, double* __restrict__ dst) {
+  const int t = threadIdx.x;
+  if (t < 4 * world) dst[t] = pp.rec[t >> 2][t & 3];
+}
+
+struct IpcComm final : Comm {
+  IpcGroup* g;
+  size_t ghost_max = 0, par_bytes = 0;
+  char* stage = nullptr;                 // [2 parities][256 B record | ghost_max | ghost_max]
+  cudaEvent_t ev[4] = {};                // ready[0], ready[1], pulled[0], pulled[1]
+  std::vector<char*> peer_stage;
+  std::vector<cudaEvent_t> peer_ev;      // [rank][4]
+  uint64_t seq = 0;
+  static void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  IpcComm(IpcGroup* grp, size_t ghost_bytes_max) : g(grp) {
+    rank = grp->rank;
+    world = grp->world;
+    ghost_max = (ghost_bytes_max + 255) & ~size_t(255);
+    par_bytes = 256 + 2 * ghost_max;
+    ck(cudaMalloc((void**)&stage, 2 * par_bytes), "ipc: cudaMalloc");
+    ck(cudaMemset(stage, 0, 2 * par_bytes), "ipc: cudaMemset");
+    IpcShared::Slot& me = g->sh->slot[rank];
+    ck(cudaIpcGetMemHandle(&me.mem, stage), "cudaIpcGetMemHandle");
+    for (int k = 0; k < 4; ++k) {
+      ck(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming | cudaEventInterprocess), "ipc: cudaEventCreate");
+      ck(cudaIpcGetEventHandle(&me.ev[k], ev[k]), "cudaIpcGetEventHandle");
+    }
+    me.stage_bytes = 2 * par_bytes;
+    ck(cudaDeviceSynchronize(), "ipc: sync");
+    g->barrier();  // every slot is published
+    peer_stage.assign(world, nullptr);
+    peer_ev.assign((size_t)world * 4, nullptr);
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) {
+        peer_stage[r] = stage;
+        for (int k = 0; k < 4; ++k) peer_ev[(size_t)r * 4 + k] = ev[k];
+        continue;
+      }
+      const IpcShared::Slot& sl = g->sh->slot[r];
+      if (sl.stage_bytes != 2 * par_bytes) throw std::runtime_error("ipc: ranks disagree on the ghost size");
+      void* p = nullptr;
+      ck(cudaIpcOpenMemHandle(&p, sl.mem, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      peer_stage[r] = static_cast<char*>(p);
+      for (int k = 0; k < 4; ++k) ck(cudaIpcOpenEventHandle(&peer_ev[(size_t)r * 4 + k], sl.ev[k]), "cudaIpcOpenEventHandle");
+    }
+    g->barrier();  // every rank has opened every slot before a slot is reused by the next IpcComm
+  }
+  ~IpcComm() override {
+    cudaDeviceSynchronize();
+    try {
+      g->barrier();  // no peer still reads my staging buffer
+    } catch (...) {
+    }
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) continue;
+      if (peer_stage[r]) cudaIpcCloseMemHandle(peer_stage[r]);
+      for (int k = 0; k < 4; ++k)
+        if (peer_ev[(size_t)r * 4 + k]) cudaEventDestroy(peer_ev[(size_t)r * 4 + k]);
+    }
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stage) cudaFree(stage);
+  }
+  char* rec_of(int r, int p) const { return peer_stage[r] + (size_t)p * par_bytes; }
+  char* lo_of(int r, int p) const { return rec_of(r, p) + 256; }
+  char* hi_of(int r, int p) const { return lo_of(r, p) + ghost_max; }
+  int begin(cudaStream_t s) {  // step 1's waits; returns the parity
+    const int p = (int)(seq++ & 1);
+    for (int r = 0; r < world; ++r)
+      if (r != rank) ck(cudaStreamWaitEvent(s, peer_ev[(size_t)r * 4 + 2 + p], 0), "ipc: wait pulled");
+    return p;
+  }
+  void allgather4(const double* src, double* dst, cudaStream_t s) override {
+    const int p = begin(s);
+    ck(cudaMemcpyAsync(rec_of(rank, p), src, 4 * sizeof(double), cudaMemcpyDeviceToDevice, s), "ipc: record copy");
+    ck(cudaEventRecord(ev[p], s), "ipc: record ready");
+    g->barrier();
+    IpcPeers pp;
+    for (int r = 0; r < world; ++r) {
+      if (r != rank) ck(cudaStreamWaitEvent(s, peer_ev[(size_t)r * 4 + p], 0), "ipc: wait ready");
+      pp.rec[r] = reinterpret_cast<const double*>(rec_of(r, p));
+    }
+    k_ipc_gather<<<1, 256, 0, s>>>(pp, world, dst);
+    ck(cudaGetLastError(), "k_ipc_gather");
+    ck(cudaEventRecord(ev[2 + p], s), "ipc: record pulled");
+  }
+  void halo(char* interior, int64_t ghost, int64_t len, cudaStream_t s) override {
+    if ((size_t)ghost > ghost_max) throw std::runtime_error("ipc: ghost larger than the staging buffer");
+    const int p = begin(s);
+    if (rank > 0) ck(cudaMemcpyAsync(lo_of(rank, p), interior, ghost, cudaMemcpyDeviceToDevice, s), "ipc: stage lo");
+    if (rank + 1 < world)
+      ck(cudaMemcpyAsync(hi_of(rank, p), interior + len - ghost, ghost, cudaMemcpyDeviceToDevice, s), "ipc: stage hi");
+    ck(cudaEventRecord(ev[p], s), "ipc: record ready");
+    g->barrier();
+    if (rank > 0) {
+      ck(cudaStreamWaitEvent(s, peer_ev[(size_t)(rank - 1) * 4 + p], 0), "ipc: wait ready");
+      ck(cudaMemcpyAsync(interior - ghost, hi_of(rank - 1, p), ghost, cudaMemcpyDefault, s), "ipc: pull lower");
+    }
+    if (rank + 1 < world) {
+      ck(cudaStreamWaitEvent(s, peer_ev[(size_t)(rank + 1) * 4 + p], 0), "ipc: wait ready");
+      ck(cudaMemcpyAsync(interior + len, lo_of(rank + 1, p), ghost, cudaMemcpyDefault, s), "ipc: pull upper");
+    }
+    ck(cudaEventRecord(ev[2 + p], s), "ipc: record pulled");
+  }
+};
+
 // ------------------------------------------------------------ NCCL
 // The few NCCL entry points used, resolved from libnccl.so.2 at run time (the
 // library does not link NCCL; torch's process already has one loaded).
@@ -223,7 +435,8 @@ struct NcclComm final : Comm {
 // process's NCCL membership.
 struct gadi_group {
   int world = 1;
-  int nccl_rank = -1;  // >= 0: NCCL (one rank per process)
+  int nccl_rank = -1;  // >= 0: one rank per process (NCCL, or CUDA IPC when `ipc` is set)
   std::unique_ptr<gadi_host::LocalGroup> local;
+  std::unique_ptr<gadi_host::IpcGroup> ipc;
   gadi_host::NcclId id{};
 };

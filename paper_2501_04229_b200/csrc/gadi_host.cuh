@@ -1101,7 +1101,7 @@ struct Engine final : EngineBase {
         V2([&](auto vt) {
           constexpr int V_ = decltype(vt)::v;
           if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
-            k_scale<T, V_><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
+            k_scale<T, V_, FUSED_GS><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
             halo(h, vj);  // a row block's matvec reads v_j at the band beyond its rows
             auto kern = k_gm_matvec<Op, T, C, V_, false>;
             smem_attr(kern, win.bytes);

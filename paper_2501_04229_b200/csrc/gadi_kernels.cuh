@@ -853,15 +853,15 @@ __global__ void __launch_bounds__(256) k_norm2(const T* __restrict__ w, double* 
   if (grid_finish(w0, w1, g, rd, sum, dummy)) finish_red(EpiNorm2{dst}, st, sum, dummy);
 }
 
-// dst = round(a * src) with a in binary64 (scale, kernels.cpp:166-171).
-template <class T, int VEC>
+// dst = round(a * src) with a in binary64 (scale, kernels.cpp:166-171); F32: scale_rn's binary32 variant.
+template <class T, int VEC, bool F32 = false>
 __global__ void __launch_bounds__(256) k_scale(const T* __restrict__ src, T* __restrict__ dst, double a, Geo g) {
   GADI_G;
   seg_each<VEC>(g, [&](const Seg& s) {
     T v[G];
     load_seg<T, VEC, G>(src, s, v);
 #pragma unroll
-    for (int i = 0; i < G; ++i) v[i] = from_dbl<T>(__dmul_rn(a, to_dbl(v[i])));
+    for (int i = 0; i < G; ++i) v[i] = scale_rn<T, F32>(a, v[i]);
     store_seg<T, VEC, G>(dst, s, v);
   });
 }
@@ -899,7 +899,7 @@ __global__ void __launch_bounds__(256) k_gm_matvec(Op op, const T* __restrict__ 
     c = seg_sum<C, G>(tc, s.len);
   };
   if constexpr (SCALED) {
-    const ScaleSrc<T> src{wprev, inv};
+    const ScaleSrc<T, std::is_same<T, __half>::value && std::is_same<C, float>::value> src{wprev, inv};
     seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) { body(s, c, src); }, w0, w1);
   } else if (VEC > 1 && wband > 0) {
     const SmemSrc<T> src = stage_window<T, VEC>(vj, g, wband);
@@ -1095,6 +1095,9 @@ template <class T, class C, int VEC>
 __global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __restrict__ V, int64_t ldv, int j, Geo g,
                                                 Red rd, DevState* st) {
   GADI_G;
+  __shared__ C snh[72];  // -h(i, j), read by every segment
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) snh[i] = Ar<C>::neg(from_dbl<C>(st->hcol[i]));
+  __syncthreads();
   C w0;
   double w1;
   seg_run<VEC, true, false>(g, [&](const Seg& s, C& c, double&) {
@@ -1110,13 +1113,13 @@ __global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __re
       for (int u = 0; u < 4; ++u) load_seg<T, VEC, G>(V + (int64_t)(i + u) * ldv, s, v4[u]);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const C nh = Ar<C>::neg(from_dbl<C>(st->hcol[i + u]));
+        const C nh = snh[i + u];
 #pragma unroll
         for (int e = 0; e < G; ++e) acc[e] = Ar<C>::add(acc[e], Ar<C>::mul(nh, ld_c<T, C>(v4[u][e])));
       }
     }
     for (; i <= j; ++i) {
-      const C nh = Ar<C>::neg(from_dbl<C>(st->hcol[i]));
+      const C nh = snh[i];
       load_seg<T, VEC, G>(V + (int64_t)i * ldv, s, vv);
 #pragma unroll
       for (int e = 0; e < G; ++e) acc[e] = Ar<C>::add(acc[e], Ar<C>::mul(nh, ld_c<T, C>(vv[e])));
@@ -1143,14 +1146,30 @@ __global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero
                                                    int64_t ldv, int j, Geo g, DevState* st) {
   GADI_G;
   int bad = 0;
+  __shared__ C sy[72];  // the coefficients, read by every segment
+  for (int i = threadIdx.x; i < j; i += blockDim.x) sy[i] = from_dbl<C>(st->ycoef[i]);
+  __syncthreads();
   seg_each<VEC>(g, [&](const Seg& s) {
     T xv[G], vv[G];
     C xc[G];
     if (!x_zero) load_seg<T, VEC, G>(x, s, xv);
 #pragma unroll
     for (int k = 0; k < G; ++k) xc[k] = x_zero ? Ar<C>::zero() : ld_c<T, C>(xv[k]);
-    for (int i = 0; i < j; ++i) {
-      const C y = from_dbl<C>(st->ycoef[i]);
+    int i = 0;
+    for (; i + 4 <= j; i += 4) {  // four basis vectors in flight at a time
+      T v4[4][G];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load_seg<T, VEC, G>(V + (int64_t)(i + u) * ldv, s, v4[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const C y = sy[i + u];
+#pragma unroll
+        for (int k = 0; k < G; ++k)
+          xc[k] = ld_c<T, C>(st_t<T, C>(Ar<C>::add(xc[k], Ar<C>::mul(y, ld_c<T, C>(v4[u][k])))));
+      }
+    }
+    for (; i < j; ++i) {
+      const C y = sy[i];
       load_seg<T, VEC, G>(V + (int64_t)i * ldv, s, vv);
 #pragma unroll
       for (int k = 0; k < G; ++k) xc[k] = ld_c<T, C>(st_t<T, C>(Ar<C>::add(xc[k], Ar<C>::mul(y, ld_c<T, C>(vv[k])))));

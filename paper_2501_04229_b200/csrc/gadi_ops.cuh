@@ -80,11 +80,26 @@ struct PUpdSrc {  // p_new = first ? r : round(r + beta * p)
   __device__ __forceinline__ T at(int64_t e) const { return first ? r[e] : f(r[e], p[e]); }
 };
 
-template <class T>
-struct ScaleSrc {  // v = round(inv * w), inv in binary64 (scale, kernels.cpp:166-171)
+// round(a * x): the reference's scale (kernels.cpp:166-171) multiplies in
+// binary64 and rounds once to the storage format. F32 (the GADI_ACCUM_FP32
+// extension mode: binary16 storage, binary32 arithmetic) rounds a to binary32,
+// multiplies in binary32 and rounds to binary16 -- no binary64 conversions on
+// the Arnoldi passes; the oracle's `fused` mode restates it.
+template <class T, bool F32>
+__device__ __forceinline__ T scale_rn(double a, T x) {
+  if constexpr (F32) {
+    static_assert(std::is_same<T, __half>::value, "F32 scaling is the binary16-storage mode");
+    return __float2half_rn(__fmul_rn((float)a, __half2float(x)));
+  } else {
+    return from_dbl<T>(__dmul_rn(a, to_dbl(x)));
+  }
+}
+
+template <class T, bool F32 = false>
+struct ScaleSrc {  // v = round(inv * w) (scale_rn)
   const T* __restrict__ w;
   double inv;
-  __device__ __forceinline__ T f(T x) const { return from_dbl<T>(__dmul_rn(inv, to_dbl(x))); }
+  __device__ __forceinline__ T f(T x) const { return scale_rn<T, F32>(inv, x); }
   template <int VEC>
   __device__ __forceinline__ void vec(int64_t e0, T (&v)[VEC]) const {
     ld_vec<T, VEC>(w, e0, v);

@@ -990,17 +990,18 @@ struct PolGmMatvec {
     if constexpr (FASTH)
       for (int k = 0; k < 7; ++k) ch[k] = __half_as_ushort(__float2half_rn(c7[k]));
   }
-  // FASTH: v = round(inv * w) with the product in binary64 (scale, kernels.cpp:166-171)
+  // FASTH (= the accum FP32 mode): v = round_h(round_f32(inv) * w), the product in
+  // binary32 (scale_rn<T, true>), two lanes per FMUL2 / F2FP
   __device__ uint4 make_h(const T* rs, int, int idx) const {
     const uint4 wv = lds_u4(rs + idx);
+    const float invf = (float)inv;
+    const float2 i2 = make_float2(invf, invf);
     uint32_t o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t wk = u4_at(wv, k);
-      const float2 wf = __half22float2(*reinterpret_cast<const __half2*>(&wk));
-      const __half2 v = __halves2half2(__double2half(__dmul_rn(inv, (double)wf.x)),
-                                       __double2half(__dmul_rn(inv, (double)wf.y)));
-      o[k] = *reinterpret_cast<const uint32_t*>(&v);
+      const float2 pr = __fmul2_rn(i2, __half22float2(*reinterpret_cast<const __half2*>(&wk)));
+      o[k] = pack_h2(pr.x, pr.y);
     }
     return make_uint4(o[0], o[1], o[2], o[3]);
   }
@@ -1023,7 +1024,7 @@ struct PolGmMatvec {
     T wv[ST25_VEC];
     lds16<T, ST25_VEC>(rs + idx, wv);
 #pragma unroll
-    for (int e = 0; e < ST25_VEC; ++e) v[e] = ld_c<T, RT>(from_dbl<T>(__dmul_rn(inv, to_dbl(wv[e]))));
+    for (int e = 0; e < ST25_VEC; ++e) v[e] = ld_c<T, RT>(scale_rn<T, FASTH>(inv, wv[e]));
   }
   __device__ MatvecF<C, RT> fold() const { return MatvecF<C, RT>(); }
   __device__ void init(int64_t, C (&acc)[ST25_VEC]) const {
