@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) k_potinv128(double* __restrict__ W, int l
                                                    int* __restrict__ info) {
   extern __shared__ double sA[];  // [128][129]; the strict upper triangle stays zero
   __shared__ double sinv[NB];     // 1 / L_cc
+  __shared__ double scol[32];
   __shared__ int bad;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) bad = 0;
@@ -74,27 +75,28 @@ __global__ void __launch_bounds__(256) k_potinv128(double* __restrict__ W, int l
   __syncthreads();
   // ------------------------------------------------------------- factor
   for (int c0 = 0; c0 < NB; c0 += 32) {
-    if (warp == 0) {  // diagonal 32 x 32 block: lane = row
+    if (warp == 0) {  // diagonal 32 x 32 block: lane = row, the row in registers
       double a[32];
 #pragma unroll
       for (int c = 0; c < 32; ++c) a[c] = sA[(c0 + lane) * 129 + c0 + c];
       int isbad = 0;
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        const double piv = shfl_d(a[c], c);
+        scol[lane] = a[c];  // column c of the block, unscaled: broadcast through shared memory
+        __syncwarp();
+        const double piv = scol[c];
         if (!(piv > 0.0) && !isbad) isbad = c0 + c + 1;
         const double rs = rsqrt(piv);
-        if (lane == c) {
-          a[c] = piv * rs;
-          sinv[c0 + c] = rs;
-        } else if (lane > c) {
-          a[c] *= rs;
-        }
+        const double l = lane == c ? piv * rs : a[c] * rs;
+        a[c] = l;
+        if (lane == c) sinv[c0 + c] = rs;
 #pragma unroll
         for (int cc = c + 1; cc < 32; ++cc) {
-          const double lcc = shfl_d(a[c], cc);
-          if (lane >= cc) a[cc] = fma(-a[c], lcc, a[cc]);
+          // l_cc,c = raw * rs, the value lane cc stores as its own a[c]; rows above cc are not updated
+          const double lcc = lane >= cc ? scol[cc] * rs : 0.0;
+          a[cc] = fma(-l, lcc, a[cc]);
         }
+        __syncwarp();
       }
       if (isbad && lane == 0) bad = isbad;
 #pragma unroll
