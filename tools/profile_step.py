@@ -13,7 +13,10 @@ ap.add_argument("--outer", type=int, default=2)
 ap.add_argument("--repeat", type=int, default=1)
 a = ap.parse_args()
 wl = WORKLOADS[a.workload]
-S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
+if wl.get("kind") == "band":
+    S = g.build_band_csr(wl["N"], wl["k_off"], wl["band"], wl["mseed"])
+else:
+    S = g.build_convdiff3d(wl["n"], beta=wl["beta"])
 sysx = g.CudaGadiSystem(S)
 xt = torch.empty(S.n_rows, dtype=torch.float64, device="cuda")
 b = torch.empty_like(xt); x = torch.empty_like(xt)
