@@ -454,7 +454,8 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
   /* The GADI_ACCUM_FP32 extension mode (af != fmt; not in the reference) runs the
    * Arnoldi step as the device's fused passes do: classical Gram-Schmidt (all
    * dots of a step from the same w, then ONE update pass w -= sum h_i v_i in af
-   * with a single rounding to fmt), h(j+1, j) = sqrt(dot(w, w)) in af, and the
+   * with a single rounding to fmt), the norms beta and h(j+1, j) as sqrt(dot(., .))
+   * in af, and the
    * basis scaling v = w / h as a product in af (scale_af).
    * The reference's modified Gram-Schmidt and max-scaled norm2
    * (inner_solver.cpp:121-126) stay as they are for af == fmt. */
@@ -476,7 +477,7 @@ static int gmres_solve(const orc_csr* A0, const double* rhs, double eps, int max
       status = GADI_INNER_OVERFLOW;
       break;
     }
-    const double beta = orc_norm2(r, n, af);
+    const double beta = fused ? R(sqrt(orc_dot(r, r, n, af)), af) : orc_norm2(r, n, af);
     if (orc_norm2_64(r, n) <= target) {
       status = GADI_INNER_CONVERGED;
       break;

@@ -1056,6 +1056,20 @@ struct Engine final : EngineBase {
       }
       CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
+      if constexpr (FUSED_GS) {
+        if (x_zero) {  // one pass: r, ||r|| (binary64), beta = sqrt(dot(r, r)) (binary32), finiteness
+          V2([&](auto vt) {
+            constexpr int V_ = decltype(vt)::v;
+            k_gm_resid0<Op, V_><<<geo.nblk, nt, 0, s>>>(o, rhs, gr, geo, rd, h->st,
+                                                        lazy ? static_cast<const T*>(z) : nullptr, pz_phat);
+          });
+          coll<C>(h, EpiResidF{});
+          CKL();
+          ++h->launches;
+          read_state(h);
+          return;
+        }
+      }
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
         if (!x_zero) halo(h, x);
@@ -1067,8 +1081,13 @@ struct Engine final : EngineBase {
                                         lazy ? static_cast<const T*>(z) : nullptr, pz_phat);
         }
         coll<C>(h, EpiRedD{});
-        k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
-        coll<C>(h, EpiNorm2{&h->st->red_c});
+        if constexpr (FUSED_GS) {  // the fused mode's norm: beta = sqrt(dot(r, r))
+          k_selfdot<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, geo, rd, h->st);
+          coll<C>(h, EpiSqrtRedC{});
+        } else {
+          k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(gr, &h->st->red_c, geo, rd, h->st);
+          coll<C>(h, EpiNorm2{&h->st->red_c});
+        }
       });
       CKL();
       h->launches += 2;

@@ -776,6 +776,112 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
   if (grid_finish(w0, w1, g, rd, dc, ss)) finish_red(EpiRedD{}, st, dc, ss);
 }
 
+// The fused mode's restart residual from x = 0 (accum = FP32: binary16 storage,
+// binary32 arithmetic): r = rhs (or round(phat z), formed here) under the
+// zero-start sign rules, ||r||_2 in binary64 for the stop test AND
+// beta = sqrt(dot(r, r)) in binary32 (the unscaled norm of the fused Arnoldi
+// step; the native modes keep the reference's max-scaled norm2 in k_norm2),
+// finiteness from the segment's sum of squares (a square of a finite binary16
+// is at most 4.3e9, so the sum is finite exactly when every entry is).
+// Packed fast path: binary16 pairs are scaled with HMUL2 (the product of two
+// binary16 values is exact in binary32, so one rounding to binary16 is the
+// reference's scale), and the zero-start rules only touch -0 entries and
+// non-finite coefficients -- a chunk with neither is stored as it is.
+struct EpiResidF {
+  template <class C>
+  __device__ void finish(C ss32, double ss, DevState* st) const {
+    st->red_d = ss;
+    st->red_c = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss32))));
+  }
+  __device__ int* flag_dst(DevState* st) const { return &st->flags; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+template <class Op, int VEC>
+__global__ void __launch_bounds__(256) k_gm_resid0(Op op, const __half* __restrict__ rhs, __half* __restrict__ r,
+                                                   Geo g, Red rd, DevState* st, const __half* __restrict__ zsrc,
+                                                   double phat) {
+  using T = __half;
+  using C = float;
+  GADI_G;
+  const float pf = (float)phat;
+  const bool f16 = zsrc && (double)__half2float(__float2half_rn(pf)) == phat;
+  const __half2 p2 = __float2half2_rn(pf);
+  int bad = 0;
+  C w0;
+  double w1;
+  seg_run_ld<VEC, true, true, G>(g, zsrc ? zsrc : rhs, [&](const Seg& s, const T (&bv0)[G], C& c, double& d) {
+    T rv[G];
+    if (f16) {
+#pragma unroll
+      for (int i = 0; i < G; i += 2) {
+        const __half2 pr = __hmul2(__halves2half2(bv0[i], bv0[i + 1]), p2);
+        rv[i] = __low2half(pr);
+        rv[i + 1] = __high2half(pr);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < G; ++i) rv[i] = zsrc ? from_dbl<T>(__dmul_rn(phat, to_dbl(bv0[i]))) : bv0[i];
+    }
+    int fl[G];
+    if constexpr (VEC > 1) {
+      op.template zflags_vec<VEC>(s.lo, fl);
+    } else {
+#pragma unroll
+      for (int i = 0; i < G; ++i) fl[i] = GADI_LIVE(i) ? op.zflags(s.lo + i) : 0;
+    }
+    int special = 0;
+#pragma unroll
+    for (int i = 0; i < G; ++i) special |= (fl[i] & 2) | ((__half_as_ushort(rv[i]) == 0x8000u) ? (fl[i] & 1) : 0);
+    if (special) {  // rare: a -0 entry under a sign-set coefficient, or a non-finite coefficient
+#pragma unroll
+      for (int i = 0; i < G; ++i)
+        if (GADI_LIVE(i)) rv[i] = st_t<T, C>(zero_resid(ld_c<T, C>(rv[i]), fl[i]));
+    }
+    C tc[G];
+    double td[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      const float f = GADI_LIVE(i) ? __half2float(rv[i]) : 0.0f;
+      tc[i] = __fmul_rn(f, f);  // exact
+      td[i] = (double)tc[i];
+    }
+    store_seg<T, VEC, G>(r, s, rv);
+    c = seg_sum<C, G>(tc, s.len);
+    d = seg_sum<double, G>(td, s.len);
+    bad |= isfinite(c) ? 0 : 1;
+  }, w0, w1);
+  or_flags(&st->flags, bad);
+  C dc;
+  double ss;
+  if (grid_finish(w0, w1, g, rd, dc, ss)) finish_red(EpiResidF{}, st, dc, ss);
+}
+
+// beta = sqrt(dot(w, w)) in the inner arithmetic into st->red_c (the fused mode's
+// norm after a restart residual from x != 0)
+struct EpiSqrtRedC {
+  template <class C>
+  __device__ void finish(C ss, double, DevState* st) const {
+    st->red_c = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss))));
+  }
+  __device__ int* flag_dst(DevState*) const { return nullptr; }
+  __device__ bool skip(DevState* st) const { return (void)st, false; }
+};
+template <class T, class C, int VEC>
+__global__ void __launch_bounds__(256) k_selfdot(const T* __restrict__ w, Geo g, Red rd, DevState* st) {
+  GADI_G;
+  C w0;
+  double w1;
+  seg_run_ld<VEC, true, false, G>(g, w, [&](const Seg& s, const T (&wv)[G], C& c, double&) {
+    C tc[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) tc[i] = Ar<C>::mul(ld_c<T, C>(wv[i]), ld_c<T, C>(wv[i]));
+    c = seg_sum<C, G>(tc, s.len);
+  }, w0, w1);
+  C ss;
+  double dummy;
+  if (grid_finish(w0, w1, g, rd, ss, dummy)) finish_red(EpiSqrtRedC{}, st, ss, dummy);
+}
+
 struct EpiNorm2 {  // m * sqrt(sum) in the inner format (kernels.cpp:79-81), m = max|w| from maxbits
   double* dst;
   template <class C>
