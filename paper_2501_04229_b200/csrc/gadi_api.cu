@@ -259,12 +259,24 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
   // spec: when u_f is binary64, first try the single pass that also rounds
   // rhat with the previous step's exponent (accepted iff the exponent is
   // unchanged -- the usual case; else the two-pass route below reruns).
+  const bool trace = std::getenv("GADI_TRACE") != nullptr;
+  cudaEvent_t trU = nullptr, trR = nullptr, trR0 = nullptr, trK = nullptr, trX = nullptr;
+  double tr_gap = 0.0, tr_upd = 0.0, tr_res = 0.0, tr_kern = 0.0, tr_wake = 0.0;
+  if (trace) {
+    CK(cudaEventCreate(&trU));
+    CK(cudaEventCreate(&trR));
+    CK(cudaEventCreate(&trR0));
+    CK(cudaEventCreate(&trK));
+    CK(cudaEventCreate(&trX));
+  }
   const bool can_spec = cfg->u_f == GADI_DOUBLE && !std::getenv("GADI_NO_SPEC");
   auto rsr = [&](bool spec) {
     const bool sc = cfg->residual_scaling != 0;
     if (spec && can_spec && e->resid_spec(h->d_x, ex, sc)) {
       const int ns_r = sc ? 0 : h->ns;
+      if (trace) CK(cudaEventRecord(trK, s));
       read_state(h);
+      if (trace) CK(cudaEventRecord(trX, s));
       if (res_norm_ok(h) && h->h_st->res_e == ex) {
         rhat_n = std::ldexp(std::sqrt(h->h_st->rhat_ss), ns_r);
         tnorm = res_norm(h);
@@ -340,9 +352,22 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     // x <- x + 2^e y in u (solver.cpp:163-166), non-finite check (:168-174)
     CK(cudaMemsetAsync(&h->st->xbad, 0, 4, s));
     e->update(h->d_x, cfg->u);
+    if (trace) CK(cudaEventRecord(trU, s));
     rsr(true);  // syncs: also closes the H/S timing events
     h_ms += ms_between(h->evA, h->evB);
     s_ms += ms_between(h->evB, h->evC);
+    if (trace) {  // GADI_TRACE: where the outer part of a step goes (measurement only)
+      CK(cudaEventRecord(trR, s));
+      CK(cudaEventSynchronize(trR));
+      if (k > 0) tr_gap += ms_between(trR0, h->evA);
+      tr_upd += ms_between(h->evC, trU);
+      tr_res += ms_between(trU, trR);
+      if (cudaEventQuery(trK) == cudaSuccess && k > 2) {
+        tr_kern += ms_between(trU, trK);
+        tr_wake += ms_between(trK, trX);
+      }
+      std::swap(trR, trR0);
+    }
     if (h->h_st->xbad) {
       OuterA::resid_sync(h, h->d_x, nullptr, GADI_DOUBLE, false);
       h->history.push_back(res_norm(h) / nt0);
@@ -353,6 +378,15 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     }
     stop_norm = std::ldexp(g0, -ex);
     h->history.push_back(tnorm / nt0);
+  }
+  if (trace) {
+    std::fprintf(stderr, "[gadi trace] outer steps %d: update %.3f ms, residual pass + sync %.3f ms, host gap before the next step %.3f ms; from step 3 on: residual kernel %.3f ms, copy + host wake-up %.3f ms (totals)\n",
+                 rep->outer_iters, tr_upd, tr_res, tr_gap, tr_kern, tr_wake);
+    cudaEventDestroy(trK);
+    cudaEventDestroy(trX);
+    cudaEventDestroy(trU);
+    cudaEventDestroy(trR);
+    cudaEventDestroy(trR0);
   }
   finish();
 }

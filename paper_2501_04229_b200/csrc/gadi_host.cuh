@@ -28,6 +28,7 @@
 #include "../../include/gadi_cuda.h"
 #include "gadi_kernels.cuh"
 #include "gadi_st25.cuh"
+#include "gadi_resid64.cuh"
 #include "gadi_dist.cuh"
 #include "gadi_csr.cuh"
 
@@ -227,6 +228,71 @@ inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Re
     case 1: return launch_st25_cpt<P, 1>(pol, g, s, rd, st);
     case 2: return launch_st25_cpt<P, 2>(pol, g, s, rd, st);
     default: return launch_st25_cpt<P, 4>(pol, g, s, rd, st);
+  }
+}
+
+// k_resid64 (gadi_resid64.cuh): tile of threads*CPT 16-byte chunks per plane,
+// S staged planes of TJ+2 rows. Variants (threads, CPT, CTAs per SM) are
+// compile-time; GADI_R64 picks one (0: off, the k_st25 passes run).
+inline int r64_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("GADI_R64");
+    return e ? std::atoi(e) : 4;
+  }();
+  return v;
+}
+inline bool make_r64(int64_t n, int64_t i0, int64_t i1, int threads, int cpt, int S, St25Geo& g) {
+  if (i1 < 0) i1 = n;
+  const int64_t nloc = i1 - i0;
+  if (nloc < 1 || !is_pow2(nloc) || !is_pow2(n) || n < 64) return false;
+  const int64_t TR = n / 2, chunks = (int64_t)threads * cpt;
+  if (chunks % TR != 0) return false;
+  const int64_t TJ = chunks / TR;
+  if (TJ < 1 || TJ > n) return false;
+  g.i0 = (int)i0;
+  g.i1 = (int)i1;
+  g.n = (int)n;
+  g.lg = ilog2(n);
+  g.nn = n * n;
+  g.TR = (int)TR;
+  g.lgTR = ilog2(TR);
+  g.CPT = cpt;
+  g.TJ = (int)TJ;
+  g.lgTJ = ilog2(TJ);
+  g.njt = (int)(n / TJ);
+  int64_t IL = 32;
+  while (IL > 4 && g.njt * (nloc / IL) < 2048) IL /= 2;
+  if (const char* e = std::getenv("GADI_R64_IL")) IL = std::min(32, std::max(1, std::atoi(e)));  // tuning knob
+  IL = std::min<int64_t>(IL, nloc);
+  g.IL = (int)IL;
+  g.nblk = (int)(g.njt * (nloc / IL));
+  g.threads = threads;
+  g.stages = S;
+  g.smem = 128 + (size_t)S * ((TJ + 2) * n + 2) * sizeof(double);
+  return g.smem <= 200 * 1024;
+}
+// the variant's (threads, CPT) and whether the shape and coefficients fit
+inline bool r64_fits(int64_t n, int64_t i0, int64_t i1, const double (&c7)[7], St25Geo& g) {
+  static const int TH[6] = {0, 512, 256, 256, 512, 512}, CP[6] = {0, 2, 4, 2, 4, 2}, SS[6] = {0, 4, 4, 4, 4, 8};
+  const int v = r64_variant();
+  if (v < 1 || v > 5) return false;
+  for (int k = 0; k < 7; ++k)
+    if (!std::isfinite(c7[k])) return false;
+  return make_r64(n, i0, i1, TH[v], CP[v], SS[v], g);
+}
+template <class P, int CPT, int THREADS, int MINB, int S>
+inline void launch_resid64_v(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  smem_attr(k_resid64<P, CPT, THREADS, MINB, S>, 200 * 1024);
+  k_resid64<P, CPT, THREADS, MINB, S><<<g.nblk, THREADS, g.smem, s>>>(pol, g, rd, st);
+}
+template <class P>
+inline void launch_resid64(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
+  switch (r64_variant()) {  // g comes from r64_fits of the same variant
+    case 1: return launch_resid64_v<P, 2, 512, 1, 4>(pol, g, s, rd, st);
+    case 2: return launch_resid64_v<P, 4, 256, 2, 4>(pol, g, s, rd, st);
+    case 3: return launch_resid64_v<P, 2, 256, 2, 4>(pol, g, s, rd, st);
+    case 5: return launch_resid64_v<P, 2, 512, 1, 8>(pol, g, s, rd, st);
+    default: return launch_resid64_v<P, 4, 512, 1, 4>(pol, g, s, rd, st);
   }
 }
 
@@ -479,8 +545,11 @@ T* dalloc(int64_t n) {
   return static_cast<T*>(p);
 }
 
-inline void read_state(gadi_handle* h) {
-  CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(DevState), cudaMemcpyDeviceToHost, h->stream));
+// The scalar head of the device state (cols = 0), plus the Arnoldi column (cols = 1) or the
+// columns of a speculative window as well (cols = 2).
+inline void read_state(gadi_handle* h, int cols = 0) {
+  const size_t bytes = cols == 0 ? offsetof(DevState, hcol) : cols == 1 ? offsetof(DevState, hhist) : offsetof(DevState, ycoef);
+  CK(cudaMemcpyAsync(h->h_st, h->st, bytes, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
 }
 
@@ -565,7 +634,15 @@ struct OuterA {
       else LV(VecTag<P_DOUBLE>{});
     };
     St25Geo g25;
-    if (h->stencil() && make_st25(h->n, 8, 1, g25, 1024, true, 0, h->i0, h->i1)) {
+    bool done64 = false;
+    if (h->stencil() && uf == GADI_DOUBLE) {
+      PolResidA<P_DOUBLE> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x - eo, h->d_b - eo,
+                              s ? s - eo : nullptr, scaling ? 1 : 0, nsc_of(h->ns)};
+      if ((done64 = r64_fits(h->n, h->i0, h->i1, pol.c7, g25)))
+        launch_resid64(pol, g25, h->stream, red_of(h), h->st);
+    }
+    if (done64) {
+    } else if (h->stencil() && make_st25(h->n, 8, 1, g25, 1024, true, 0, h->i0, h->i1)) {
       auto L = [&](auto pt) {
         constexpr int PF = decltype(pt)::v;
         PolResidA<PF> pol{{h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3}, x - eo, h->d_b - eo,
@@ -933,12 +1010,13 @@ struct Engine final : EngineBase {
       return false;
     }
   }
-  bool gmmatvec25(const Op& o, const T* wprev, double inv, T* vj, T* w) {
+  bool gmmatvec25(const Op& o, const T* wprev, double inv, T* vj, T* w, bool inv_dev = false) {
     if constexpr (std::is_same<Op, Stencil7<C>>::value) {
       if (!st25) return false;
       const int64_t eo = h->e_off();
       PolGmMatvec<T, C> pol{{o.c[0], o.c[1], o.c[2], o.c[3], o.c[4], o.c[5], o.c[6]}, wprev - eo, inv, vj - eo,
                             V - eo, w - eo};
+      pol.inv_dev = inv_dev ? 1 : 0;
       if constexpr (PolGmMatvec<T, C>::FASTH)
         if (st25h) {
           launch_st25h(pol, g25mh, h->stream, red_of(h), h->st);
@@ -1049,7 +1127,17 @@ struct Engine final : EngineBase {
     bool x_zero = true;  // x = 0 until the first update (inner_solver.cpp:92)
     bool lazy = rhs_v == pz && pz_lazy;  // rhs = round(pz_phat z), not stored yet
     pz_lazy = false;
-    auto resid = [&]() {  // r = rhs - S x ; flags, max, ||r||_2 (binary64), norm2 in fmt
+    // Speculative Arnoldi windows (fused mode on the st25 passes): the steps of a window are
+    // queued back to back -- each step's basis scaling 1 / h(j+1, j) is formed on the device
+    // (gm_inv) and its column kept in hhist -- and the host reads the whole window with one
+    // sync, then rotates the columns in order. A step past the one where the host stops
+    // (convergence, breakdown, overflow) only wrote basis / work vectors nobody reads.
+    static const bool spec_env = [] {
+      const char* e = std::getenv("GADI_GM_SPEC");
+      return !e || std::atoi(e) != 0;
+    }();
+    const bool spec_ok = FUSED_GS && !SPARSE && st25 && spec_env;
+    auto resid = [&](bool sync = true) {  // r = rhs - S x ; flags, max, ||r||_2 (binary64), norm2 in fmt
       if (lazy && !x_zero) {
         scale_pz(pz_phat);
         lazy = false;
@@ -1060,13 +1148,23 @@ struct Engine final : EngineBase {
         if (x_zero) {  // one pass: r, ||r|| (binary64), beta = sqrt(dot(r, r)) (binary32), finiteness
           V2([&](auto vt) {
             constexpr int V_ = decltype(vt)::v;
+            if constexpr (V_ == 8 && !SPARSE) {
+              // packed pass: phat is a binary16 value (solver.cpp:117 rounds it to u_r), so HMUL2 scales
+              const __half ph = __float2half_rn((float)pz_phat);
+              if (!lazy || (double)__half2float(ph) == pz_phat) {
+                const uint32_t pb = __half_as_ushort(ph);
+                k_gm_resid0p<Op><<<geo.nblk, nt, 0, s>>>(o, lazy ? static_cast<const T*>(z) : rhs, gr, geo, rd, h->st,
+                                                         lazy ? 1 : 0, pb | (pb << 16));
+                return;
+              }
+            }
             k_gm_resid0<Op, V_><<<geo.nblk, nt, 0, s>>>(o, rhs, gr, geo, rd, h->st,
                                                         lazy ? static_cast<const T*>(z) : nullptr, pz_phat);
           });
           coll<C>(h, EpiResidF{});
           CKL();
           ++h->launches;
-          read_state(h);
+          if (sync) read_state(h);
           return;
         }
       }
@@ -1091,10 +1189,76 @@ struct Engine final : EngineBase {
       });
       CKL();
       h->launches += 2;
-      read_state(h);
+      if (sync) read_state(h);
+    };
+    // one Arnoldi step's kernels: v_j = w_prev * inv, w = S v_j, the column h(., j)
+    auto arnoldi = [&](int j, double inv, bool inv_dev, int slot) {
+      const T* wprev = j == 0 ? gr : (((j - 1) & 1) ? wB : wA);
+      T* vj = V + (int64_t)j * ldv;
+      T* w = (j & 1) ? wB : wA;
+      V2([&](auto vt) {
+        constexpr int V_ = decltype(vt)::v;
+        if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
+          k_scale<T, V_, FUSED_GS><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
+          halo(h, vj);  // a row block's matvec reads v_j at the band beyond its rows
+          auto kern = k_gm_matvec<Op, T, C, V_, false>;
+          smem_attr(kern, win.bytes);
+          kern<<<geo.nblk, nt, win.bytes, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st, win.band);
+          ++h->launches;
+        } else {
+          halo(h, wprev);
+          if (!gmmatvec25(o, wprev, inv, vj, w, inv_dev))
+            k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
+        }
+        coll<C>(h, EpiHcol{0});
+        if constexpr (FUSED_GS) {
+          // accum = FP32: classical Gram-Schmidt in two passes (gadi_kernels.cuh)
+          const int64_t ps = h->partm_stride;
+          for (int i0 = 1; i0 <= j;) {
+            const int left = j - i0 + 1, J = h->sharded() ? 1 : std::min(left, 4);
+            if (J == 4) k_gm_dots<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+            else if (J == 3) k_gm_dots<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+            else if (J == 2) k_gm_dots<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+            else k_gm_dots<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
+            if (J == 1) coll<C>(h, EpiHcol{i0});
+            i0 += J;
+            ++h->launches;
+          }
+          k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
+          coll<C>(h, EpiCgsNorm{j});
+          if (slot >= 0) k_gm_column_done<<<1, 1, 0, s>>>(h->st, j, slot);
+          h->launches += 2;
+        } else {
+          for (int i = 0; i <= j; ++i) {
+            T* vi = V + (int64_t)i * ldv;
+            if (i < j) {
+              k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + ldv, i, geo, rd, h->st);
+              coll<C>(h, EpiHcol{i + 1});
+            } else {
+              CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
+              k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
+              coll_flags(h, nullptr);  // max|w| over all ranks
+            }
+          }
+          k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
+          coll<C>(h, EpiNorm2{&h->st->hcol[j + 1]});
+          h->launches += j + 3;
+        }
+      });
+      CKL();
     };
     while (total < spec.max_inner_iters) {
-      resid();
+      // spec: the restart residual and the first window go out together
+      int jq = 0, win0 = 0;  // steps queued so far in this cycle; first step of the current window
+      auto queue_window = [&](int j0) {
+        const int hi = std::min({m, j0 + GM_SPEC_MAX, j0 + (spec.max_inner_iters - total)});
+        for (int jj = j0; jj < hi; ++jj) arnoldi(jj, 0.0, true, jj - j0);
+        win0 = j0;
+        jq = hi;
+        read_state(h, 2);
+      };
+      resid(!spec_ok);
+      if (spec_ok) queue_window(0);
       if (h->h_st->flags & 1) {
         status = INNER_OVERFLOW;
         break;
@@ -1113,61 +1277,16 @@ struct Engine final : EngineBase {
       int j = 0;
       bool happy = false;
       double inv = 1.0 / beta;  // v_0 = r / beta (scale with a binary64 factor)
-      const T* wprev = gr;
       for (; j < m && total < spec.max_inner_iters; ++j, ++total) {
-        T* vj = V + (int64_t)j * ldv;
-        T* w = (j & 1) ? wB : wA;
-        V2([&](auto vt) {
-          constexpr int V_ = decltype(vt)::v;
-          if constexpr (SPARSE) {  // v_j = w / h as its own pass, then the gathered matvec
-            k_scale<T, V_, FUSED_GS><<<geo.nblk, nt, 0, s>>>(wprev, vj, inv, geo);
-            halo(h, vj);  // a row block's matvec reads v_j at the band beyond its rows
-            auto kern = k_gm_matvec<Op, T, C, V_, false>;
-            smem_attr(kern, win.bytes);
-            kern<<<geo.nblk, nt, win.bytes, s>>>(o, nullptr, 0.0, vj, V, w, geo, rd, h->st, win.band);
-            ++h->launches;
-          } else {
-            halo(h, wprev);
-            if (!gmmatvec25(o, wprev, inv, vj, w))
-              k_gm_matvec<Op, T, C, V_, true><<<geo.nblk, nt, 0, s>>>(o, wprev, inv, vj, V, w, geo, rd, h->st);
-          }
-          coll<C>(h, EpiHcol{0});
-          if constexpr (FUSED_GS) {
-            // accum = FP32: classical Gram-Schmidt in two passes (gadi_kernels.cuh)
-            const int64_t ps = h->partm_stride;
-            for (int i0 = 1; i0 <= j;) {
-              const int left = j - i0 + 1, J = h->sharded() ? 1 : std::min(left, 4);
-              if (J == 4) k_gm_dots<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
-              else if (J == 3) k_gm_dots<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
-              else if (J == 2) k_gm_dots<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
-              else k_gm_dots<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(w, V, ldv, i0, geo, rd, h->d_partm, ps, h->st);
-              if (J == 1) coll<C>(h, EpiHcol{i0});
-              i0 += J;
-              ++h->launches;
-            }
-            k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
-            coll<C>(h, EpiCgsNorm{j});
-            h->launches += 2;
-          } else {
-            for (int i = 0; i <= j; ++i) {
-              T* vi = V + (int64_t)i * ldv;
-              if (i < j) {
-                k_gm_mgs<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(w, vi, vi + ldv, i, geo, rd, h->st);
-                coll<C>(h, EpiHcol{i + 1});
-              } else {
-                CK(cudaMemsetAsync(&h->st->maxbits, 0, 8, s));
-                k_gm_mgs<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(w, vi, nullptr, i, geo, rd, h->st);
-                coll_flags(h, nullptr);  // max|w| over all ranks
-              }
-            }
-            k_norm2<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, &h->st->hcol[j + 1], geo, rd, h->st);
-            coll<C>(h, EpiNorm2{&h->st->hcol[j + 1]});
-            h->launches += j + 3;
-          }
-        });
-        CKL();
-        read_state(h);
-        for (int i = 0; i <= j + 1; ++i) HC(i, j) = h->h_st->hcol[i];
+        const double* col = h->h_st->hcol;
+        if (spec_ok) {
+          if (j == jq) queue_window(j);
+          col = h->h_st->hhist[j - win0];
+        } else {
+          arnoldi(j, inv, false, -1);
+          read_state(h, 1);
+        }
+        for (int i = 0; i <= j + 1; ++i) HC(i, j) = col[i];
         const double h1 = HC(j + 1, j);
         if (!std::isfinite(h1)) {
           status = INNER_OVERFLOW;
@@ -1176,7 +1295,6 @@ struct Engine final : EngineBase {
         // v_{j+1} = w / h1 happens inside the next matvec (skipped if h1 == 0:
         // the loop then ends at this step, below).
         inv = h1 != 0.0 ? 1.0 / h1 : 0.0;
-        wprev = w;
         for (int i = 0; i < j; ++i) {
           const double t1 = Rf(Rf(cs[i] * HC(i, j)) + Rf(sn[i] * HC(i + 1, j)));
           const double t2 = Rf(Rf(cs[i] * HC(i + 1, j)) - Rf(sn[i] * HC(i, j)));
@@ -1273,8 +1391,10 @@ struct Engine final : EngineBase {
       return false;
     } else {
       St25Geo gs;
-      // 2048-chunk tiles, 16 warps x 4 chunks (measured r06: 789 vs 854 us at C3)
-      if (!make_st25(h->n, 8, 1, gs, 2048, true, 0, h->i0, h->i1, 4, 512) &&
+      // k_resid64 where the shape fits; else k_st25 on 2048-chunk tiles, 16 warps x 4 chunks
+      const double c7[7] = {h->t2, h->t2, h->t2, h->t1, h->t3, h->t3, h->t3};
+      const bool fits64 = r64_fits(h->n, h->i0, h->i1, c7, gs);
+      if (!fits64 && !make_st25(h->n, 8, 1, gs, 2048, true, 0, h->i0, h->i1, 4, 512) &&
           !make_st25(h->n, 8, 1, gs, 1024, true, 0, h->i0, h->i1))
         return false;
       CK(cudaMemsetAsync(&h->st->maxbits, 0, sizeof(unsigned long long), h->stream));
@@ -1289,7 +1409,8 @@ struct Engine final : EngineBase {
                           scaling ? 1 : 0,
                           nsc_of(h->ns),
                           nsc_of(scaling ? 0 : h->ns)};
-      launch_st25(pol, gs, h->stream, red_of(h), h->st);
+      if (fits64) launch_resid64(pol, gs, h->stream, red_of(h), h->st);
+      else launch_st25(pol, gs, h->stream, red_of(h), h->st);
       CKL();
       ++h->launches;
       coll<double>(h, EpiResidSpec{scaling ? 1 : 0});

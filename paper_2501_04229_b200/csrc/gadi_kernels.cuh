@@ -39,6 +39,8 @@ struct Geo {
   __host__ __device__ int threads() const { return L * W; }
 };
 
+constexpr int GM_SPEC_MAX = 8;  // Arnoldi steps queued per host sync
+
 struct Red {
   double* part0;
   double* part1;
@@ -55,9 +57,9 @@ struct DevState {
   int flags;
   int cg_xvalid;
   unsigned long long maxbits;
-  // GMRES Arnoldi column, h(0..j+1, j)
-  double hcol[72];
-  double ycoef[72];
+  // speculative Arnoldi windows (fused mode): 1 / h(j+1, j) (or 1 / beta) for the next step's
+  // basis scaling, formed on the device
+  double gm_inv;
   // outer loop
   double res_ss, res_max, rhat_ss;
   int res_e, xbad;
@@ -68,6 +70,11 @@ struct DevState {
   // k_dist_finish): a peer may still be pulling record c while this rank's
   // next reduction writes record c+1.
   int dist, dist_par;
+  // ---- the head above is what read_state copies; the arrays below only on request
+  // GMRES Arnoldi column, h(0..j+1, j), and the columns of the steps of a speculative window
+  double hcol[72];
+  double hhist[GM_SPEC_MAX][72];
+  double ycoef[72];
   double dist_loc[2][4];
   double dist_all[2][4 * GADI_MAX_RANKS];
 };
@@ -787,11 +794,15 @@ __global__ void __launch_bounds__(256) k_gm_resid(Op op, const T* __restrict__ x
 // binary16 values is exact in binary32, so one rounding to binary16 is the
 // reference's scale), and the zero-start rules only touch -0 entries and
 // non-finite coefficients -- a chunk with neither is stored as it is.
+// v_0 = r / beta: the factor for a speculative first Arnoldi step (out of line, as gm_column_done)
+static __device__ __noinline__ void gm_beta_done(DevState* st) { st->gm_inv = 1.0 / st->red_c; }
 struct EpiResidF {
   template <class C>
   __device__ void finish(C ss32, double ss, DevState* st) const {
     st->red_d = ss;
-    st->red_c = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss32))));
+    const double beta = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss32))));
+    st->red_c = beta;
+    gm_beta_done(st);
   }
   __device__ int* flag_dst(DevState* st) const { return &st->flags; }
   __device__ bool skip(DevState* st) const { return (void)st, false; }
@@ -861,7 +872,9 @@ __global__ void __launch_bounds__(256) k_gm_resid0(Op op, const __half* __restri
 struct EpiSqrtRedC {
   template <class C>
   __device__ void finish(C ss, double, DevState* st) const {
-    st->red_c = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss))));
+    const double beta = to_dbl(Ar<C>::from_d(__dsqrt_rn(Ar<C>::to_d(ss))));
+    st->red_c = beta;
+    gm_beta_done(st);
   }
   __device__ int* flag_dst(DevState*) const { return nullptr; }
   __device__ bool skip(DevState* st) const { return (void)st, false; }
@@ -1186,6 +1199,14 @@ __global__ void __launch_bounds__(256) k_gm_dots(const T* __restrict__ w, const 
   }
 }
 
+// After column j of a speculative Arnoldi window is complete (one thread, its own launch so
+// that k_gm_cgs keeps its code): the host's inv for v_{j+1} = w / h1, and the column into
+// hhist[slot].
+static __global__ void k_gm_column_done(DevState* st, int j, int slot) {
+  const double h1 = st->hcol[j + 1];
+  st->gm_inv = h1 != 0.0 ? 1.0 / h1 : 0.0;
+  for (int i = 0; i <= j + 1; ++i) st->hhist[slot][i] = st->hcol[i];
+}
 struct EpiCgsNorm {  // h(j+1, j) = sqrt(dot(w, w)) in the inner arithmetic
   int j;
   template <class C>

@@ -319,9 +319,12 @@ __device__ __forceinline__ void st25_ticket(const P& pol, const St25Geo& g, cons
   __shared__ int s_last;
   R0* red0 = reinterpret_cast<R0*>(redb0);
   const int tid = threadIdx.x;
-  if (P::HAS_R0 || P::HAS_R1) __threadfence();
+  // the partials were written by threads t < IL <= 32 (st25_partials), all in warp 0 with the ticket thread
+  if ((P::HAS_R0 || P::HAS_R1) && tid < ST25_IL_MAX) __threadfence();
   if (P::HAS_MAX) block_max_abs(&st->maxbits, mloc);
   if (P::HAS_FLAG) or_flags(pol.flag_dst(st), flag);
+  // every warp's max / flag atomics precede this CTA's ticket (the last CTA reads them)
+  if (P::HAS_MAX || P::HAS_FLAG) __syncthreads();
   if (tid == 0) {
     __threadfence();
     const unsigned t = atomicAdd(rd.ticket, 1u);
@@ -985,8 +988,10 @@ struct PolGmMatvec {
   const T* v0;
   T* w;
   uint32_t ch[7];
+  int inv_dev;  // 1: inv is st->gm_inv, formed by the previous step's epilogue (no host sync in between)
   __device__ bool skip(DevState*) const { return false; }
-  __device__ void prepare(DevState*) {
+  __device__ void prepare(DevState* st) {
+    if (inv_dev) inv = *(volatile double*)&st->gm_inv;
     if constexpr (FASTH)
       for (int k = 0; k < 7; ++k) ch[k] = __half_as_ushort(__float2half_rn(c7[k]));
   }
