@@ -1224,7 +1224,16 @@ struct Engine final : EngineBase {
             i0 += J;
             ++h->launches;
           }
-          k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
+          if constexpr (V_ > 1) {
+            if (j == 0) k_gm_cgs_few<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            else if (j == 1) k_gm_cgs_few<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            else if (j == 2) k_gm_cgs_few<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            else if (j == 3) k_gm_cgs_few<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            else if (j == 4) k_gm_cgs_few<T, C, V_, 5><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            else k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
+          } else {
+            k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
+          }
           coll<C>(h, EpiCgsNorm{j});
           if (slot >= 0) k_gm_column_done<<<1, 1, 0, s>>>(h->st, j, slot);
           h->launches += 2;
@@ -1337,7 +1346,19 @@ struct Engine final : EngineBase {
       CK(cudaMemsetAsync(&h->st->flags, 0, 4, s));
       V2([&](auto vt) {
         constexpr int V_ = decltype(vt)::v;
-        k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, x_zero ? 1 : 0, V, ldv, j, geo, h->st);
+        const int xz = x_zero ? 1 : 0;
+        if constexpr (V_ > 1) {
+          switch (j) {
+            case 1: k_gm_update_few<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 2: k_gm_update_few<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 3: k_gm_update_few<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 4: k_gm_update_few<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 5: k_gm_update_few<T, C, V_, 5><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            default: k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, j, geo, h->st);
+          }
+        } else {
+          k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, j, geo, h->st);
+        }
       });
       CKL();
       ++h->launches;

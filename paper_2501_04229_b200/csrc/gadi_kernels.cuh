@@ -412,6 +412,28 @@ __device__ __forceinline__ float fhfma(__half a, __half b, float c) {
   return d;
 }
 
+template <int SA, int SB>  // SA / SB: which half (0 low, 1 high) of a / b
+__device__ __forceinline__ float fhf(uint32_t a, uint32_t b, float c) {
+  float d;
+  if constexpr (SA == 0 && SB == 0)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bl, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else if constexpr (SA == 0 && SB == 1)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bh, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else if constexpr (SA == 1 && SB == 0)
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bl, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  else
+    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bh, %3;}"
+        : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+// nonzero iff one of the two binary16 halves of w equals the pattern's half (pat2 = pat | pat << 16)
+__device__ __forceinline__ uint32_t any_half_eq(uint32_t w, uint32_t pat2) {
+  const uint32_t t = w ^ pat2;
+  return (t - 0x00010001u) & ~t & 0x80008000u;
+}
 template <class C, class T>
 struct MatvecF {  // acc + coef * x (kernels.cpp:47-52)
   // PACKED: binary32 folds may pair the products (FMUL2, fold_vec in
@@ -633,6 +655,48 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
   int bad = 0;
   C w0;
   double w1;
+  if constexpr (VEC == 8 && MatvecF<C, T>::EXACT_H) {
+    // binary16 storage, binary32 arithmetic: the chunks stay packed (two lanes per FMUL2 / F2FP,
+    // squares as FHFMA onto -0, finiteness from one bit test per word); the same operations per
+    // element and the same trees as the generic body below
+    const float2 a2 = make_float2(a, a), na2 = make_float2(na, na);
+    seg_run<VEC, true, true>(g, [&](const Seg& s, C& c, double& d) {
+      const int64_t ch = s.lo >> 3;
+      uint4 xu = make_uint4(0, 0, 0, 0);
+      if (!first) xu = reinterpret_cast<const uint4*>(x)[ch];
+      const uint4 ru = reinterpret_cast<const uint4*>(r)[ch];
+      const uint4 pu = __ldg(reinterpret_cast<const uint4*>(p) + ch);
+      const uint4 qu = __ldg(reinterpret_cast<const uint4*>(q) + ch);
+      const uint32_t xw[4] = {xu.x, xu.y, xu.z, xu.w}, rw[4] = {ru.x, ru.y, ru.z, ru.w};
+      const uint32_t pw[4] = {pu.x, pu.y, pu.z, pu.w}, qw[4] = {qu.x, qu.y, qu.z, qu.w};
+      uint32_t xo[4], ro[4], infs = 0;
+      float tc[8];
+      double td[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 xf = first ? make_float2(0.0f, 0.0f) : __half22float2(*reinterpret_cast<const __half2*>(&xw[k]));
+        const float2 ap = __fmul2_rn(a2, __half22float2(*reinterpret_cast<const __half2*>(&pw[k])));
+        const __half2 xn = __floats2half2_rn(__fadd_rn(xf.x, ap.x), __fadd_rn(xf.y, ap.y));
+        xo[k] = *reinterpret_cast<const uint32_t*>(&xn);
+        const float2 rf = __half22float2(*reinterpret_cast<const __half2*>(&rw[k]));
+        const float2 aq = __fmul2_rn(na2, __half22float2(*reinterpret_cast<const __half2*>(&qw[k])));
+        const __half2 rn = __floats2half2_rn(__fadd_rn(rf.x, aq.x), __fadd_rn(rf.y, aq.y));
+        ro[k] = *reinterpret_cast<const uint32_t*>(&rn);
+        tc[2 * k] = fhf<0, 0>(ro[k], ro[k], -0.0f);
+        tc[2 * k + 1] = fhf<1, 1>(ro[k], ro[k], -0.0f);
+        td[2 * k] = (double)tc[2 * k];
+        td[2 * k + 1] = (double)tc[2 * k + 1];
+        // an exponent field of all ones: r -> bit 0, x -> bit 1 of `bad`
+        infs |= (any_half_eq(ro[k] & 0x7c007c00u, 0x7c007c00u) ? 1u : 0u) |
+                (any_half_eq(xo[k] & 0x7c007c00u, 0x7c007c00u) ? 2u : 0u);
+      }
+      reinterpret_cast<uint4*>(x)[ch] = make_uint4(xo[0], xo[1], xo[2], xo[3]);
+      reinterpret_cast<uint4*>(r)[ch] = make_uint4(ro[0], ro[1], ro[2], ro[3]);
+      bad |= (int)infs;
+      c = seg_sum<C, G>(tc, G);
+      d = seg_sum<double, G>(td, G);
+    }, w0, w1);
+  } else
   seg_run<VEC, true, true>(g, [&](const Seg& s, C& c, double& d) {
     T xv[G], rv[G], pv[G], qv[G];
     if (!first) load_seg<T, VEC, G>(x, s, xv);
@@ -1266,6 +1330,69 @@ __global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __re
   if (grid_finish(w0, w1, g, rd, ss, dummy)) finish_red(EpiCgsNorm{j}, st, ss, dummy);
 }
 
+// k_gm_cgs for the first Arnoldi steps (NB = j + 1 <= 5 basis vectors): all of a segment's
+// loads are issued together, and with NB <= 2 the next segment's loads too (double buffer),
+// so at least four 16-byte loads per lane are in flight (the generic body has NB + 1: 198 us
+// for 0.8 GB at j = 0). Same per-element sequence and the same reduction tree.
+template <class T, class C, int VEC, int NB>
+__global__ void __launch_bounds__(256) k_gm_cgs_few(T* __restrict__ w, const T* __restrict__ V, int64_t ldv, Geo g,
+                                                    Red rd, DevState* st) {
+  GADI_G;
+  static_assert(VEC > 1, "aligned segments");
+  constexpr int j = NB - 1;
+  constexpr bool PF = NB <= 2;
+  C nh[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) nh[i] = Ar<C>::neg(from_dbl<C>(st->hcol[i]));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto seg_t = [&](int r) { return (((int64_t)blockIdx.x * g.W + warp) * g.R + r) * g.L + lane; };
+  T wv[PF ? 2 : 1][G], vb[PF ? 2 : 1][NB][G];
+  auto loads = [&](int r, int buf) {
+    const int64_t e0 = seg_t(r) * VEC;
+    ld_vec<T, VEC>(w, e0, wv[buf]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u) ld_vec<T, VEC>(V + (int64_t)u * ldv, e0, vb[buf][u]);
+  };
+  C a0[RMAX];
+  if (PF) loads(0, 0);
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r < g.R) {
+      const int buf = PF ? (r & 1) : 0;
+      if (PF) {
+        if (r + 1 < g.R) loads(r + 1, buf ^ 1);
+      } else {
+        loads(r, 0);
+      }
+      C acc[G];
+#pragma unroll
+      for (int e = 0; e < G; ++e) acc[e] = ld_c<T, C>(wv[buf][e]);
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+#pragma unroll
+        for (int e = 0; e < G; ++e) acc[e] = Ar<C>::add(acc[e], Ar<C>::mul(nh[u], ld_c<T, C>(vb[buf][u][e])));
+      C tc[G];
+      T ov[G];
+#pragma unroll
+      for (int e = 0; e < G; ++e) {
+        ov[e] = st_t<T, C>(acc[e]);
+        const C rr = ld_c<T, C>(ov[e]);
+        tc[e] = Ar<C>::mul(rr, rr);
+      }
+      st_vec<T, VEC>(w, seg_t(r) * VEC, ov);
+      a0[r] = warp_tree(seg_sum<C, G>(tc, G), g.L);
+    }
+  }
+#pragma unroll
+  for (int s2 = 1; s2 < RMAX; s2 <<= 1)
+#pragma unroll
+    for (int r = 0; r + s2 < RMAX; r += 2 * s2)
+      if (r + s2 < g.R) a0[r] = Ar<C>::add(a0[r], a0[r + s2]);
+  C ss;
+  double dummy;
+  if (grid_finish(a0[0], 0.0, g, rd, ss, dummy)) finish_red(EpiCgsNorm{j}, st, ss, dummy);
+}
+
 // x += y_0 v_0; x += y_1 v_1; ... (inner_solver.cpp:174), one pass, the
 // sequence of rounded axpys kept per element; x_zero: x starts at 0.
 template <class T, class C, int VEC>
@@ -1305,6 +1432,41 @@ __global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero
     for (int k = 0; k < G; ++k) {
       xv[k] = st_t<T, C>(xc[k]);
       if (GADI_LIVE(k)) bad |= finite_t(xv[k]) ? 0 : 1;
+    }
+    store_seg<T, VEC, G>(x, s, xv);
+  });
+  or_flags(&st->flags, bad);
+}
+
+// k_gm_update for a short cycle (NB = j <= 5 basis vectors): every load of a segment is issued
+// before the first axpy (the generic body reads the vectors past a multiple of four one at a
+// time). Same sequence of rounded axpys per element.
+template <class T, class C, int VEC, int NB>
+__global__ void __launch_bounds__(256) k_gm_update_few(T* __restrict__ x, int x_zero, const T* __restrict__ V,
+                                                       int64_t ldv, Geo g, DevState* st) {
+  GADI_G;
+  static_assert(VEC > 1, "aligned segments");
+  int bad = 0;
+  C y[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) y[i] = from_dbl<C>(st->ycoef[i]);
+  seg_each<VEC>(g, [&](const Seg& s) {
+    T xv[G], vb[NB][G];
+    if (!x_zero) load_seg<T, VEC, G>(x, s, xv);
+#pragma unroll
+    for (int u = 0; u < NB; ++u) load_seg<T, VEC, G>(V + (int64_t)u * ldv, s, vb[u]);
+    C xc[G];
+#pragma unroll
+    for (int k = 0; k < G; ++k) xc[k] = x_zero ? Ar<C>::zero() : ld_c<T, C>(xv[k]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+#pragma unroll
+      for (int k = 0; k < G; ++k)
+        xc[k] = ld_c<T, C>(st_t<T, C>(Ar<C>::add(xc[k], Ar<C>::mul(y[u], ld_c<T, C>(vb[u][k])))));
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      xv[k] = st_t<T, C>(xc[k]);
+      bad |= finite_t(xv[k]) ? 0 : 1;
     }
     store_seg<T, VEC, G>(x, s, xv);
   });

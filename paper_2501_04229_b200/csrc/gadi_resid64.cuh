@@ -313,10 +313,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_resid64(const P pol, St25Geo 
 }
 
 // ------------------------------------------------ packed zero-start residual
-__device__ __forceinline__ uint32_t any_half_eq(uint32_t w, uint32_t pat2) {  // nonzero iff a half of w equals pat
-  const uint32_t t = w ^ pat2;
-  return (t - 0x00010001u) & ~t & 0x80008000u;
-}
 
 template <class Op>
 __global__ void __launch_bounds__(256) k_gm_resid0p(Op op, const __half* __restrict__ src, __half* __restrict__ r,

@@ -144,23 +144,6 @@ __device__ __forceinline__ void mul_vec(C a, const X (&x)[VEC], C (&out)[VEC]) {
 // product on these paths multiplies two binary16 values, exact in binary32,
 // so a fused op rounds exactly once where the reference rounds the sum (see
 // fhfma in gadi_kernels.cuh): the bits are the reference's.
-template <int SA, int SB>  // SA / SB: which half (0 low, 1 high) of a / b
-__device__ __forceinline__ float fhf(uint32_t a, uint32_t b, float c) {
-  float d;
-  if constexpr (SA == 0 && SB == 0)
-    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bl, %3;}"
-        : "=f"(d) : "r"(a), "r"(b), "f"(c));
-  else if constexpr (SA == 0 && SB == 1)
-    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bh, %3;}"
-        : "=f"(d) : "r"(a), "r"(b), "f"(c));
-  else if constexpr (SA == 1 && SB == 0)
-    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bl, %3;}"
-        : "=f"(d) : "r"(a), "r"(b), "f"(c));
-  else
-    asm("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bh, %3;}"
-        : "=f"(d) : "r"(a), "r"(b), "f"(c));
-  return d;
-}
 // a.half(S) + c in binary32, one rounding (FHADD)
 template <int S>
 __device__ __forceinline__ float fhadd(uint32_t a, float c) {
