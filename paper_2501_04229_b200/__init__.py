@@ -687,6 +687,18 @@ class GprModel:
         _check(lib().gadi_gpr_predict(self._h, _p(sizes), len(sizes), _p(mean), _p(sd)))
         return mean, sd
 
+    def predict_sharded(self, sizes, rank, world, group=None, gather=True):
+        """predict_alpha over a rank's slice of the queries (they are independent: no
+        data-path exchange); with gather=True every rank returns all (mean, sd), assembled
+        in rank order over torch.distributed. Each query's result is the bits of predict()."""
+        from .partition import gather_queries, query_shard
+        sizes = _f64(sizes)
+        lo, hi = query_shard(len(sizes), world, rank)
+        mean, sd = self.predict(sizes[lo:hi]) if hi > lo else (np.empty(0), np.empty(0))
+        if not gather:
+            return mean, sd
+        return gather_queries(mean, sd, len(sizes), group)
+
     def close(self):
         if self._h:
             lib().gadi_gpr_destroy(self._h)

@@ -177,3 +177,43 @@ def exchange_band(blk: RowBlock, x_local, group=None):
     for r in reqs:
         r.wait()
     return torch.cat([t for t in (below, x_local, above) if t is not None])
+
+
+# ------------------------------------------------------------ GPR query shards
+def query_shard(q_len: int, world: int, rank: int):
+    """Rank r's contiguous slice [lo, hi) of q_len prediction queries (SURVEY
+    §8(e), C5): the queries are independent, so the predictor shards them with
+    no data-path exchange; slices differ by at most one query."""
+    if not (0 <= rank < world) or q_len < 0:
+        raise ValueError("bad shard")
+    base, rem = divmod(q_len, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def gather_queries(local_mean, local_sd, q_len: int, group=None):
+    """All ranks' slices of (mean, sd) assembled in rank order on every rank
+    (one all_gather of padded slices; gloo or nccl)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    width = (q_len + world - 1) // world
+    pad = torch.zeros(2, width, dtype=torch.float64)
+    pad[0, : len(local_mean)] = torch.as_tensor(np.asarray(local_mean, dtype=np.float64))
+    pad[1, : len(local_sd)] = torch.as_tensor(np.asarray(local_sd, dtype=np.float64))
+    dev = None
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        pad = pad.to(dev)
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    mean = np.empty(q_len)
+    sd = np.empty(q_len)
+    for r in range(world):
+        lo, hi = query_shard(q_len, world, r)
+        t = parts[r].cpu().numpy()
+        mean[lo:hi] = t[0, : hi - lo]
+        sd[lo:hi] = t[1, : hi - lo]
+    return mean, sd

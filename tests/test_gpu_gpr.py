@@ -115,3 +115,24 @@ def test_default_path_choice_follows_error_model():
     m.predict(q[:512])
     assert m.timings()["variance_path"] == "fp64"
     m.close()
+
+
+@pytest.mark.parametrize("path", ["tensor", "fp64"])
+def test_query_shards_equal_full_prediction(monkeypatch, path):
+    """the queries shard across ranks with no exchange; each
+    rank's slice (predict_sharded, gather=False) holds the bits of the full
+    prediction at its queries, for uneven slices and both variance paths."""
+    from bench import c5_data
+    from paper_2501_04229_b200.partition import query_shard
+    sizes, alphas, q, fixed = c5_data()
+    q = q[:20011]
+    monkeypatch.setenv("GADI_GPR_VAR", path)
+    m = g.gpr_fit(sizes, alphas, fixed=fixed)
+    mean, sd = m.predict(q)
+    for world in (2, 3):
+        for rank in range(world):
+            lo, hi = query_shard(len(q), world, rank)
+            ml, sl = m.predict_sharded(q, rank, world, gather=False)
+            assert np.array_equal(ml.view(np.int64), mean[lo:hi].view(np.int64))
+            assert np.array_equal(sl.view(np.int64), sd[lo:hi].view(np.int64))
+    m.close()

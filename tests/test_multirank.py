@@ -219,3 +219,52 @@ def test_gloo_row_block_protocol(orc):
     for r in range(world):
         assert out[r]["split_ok"] and out[r]["matvec_ok"]
         assert np.array([out[r]["dot"]]).view(np.int64)[0] == np.array([want]).view(np.int64)[0]
+
+
+# ------------------------------------------------------------ GPR query shards
+def test_query_shard_covers_all():
+    from paper_2501_04229_b200.partition import query_shard
+
+    for q_len in (0, 1, 5, 64, 65536, 65537):
+        for world in (1, 2, 3, 8):
+            spans = [query_shard(q_len, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == q_len
+            assert all(spans[r][1] == spans[r + 1][0] for r in range(world - 1))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _qs_worker(rank, world, port, q_len, out_q):
+    import torch.distributed as dist
+
+    from paper_2501_04229_b200.partition import gather_queries, query_shard
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        xs = np.arange(q_len, dtype=np.float64) * 0.37 + 1.0
+        lo, hi = query_shard(q_len, world, rank)
+        # a stand-in for predict(): any per-query function (the queries are independent)
+        mean, sd = gather_queries(np.sin(xs[lo:hi]), np.sqrt(xs[lo:hi]), q_len)
+        out_q.put((rank, bool(np.array_equal(mean, np.sin(xs)) and np.array_equal(sd, np.sqrt(xs)))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("q_len", [7, 1000])
+def test_gloo_query_shards(q_len):
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_qs_worker, args=(r, world, port, q_len, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(out[r] for r in range(world))

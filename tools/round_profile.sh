@@ -18,7 +18,7 @@ ncu -f --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.s
 python tools/profile_step.py --workload c4 --outer 1 > "$OUT/profile_step_c4_plain.txt" 2>&1 && \
 ncu -f --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file "$OUT/launches_c4_outer1.csv" python tools/profile_step.py --workload c4 --outer 1 > /dev/null 2>&1
-for k in PolSpmvp PolGmMatvec k_cg_update k_gm_cgs k_gm_dots PolResidSpec k_gm_resid; do
+for k in PolSpmvp PolGmMatvec k_cg_update k_gm_cgs_few k_gm_dots k_resid64 k_gm_resid0p k_gm_update_few; do
   ncu -f --set full --import-source on --clock-control none --kernel-name-base demangled -k regex:$k \
     --launch-skip 2 -c 1 -o /tmp/full_$k python tools/profile_step.py --outer 1 > /dev/null 2>&1
   ncu -i /tmp/full_$k.ncu-rep --page raw --csv > "$OUT/raw_$k.csv"
