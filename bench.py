@@ -289,7 +289,8 @@ def run_c5(args, rank, world):
         peak_kind = "measured (bf16 burst)"
     ach = tens_flops / (vms / 1e3) / 1e12 if tm["variance_path"] == "tensor" else None
     out = {"metric": metric, "value": dt, "unit": "s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": False, "scaling": "weak",
+           "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": False,
+           "scaling": "strong" if world > 1 else "weak",
            "vs_baseline": None, "dtype": "f64 fit / f16 hi+lo tensor-core variances (f32 accumulate)",
            "data": "synthetic", "config": cfg,
            "e2e": {"value": dt, "unit": "s", "h2d_bytes_per_step": 8 * (2 * mq + nq),

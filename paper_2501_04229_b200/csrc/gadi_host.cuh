@@ -234,12 +234,9 @@ inline void launch_st25(const P& pol, const St25Geo& g, cudaStream_t s, const Re
 // k_resid64 (gadi_resid64.cuh): tile of threads*CPT 16-byte chunks per plane,
 // S staged planes of TJ+2 rows. Variants (threads, CPT, CTAs per SM) are
 // compile-time; GADI_R64 picks one (0: off, the k_st25 passes run).
-inline int r64_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("GADI_R64");
-    return e ? std::atoi(e) : 4;
-  }();
-  return v;
+inline int r64_variant() {  // read per launch (a test switch; one getenv per outer step)
+  const char* e = std::getenv("GADI_R64");
+  return e ? std::atoi(e) : 4;
 }
 inline bool make_r64(int64_t n, int64_t i0, int64_t i1, int threads, int cpt, int S, St25Geo& g) {
   if (i1 < 0) i1 = n;
@@ -287,13 +284,12 @@ inline void launch_resid64_v(const P& pol, const St25Geo& g, cudaStream_t s, con
 }
 template <class P>
 inline void launch_resid64(const P& pol, const St25Geo& g, cudaStream_t s, const Red& rd, DevState* st) {
-  switch (r64_variant()) {  // g comes from r64_fits of the same variant
-    case 1: return launch_resid64_v<P, 2, 512, 1, 4>(pol, g, s, rd, st);
-    case 2: return launch_resid64_v<P, 4, 256, 2, 4>(pol, g, s, rd, st);
-    case 3: return launch_resid64_v<P, 2, 256, 2, 4>(pol, g, s, rd, st);
-    case 5: return launch_resid64_v<P, 2, 512, 1, 8>(pol, g, s, rd, st);
-    default: return launch_resid64_v<P, 4, 512, 1, 4>(pol, g, s, rd, st);
-  }
+  // the variant r64_fits built g for (threads, chunks per thread, stages)
+  if (g.threads == 512 && g.CPT == 2 && g.stages == 4) return launch_resid64_v<P, 2, 512, 1, 4>(pol, g, s, rd, st);
+  if (g.threads == 256 && g.CPT == 4) return launch_resid64_v<P, 4, 256, 2, 4>(pol, g, s, rd, st);
+  if (g.threads == 256 && g.CPT == 2) return launch_resid64_v<P, 2, 256, 2, 4>(pol, g, s, rd, st);
+  if (g.threads == 512 && g.CPT == 2) return launch_resid64_v<P, 2, 512, 1, 8>(pol, g, s, rd, st);
+  return launch_resid64_v<P, 4, 512, 1, 4>(pol, g, s, rd, st);
 }
 
 // k_st25h geometry: the k_st25 tiling with a padded 3-plane operand ring;
@@ -1132,10 +1128,8 @@ struct Engine final : EngineBase {
     // (gm_inv) and its column kept in hhist -- and the host reads the whole window with one
     // sync, then rotates the columns in order. A step past the one where the host stops
     // (convergence, breakdown, overflow) only wrote basis / work vectors nobody reads.
-    static const bool spec_env = [] {
-      const char* e = std::getenv("GADI_GM_SPEC");
-      return !e || std::atoi(e) != 0;
-    }();
+    const char* spec_e = std::getenv("GADI_GM_SPEC");  // a test switch, read per solve
+    const bool spec_env = !spec_e || std::atoi(spec_e) != 0;
     const bool spec_ok = FUSED_GS && !SPARSE && st25 && spec_env;
     auto resid = [&](bool sync = true) {  // r = rhs - S x ; flags, max, ||r||_2 (binary64), norm2 in fmt
       if (lazy && !x_zero) {

@@ -393,3 +393,54 @@ def test_fast_path_whole_solve_n256_equals_generic(monkeypatch):
     assert res.report.inner_iter_totals == ref.report.inner_iter_totals
     assert same(res.x, ref.x)
     assert same(res.report.rel_residual_history, ref.report.rel_residual_history)
+
+
+@pytest.mark.parametrize("n,fmt,accum", [(64, HALF, True), (64, SINGLE, False), (128, HALF, True)])
+def test_resid64_variants_equal_st25(monkeypatch, n, fmt, accum):
+    """The dedicated binary64 outer-residual kernel (k_resid64, n >= 64: both the
+    two-pass PolResidA route of the first steps and the speculative PolResidSpec
+    pass) against the generic k_st25 passes (GADI_R64=0, validated against the
+    oracle at small n), for every compiled variant: x, history and counts bit for bit."""
+    S = g.build_convdiff3d(n, r=0.0975)
+    b = np.random.default_rng(5).uniform(-1, 1, n ** 3)
+    b[7::13] *= 1e-6
+    cfg = g.GadiConfig(alpha=0.3, xi=1e-20, u_r=g.Precision(fmt), max_outer_iters=6,
+                       accum=g.Accum.Fp32 if accum else g.Accum.Native,
+                       inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30))
+    monkeypatch.setenv("GADI_R64", "0")
+    ref = g.gadi_ir_solve(S, b, g.hss_split(S), cfg)
+    for v in ("1", "2", "3", "4", "5"):
+        monkeypatch.setenv("GADI_R64", v)
+        res = g.gadi_ir_solve(S, b, g.hss_split(S), cfg)
+        assert res.report.outer_iters == ref.report.outer_iters == 6
+        assert same(res.x, ref.x), v
+        assert same(res.report.rel_residual_history, ref.report.rel_residual_history), v
+    monkeypatch.delenv("GADI_R64")
+
+
+@pytest.mark.parametrize("eps,max_inner,restart", [(1e-9, 40, 12), (1e-12, 5, 30), (1e-6, 40, 5)])
+def test_speculative_arnoldi_windows_equal_stepwise(monkeypatch, eps, max_inner, restart):
+    """Fused-mode GMRES with the Arnoldi steps queued in windows of up to 8 (one
+    host sync per window, 1/h formed on the device) against the step-by-step
+    loop (GADI_GM_SPEC=0): windows that cross restarts, that end by convergence
+    in mid-window, and the C3 shape (5 steps, one window) -- same x, counts, status."""
+    n = 32
+    S = g.build_convdiff3d(n, r=0.0975)
+    rng = np.random.default_rng(17)
+    rhs = rng.uniform(-1, 1, n ** 3).astype(np.float16).astype(np.float64)
+    rhs[3::11] = -0.0
+    stop = float(np.sqrt(np.sum(rhs * rhs)))
+    spec = g.InnerSolverSpec(g.InnerMethod.Gmres, eps, max_inner, restart)
+
+    def run():
+        sysx = g.CudaGadiSystem(S)
+        sysx.prepare(0.2, 1.0, g.Precision.Half, spec, g.Accum.Fp32)
+        sysx.set_inner_stop_norm(stop)
+        return sysx.solve_S(rhs)
+
+    x, it, st = run()
+    monkeypatch.setenv("GADI_GM_SPEC", "0")
+    wx, wit, wst = run()
+    monkeypatch.delenv("GADI_GM_SPEC")
+    assert (it, int(st)) == (wit, int(wst))
+    assert same(x, wx)
