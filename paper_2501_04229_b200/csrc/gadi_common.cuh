@@ -252,7 +252,12 @@ __device__ __forceinline__ __half shfl_xor_c<__half>(__half v, int o, unsigned m
 // every participating lane ends with the total.
 template <class C>
 __device__ __forceinline__ C warp_tree(C v, int width) {
-  const unsigned mask = width >= 32 ? 0xffffffffu : ((1u << width) - 1u);
+  if (width >= 32) {  // the usual case: five unconditional levels (one uniform branch, not five)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) v = Ar<C>::add(v, shfl_xor_c(v, o, 0xffffffffu));
+    return v;
+  }
+  const unsigned mask = (1u << width) - 1u;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1)
     if (o < width) v = Ar<C>::add(v, shfl_xor_c(v, o, mask));

@@ -1229,7 +1229,10 @@ struct Engine final : EngineBase {
             k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
           }
           coll<C>(h, EpiCgsNorm{j});
-          if (slot >= 0) k_gm_column_done<<<1, 1, 0, s>>>(h->st, j, slot);
+          if (slot >= 0) {
+            k_gm_column_done<<<1, 1, 0, s>>>(h->st, j, slot);
+            ++h->launches;
+          }
           h->launches += 2;
         } else {
           for (int i = 0; i <= j; ++i) {
