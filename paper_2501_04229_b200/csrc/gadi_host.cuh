@@ -1088,7 +1088,9 @@ struct Engine final : EngineBase {
           k_cg_spmvp<Op, T, C, V_><<<geo.nblk, nt, 0, s>>>(o, r, p_in, p_out, q, first, geo, rd, h->st);
         }
         coll<C>(h, EpiCgPap{});
-        k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st);
+        // the residual vector is dead after the last possible iteration (the next outer step rewrites rhat)
+        k_cg_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, r, p_out, q, first, geo, rd, h->st,
+                                                      it + 1 < spec.max_inner_iters ? 1 : 0);
         coll<C>(h, EpiCgUpdate{});
       });
       CKL();
@@ -1186,7 +1188,7 @@ struct Engine final : EngineBase {
       if (sync) read_state(h);
     };
     // one Arnoldi step's kernels: v_j = w_prev * inv, w = S v_j, the column h(., j)
-    auto arnoldi = [&](int j, double inv, bool inv_dev, int slot) {
+    auto arnoldi = [&](int j, double inv, bool inv_dev, int slot, bool last) {  // last: no step follows in this cycle
       const T* wprev = j == 0 ? gr : (((j - 1) & 1) ? wB : wA);
       T* vj = V + (int64_t)j * ldv;
       T* w = (j & 1) ? wB : wA;
@@ -1219,11 +1221,16 @@ struct Engine final : EngineBase {
             ++h->launches;
           }
           if constexpr (V_ > 1) {
-            if (j == 0) k_gm_cgs_few<T, C, V_, 1><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
-            else if (j == 1) k_gm_cgs_few<T, C, V_, 2><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
-            else if (j == 2) k_gm_cgs_few<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
-            else if (j == 3) k_gm_cgs_few<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
-            else if (j == 4) k_gm_cgs_few<T, C, V_, 5><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            auto few = [&](auto nbt) {  // the last step of a cycle reduces the updated w without storing it
+              constexpr int NB = decltype(nbt)::value;
+              if (last) k_gm_cgs_few<T, C, V_, NB, false><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+              else k_gm_cgs_few<T, C, V_, NB, true><<<geo.nblk, nt, 0, s>>>(w, V, ldv, geo, rd, h->st);
+            };
+            if (j == 0) few(std::integral_constant<int, 1>{});
+            else if (j == 1) few(std::integral_constant<int, 2>{});
+            else if (j == 2) few(std::integral_constant<int, 3>{});
+            else if (j == 3) few(std::integral_constant<int, 4>{});
+            else if (j == 4) few(std::integral_constant<int, 5>{});
             else k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
           } else {
             k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
@@ -1258,7 +1265,8 @@ struct Engine final : EngineBase {
       int jq = 0, win0 = 0;  // steps queued so far in this cycle; first step of the current window
       auto queue_window = [&](int j0) {
         const int hi = std::min({m, j0 + GM_SPEC_MAX, j0 + (spec.max_inner_iters - total)});
-        for (int jj = j0; jj < hi; ++jj) arnoldi(jj, 0.0, true, jj - j0);
+        for (int jj = j0; jj < hi; ++jj)
+          arnoldi(jj, 0.0, true, jj - j0, jj + 1 == m || total + (jj - j0) + 1 == spec.max_inner_iters);
         win0 = j0;
         jq = hi;
         read_state(h, 2);
@@ -1289,7 +1297,7 @@ struct Engine final : EngineBase {
           if (j == jq) queue_window(j);
           col = h->h_st->hhist[j - win0];
         } else {
-          arnoldi(j, inv, false, -1);
+          arnoldi(j, inv, false, -1, j + 1 == m || total + 1 == spec.max_inner_iters);
           read_state(h, 1);
         }
         for (int i = 0; i <= j + 1; ++i) HC(i, j) = col[i];

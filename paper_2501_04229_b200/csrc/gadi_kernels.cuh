@@ -647,7 +647,9 @@ __global__ void __launch_bounds__(256) k_cg_pupd(const T* __restrict__ r, const 
 template <class T, class C, int VEC>
 __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
                                                    const T* __restrict__ q, int first, Geo g, Red rd,
-                                                   DevState* st) {
+                                                   DevState* st, int keep_r = 1) {
+  // keep_r = 0: the solve ends with this iteration whatever the stop test says (it is
+  // iteration max_inner), and nothing reads the residual vector afterwards: r is reduced, not stored
   if (*(volatile int*)&st->cg_done) return;
   GADI_G;
   const C a = from_dbl<C>(st->cg_a);
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
                 (any_half_eq(xo[k] & 0x7c007c00u, 0x7c007c00u) ? 2u : 0u);
       }
       reinterpret_cast<uint4*>(x)[ch] = make_uint4(xo[0], xo[1], xo[2], xo[3]);
-      reinterpret_cast<uint4*>(r)[ch] = make_uint4(ro[0], ro[1], ro[2], ro[3]);
+      if (keep_r) reinterpret_cast<uint4*>(r)[ch] = make_uint4(ro[0], ro[1], ro[2], ro[3]);
       bad |= (int)infs;
       c = seg_sum<C, G>(tc, G);
       d = seg_sum<double, G>(td, G);
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(T* __restrict__ x, T* __re
       }
     }
     store_seg<T, VEC, G>(x, s, xv);
-    store_seg<T, VEC, G>(r, s, rv);
+    if (keep_r) store_seg<T, VEC, G>(r, s, rv);
     c = seg_sum<C, G>(tc, s.len);
     d = seg_sum<double, G>(td, s.len);
   }, w0, w1);
@@ -1334,7 +1336,9 @@ __global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __re
 // loads are issued together, and with NB <= 2 the next segment's loads too (double buffer),
 // so at least four 16-byte loads per lane are in flight (the generic body has NB + 1: 198 us
 // for 0.8 GB at j = 0). Same per-element sequence and the same reduction tree.
-template <class T, class C, int VEC, int NB>
+// STORE = false: the last step of a cycle (restart or max_inner reached) -- the updated w is
+// only reduced (h(j+1, j)), nothing reads it afterwards.
+template <class T, class C, int VEC, int NB, bool STORE = true>
 __global__ void __launch_bounds__(256) k_gm_cgs_few(T* __restrict__ w, const T* __restrict__ V, int64_t ldv, Geo g,
                                                     Red rd, DevState* st) {
   GADI_G;
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(256) k_gm_cgs_few(T* __restrict__ w, const T* 
         const C rr = ld_c<T, C>(ov[e]);
         tc[e] = Ar<C>::mul(rr, rr);
       }
-      st_vec<T, VEC>(w, seg_t(r) * VEC, ov);
+      if constexpr (STORE) st_vec<T, VEC>(w, seg_t(r) * VEC, ov);
       a0[r] = warp_tree(seg_sum<C, G>(tc, G), g.L);
     }
   }
