@@ -256,6 +256,7 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
   // pass also yields true_residual_norm (the reference recomputes it).
   int ex = 0;
   double tnorm = 0.0, rhat_n = 0.0;  // ||b - A x||_2 and ||rhat||_2 (in the scaled frame), binary64
+  bool rhat_ss_at0 = false;          // st->rhat_ss = sum of rhat^2 unscaled (ns_r = 0): what k_cg_init would reduce
   // spec: when u_f is binary64, first try the single pass that also rounds
   // rhat with the previous step's exponent (accepted iff the exponent is
   // unchanged -- the usual case; else the two-pass route below reruns).
@@ -280,6 +281,7 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
       if (res_norm_ok(h) && h->h_st->res_e == ex) {
         rhat_n = std::ldexp(std::sqrt(h->h_st->rhat_ss), ns_r);
         tnorm = res_norm(h);
+        rhat_ss_at0 = ns_r == 0;
         return;
       }
     }
@@ -289,6 +291,7 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     read_state(h);
     ex = h->h_st->res_e;
     rhat_n = std::ldexp(std::sqrt(h->h_st->rhat_ss), ns_r);
+    rhat_ss_at0 = ns_r == 0;
     if (cfg->u_f != GADI_DOUBLE) {
       OuterA::resid_sync(h, h->d_x, nullptr, GADI_DOUBLE, false);
       tnorm = res_norm(h);
@@ -331,9 +334,12 @@ void run(gadi_handle* h, const gadi_config* cfg, gadi_report* rep) {
     const double target = cfg->inner.tol_epsilon * stop_norm;
     CK(cudaEventRecord(h->evA, s));
     // solve_H uses the spec method (solver.cpp:212-216)
+    // rhat's binary64 sum of squares is on the device from the pass that produced it (rsr)
+    e->rhs_ss_known = !lu && cfg->inner.method == GADI_INNER_CG && rhat_ss_at0;
     InnerOut zo = lu                                  ? lu_solve(h, e, 1, e->rhat, e->z)
                   : cfg->inner.method == GADI_INNER_CG ? e->cg(1, e->rhat, e->z, target)
                                                        : e->gmres(1, e->rhat, e->z, target);
+    e->rhs_ss_known = false;
     CK(cudaEventRecord(h->evB, s));
     rep->inner_iter_totals += zo.iters;
     rep->h_iters += zo.iters;

@@ -737,6 +737,9 @@ struct EngineBase {
   double alpha = 1, omega = 1;
   // inner-format device vectors (type-erased)
   void *rhat = nullptr, *z = nullptr, *pz = nullptr, *y = nullptr;
+  // set by the outer loop right before cg(): rhs is the rhat an outer residual pass just
+  // produced, and st->rhat_ss holds its binary64 sum of squares at scale 2^0 (consumed by cg)
+  bool rhs_ss_known = false;
   // H/S solves on inner-format device vectors; CG consumes rhs (r in place)
   virtual InnerOut cg(int which, void* rhs, void* x, double target) = 0;
   virtual InnerOut gmres(int which, const void* rhs, void* x, double target) = 0;
@@ -1052,13 +1055,28 @@ struct Engine final : EngineBase {
     const Op& o = op(which);
     const int nt = geo.threads();
     *(volatile int*)h->h_done = 0;
+    bool known = rhs_ss_known && rhs_v == rhat;
+    rhs_ss_known = false;
+    if (known && std::getenv("GADI_CHECK_SS")) {
+      // self-check (tests): reduce the binary64 sum here too and compare it with the outer pass's
+      V2([&](auto vt) {
+        constexpr int V_ = decltype(vt)::v;
+        k_cg_init<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(r, spec.max_inner_iters, target, geo, rd, h->st);
+      });
+      CKL();
+      coll<C>(h, EpiCgInit{spec.max_inner_iters, target, 0});
+      read_state(h);
+      if (std::memcmp(&h->h_st->red_d, &h->h_st->rhat_ss, sizeof(double)) != 0)
+        throw Err{GADI_E_STATE, "k_cg_init: the outer pass's sum of squares of rhat differs from the CG pass's"};
+    }
     V2([&](auto vt) {
       constexpr int V_ = decltype(vt)::v;
-      k_cg_init<T, C, V_><<<geo.nblk, nt, 0, s>>>(r, spec.max_inner_iters, target, geo, rd, h->st);
+      if (known) k_cg_init<T, C, V_, false><<<geo.nblk, nt, 0, s>>>(r, spec.max_inner_iters, target, geo, rd, h->st);
+      else k_cg_init<T, C, V_, true><<<geo.nblk, nt, 0, s>>>(r, spec.max_inner_iters, target, geo, rd, h->st);
     });
     CKL();
     ++h->launches;
-    coll<C>(h, EpiCgInit{spec.max_inner_iters, target});
+    coll<C>(h, EpiCgInit{spec.max_inner_iters, target, known ? 1 : 0});
     const int kAhead = (int)h->ring.size();
     for (int it = 0; it < spec.max_inner_iters; ++it) {
       if (it >= kAhead) {

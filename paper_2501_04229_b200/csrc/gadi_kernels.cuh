@@ -482,8 +482,11 @@ struct MatvecAF {  // b = A x in binary64 (problems.cpp:44)
 struct EpiCgInit {  // inner_solver.cpp:51-57
   int max_inner;
   double target;
+  int known;  // 1: ||r||^2 (binary64) is st->rhat_ss, reduced by the outer pass that produced r = rhat
   template <class C>
   __device__ void finish(C rs, double ss, DevState* st) const {
+    st->red_d = ss;  // the sum this pass reduced (GADI_CHECK_SS compares it with rhat_ss)
+    if (known) ss = st->rhat_ss;
     st->cg_rs = to_dbl(rs);
     st->cg_it = 0;
     st->cg_flags = 0;
@@ -548,33 +551,38 @@ struct EpiHcol {  // an Arnoldi coefficient h(i, j)
 
 // r = rhs (in place), rs = dot(r, r) and the initial stop test
 // (inner_solver.cpp:51-57). x and p are produced by the first iteration.
-template <class T, class C, int VEC>
+// DBL = false: the binary64 ||r||^2 of the stop test is already known (r is the rhat an outer
+// residual pass just produced and reduced over the same tree: st->rhat_ss), so only the
+// inner-format dot is reduced -- no binary64 conversions, adds or second tree.
+template <class T, class C, int VEC, bool DBL = true>
 __global__ void __launch_bounds__(256) k_cg_init(const T* __restrict__ r, int max_inner, double target, Geo g,
                                                  Red rd, DevState* st) {
   GADI_G;
   C w0;
   double w1;
-  seg_run_ld<VEC, true, true, G>(g, r, [&](const Seg& s, const T (&v)[G], C& c, double& d) {
+  seg_run_ld<VEC, true, DBL, G>(g, r, [&](const Seg& s, const T (&v)[G], C& c, double& d) {
     C tc[G];
     double td[G];
 #pragma unroll
     for (int i = 0; i < G; ++i) {
       if constexpr (MatvecF<C, T>::EXACT_H) {  // the square of a binary16 value is exact in binary32
         tc[i] = fhfma(v[i], v[i], -0.0f);
-        td[i] = (double)tc[i];
+        if (DBL) td[i] = (double)tc[i];
       } else {
         const C cv = ld_c<T, C>(v[i]);
         tc[i] = Ar<C>::mul(cv, cv);
-        const double dv = to_dbl(v[i]);
-        td[i] = __dmul_rn(dv, dv);
+        if (DBL) {
+          const double dv = to_dbl(v[i]);
+          td[i] = __dmul_rn(dv, dv);
+        }
       }
     }
     c = seg_sum<C, G>(tc, s.len);
-    d = seg_sum<double, G>(td, s.len);
+    if (DBL) d = seg_sum<double, G>(td, s.len);
   }, w0, w1);
   C rs;
   double ss;
-  if (grid_finish(w0, w1, g, rd, rs, ss)) finish_red(EpiCgInit{max_inner, target}, st, rs, ss);
+  if (grid_finish(w0, w1, g, rd, rs, ss)) finish_red(EpiCgInit{max_inner, target, DBL ? 0 : 1}, st, rs, ss);
 }
 
 // p_out = r + beta p_in (or r on the first iteration; inner_solver.cpp:53,76),

@@ -444,3 +444,33 @@ def test_speculative_arnoldi_windows_equal_stepwise(monkeypatch, eps, max_inner,
     monkeypatch.delenv("GADI_GM_SPEC")
     assert (it, int(st)) == (wit, int(wst))
     assert same(x, wx)
+
+
+@pytest.mark.parametrize("kind,fmt,accum", [("stencil", HALF, True), ("stencil", SINGLE, False), ("stencil", DOUBLE, False),
+                                            ("band", HALF, True)])
+def test_cg_start_reuses_outer_sum_of_squares(orc, monkeypatch, kind, fmt, accum):
+    """The H solve's start (k_cg_init) takes the binary64 ||rhat||^2 of its stop test from the
+    outer pass that produced rhat (same values, same tree) and reduces only the inner-format
+    dot. GADI_CHECK_SS makes the library reduce it again and throw if one bit differs, on
+    stencil (n = 64: k_resid64; two-pass steps and speculative steps) and SELL systems; the
+    solve must also equal the oracle's."""
+    if kind == "stencil":
+        n = 64 if fmt != DOUBLE else 16
+        S, A = stencil_and_csr(orc, n, r=0.0975 if n == 64 else None)
+        alpha = 0.3
+    else:
+        A = orc.band(8192, 26, 300, 4)
+        S = g.build_band_csr(8192, 26, 300, 4)
+        alpha = 3.0
+    _, b = orc.make_rhs(A, 1, -1.0, 1.0)
+    gcfg = g.GadiConfig(alpha=alpha, xi=1e-20, u_r=g.Precision(fmt), stall_window=400, max_outer_iters=8,
+                        accum=g.Accum.Fp32 if accum else g.Accum.Native,
+                        inner=g.InnerSolverSpec(g.InnerMethod.Cg, 1e-12, 5, 30))
+    monkeypatch.setenv("GADI_CHECK_SS", "1")
+    res = g.gadi_ir_solve(S, b, g.hss_split(S), gcfg)
+    monkeypatch.delenv("GADI_CHECK_SS")
+    cfg = Config.make(alpha=alpha, xi=1e-20, u_r=fmt, method=CG, tol_epsilon=1e-12, max_inner_iters=5,
+                      stall_window=400, accum=1 if accum else 0, max_outer_iters=8)
+    wx, wrep, _ = orc.solve(A, b, cfg)
+    assert res.report.outer_iters == wrep.outer_iters
+    assert same(res.x, wx)
