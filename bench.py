@@ -8,8 +8,8 @@ residual 1e-10 (xi = 1e-20): FP64 outer residual/update, inner CG on H and
 GMRES on S on the device. Workloads (BASELINE.json configs):
   c3 (default, the north star's target): 3D convection-diffusion n=512
      (N = 134,217,728), beta=100, FP16 storage / FP32 arithmetic inner, FP64
-     outer, alpha=0.24, omega=1, CG/GMRES(30) with eps=1e-12, max_inner=5
-     (the fastest time-to-solution of an alpha x max_inner sweep on B200).
+     outer, alpha=0.22, omega=0.25, CG/GMRES(30) with eps=1e-12, max_inner=7
+     (the fastest time-to-solution of an (alpha, omega, max_inner) sweep on B200).
   c2: n=256 (N = 16,777,216), beta=10, FP32 inner, alpha=0.07, max_inner=10 (swept, round 2).
   c1: the reference's own CPU case: build_convdiff3d(32) (beta=1), FP16 inner
      through its default inner method (BandLU, lu_direct), alpha=0.1; the
@@ -46,7 +46,7 @@ WORKLOADS = {
     # FP16 inner through the reference's default inner method (BandLU, lu_direct), FP64 outer
     "c1": dict(n=32, beta=1.0, u_r=0, accum=0, method=0, alpha=0.1, eps=1e-2, max_inner=1000, restart=30,
                seed=0, lo=0.0, hi=1.0, s_r=4, name="convdiff3d n=32 beta=1 fp16 lu_direct inner (BandLU)"),
-    "c3": dict(n=512, beta=100.0, u_r=0, accum=1, alpha=0.24, eps=1e-12, max_inner=5, restart=30,
+    "c3": dict(n=512, beta=100.0, u_r=0, accum=1, alpha=0.22, omega=0.25, eps=1e-12, max_inner=7, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=2, name="convdiff3d n=512 beta=100 fp16-storage/fp32-accum inner"),
     "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.07, eps=1e-12, max_inner=10, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=4, name="convdiff3d n=256 beta=10 fp32 inner"),
@@ -58,7 +58,7 @@ WORKLOADS = {
 }
 # outer iterations the device solve needs for each workload (measured on B200,
 # profiles/); used only to project the CPU reference's time-to-solution
-OUTER_ITERS = {"c3": 775, "c2": 507, "c4": 28, "c1": 0}
+OUTER_ITERS = {"c3": 442, "c2": 507, "c4": 28, "c1": 0}
 
 
 def load_peaks():
@@ -177,7 +177,7 @@ def cpu_reference_sample(wl, full=False, outer=None):
         A = o.convdiff(ns, 6.0, -1.0 - r, -1.0 + r)
     _, b = o.make_rhs(A, wl["seed"], wl["lo"], wl["hi"])
     k1, k2 = (1, 2) if big else (1, 3)
-    cfg = Config.make(alpha=wl["alpha"], xi=1e-20, u_r=1, method=CG, tol_epsilon=wl["eps"],
+    cfg = Config.make(alpha=wl["alpha"], omega=wl.get("omega", 1.0), xi=1e-20, u_r=1, method=CG, tol_epsilon=wl["eps"],
                       max_inner_iters=wl["max_inner"], restart=wl["restart"])
     if use_ref:
         t_split, t1, t2, o1, o2 = Reference().solve_steps_timed(A, b, cfg, k1, k2)
@@ -369,7 +369,7 @@ def main():
     band = wl.get("kind") == "band"
     Nw = wl["N"] if band else wl["n"] ** 3
     lu = wl.get("method") == 0
-    cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": 1.0,
+    cfg_json = {"workload": wl["name"], "N": Nw, "alpha": wl["alpha"], "omega": wl.get("omega", 1.0),
                 "inner": "lu_direct(H, S)" if lu else "cg(H)/gmres(S)",
                 "max_inner": wl["max_inner"], "tol_epsilon": wl["eps"], "xi": 1e-20,
                 "l2": "inputs larger than L2 (x, b: 8N bytes each)",
@@ -435,7 +435,8 @@ def main():
     torch.cuda.synchronize()
     b_h = b.cpu().pin_memory()
     x_h = torch.empty(N, dtype=torch.float64).pin_memory()
-    cfg = g.GadiConfig(alpha=wl["alpha"], xi=1e-20, u_r=g.Precision(wl["u_r"]), accum=g.Accum(wl["accum"]),
+    cfg = g.GadiConfig(alpha=wl["alpha"], omega=wl.get("omega", 1.0), xi=1e-20, u_r=g.Precision(wl["u_r"]),
+                       accum=g.Accum(wl["accum"]),
                        inner=g.InnerSolverSpec(g.InnerMethod(wl.get("method", 1)), wl["eps"], wl["max_inner"],
                                                wl["restart"]))
     b_np = b_h.numpy()

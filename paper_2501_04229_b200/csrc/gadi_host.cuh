@@ -1249,6 +1249,8 @@ struct Engine final : EngineBase {
             else if (j == 2) few(std::integral_constant<int, 3>{});
             else if (j == 3) few(std::integral_constant<int, 4>{});
             else if (j == 4) few(std::integral_constant<int, 5>{});
+            else if (j == 5) few(std::integral_constant<int, 6>{});
+            else if (j == 6) few(std::integral_constant<int, 7>{});
             else k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
           } else {
             k_gm_cgs<T, C, V_><<<geo.nblk, nt, 0, s>>>(w, V, ldv, j, geo, rd, h->st);
@@ -1377,6 +1379,8 @@ struct Engine final : EngineBase {
             case 3: k_gm_update_few<T, C, V_, 3><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
             case 4: k_gm_update_few<T, C, V_, 4><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
             case 5: k_gm_update_few<T, C, V_, 5><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 6: k_gm_update_few<T, C, V_, 6><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
+            case 7: k_gm_update_few<T, C, V_, 7><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, geo, h->st); break;
             default: k_gm_update<T, C, V_><<<geo.nblk, nt, 0, s>>>(x, xz, V, ldv, j, geo, h->st);
           }
         } else {

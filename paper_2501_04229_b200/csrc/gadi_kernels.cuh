@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(256) k_gm_cgs(T* __restrict__ w, const T* __re
   if (grid_finish(w0, w1, g, rd, ss, dummy)) finish_red(EpiCgsNorm{j}, st, ss, dummy);
 }
 
-// k_gm_cgs for the first Arnoldi steps (NB = j + 1 <= 5 basis vectors): all of a segment's
+// k_gm_cgs for the first Arnoldi steps (NB = j + 1 <= 7 basis vectors): all of a segment's
 // loads are issued together, and with NB <= 2 the next segment's loads too (double buffer),
 // so at least four 16-byte loads per lane are in flight (the generic body has NB + 1: 198 us
 // for 0.8 GB at j = 0). Same per-element sequence and the same reduction tree.
@@ -1450,7 +1450,7 @@ __global__ void __launch_bounds__(256) k_gm_update(T* __restrict__ x, int x_zero
   or_flags(&st->flags, bad);
 }
 
-// k_gm_update for a short cycle (NB = j <= 5 basis vectors): every load of a segment is issued
+// k_gm_update for a short cycle (NB = j <= 7 basis vectors): every load of a segment is issued
 // before the first axpy (the generic body reads the vectors past a multiple of four one at a
 // time). Same sequence of rounded axpys per element.
 template <class T, class C, int VEC, int NB>

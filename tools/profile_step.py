@@ -21,7 +21,8 @@ sysx = g.CudaGadiSystem(S)
 xt = torch.empty(S.n_rows, dtype=torch.float64, device="cuda")
 b = torch.empty_like(xt); x = torch.empty_like(xt)
 sysx.make_rhs(wl["seed"], wl["lo"], wl["hi"], xt.data_ptr(), b.data_ptr())
-cfg = g.GadiConfig(alpha=wl["alpha"], xi=1e-20, u_r=g.Precision(wl["u_r"]), accum=g.Accum(wl["accum"]),
+cfg = g.GadiConfig(alpha=wl["alpha"], omega=wl.get("omega", 1.0), xi=1e-20, u_r=g.Precision(wl["u_r"]),
+                   accum=g.Accum(wl["accum"]),
                    inner=g.InnerSolverSpec(g.InnerMethod.Cg, wl["eps"], wl["max_inner"], wl["restart"]),
                    max_outer_iters=a.outer)
 for _ in range(a.repeat):
