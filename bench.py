@@ -10,7 +10,7 @@ GMRES on S on the device. Workloads (BASELINE.json configs):
      (N = 134,217,728), beta=100, FP16 storage / FP32 arithmetic inner, FP64
      outer, alpha=0.22, omega=0.25, CG/GMRES(30) with eps=1e-12, max_inner=7
      (the fastest time-to-solution of an (alpha, omega, max_inner) sweep on B200).
-  c2: n=256 (N = 16,777,216), beta=10, FP32 inner, alpha=0.07, max_inner=10 (swept, round 2).
+  c2: n=256 (N = 16,777,216), beta=10, FP32 inner, alpha=0.11, omega=0.25, max_inner=10 (swept, round 2).
   c1: the reference's own CPU case: build_convdiff3d(32) (beta=1), FP16 inner
      through its default inner method (BandLU, lu_direct), alpha=0.1; the
      reference arm times its whole solve (measured, not projected).
@@ -48,7 +48,7 @@ WORKLOADS = {
                seed=0, lo=0.0, hi=1.0, s_r=4, name="convdiff3d n=32 beta=1 fp16 lu_direct inner (BandLU)"),
     "c3": dict(n=512, beta=100.0, u_r=0, accum=1, alpha=0.22, omega=0.25, eps=1e-12, max_inner=7, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=2, name="convdiff3d n=512 beta=100 fp16-storage/fp32-accum inner"),
-    "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.07, eps=1e-12, max_inner=10, restart=30,
+    "c2": dict(n=256, beta=10.0, u_r=1, accum=0, alpha=0.11, omega=0.25, eps=1e-12, max_inner=10, restart=30,
                seed=1, lo=-1.0, hi=1.0, s_r=4, name="convdiff3d n=256 beta=10 fp32 inner"),
     # BASELINE configs[3]: general nonsymmetric CSR, N = 2^24, 26 off-diagonals per row
     # uniform within +-4096 (seed 2), diagonal 1.1 x row abs sum; generated + split on the device
@@ -58,7 +58,7 @@ WORKLOADS = {
 }
 # outer iterations the device solve needs for each workload (measured on B200,
 # profiles/); used only to project the CPU reference's time-to-solution
-OUTER_ITERS = {"c3": 442, "c2": 507, "c4": 28, "c1": 0}
+OUTER_ITERS = {"c3": 442, "c2": 474, "c4": 28, "c1": 0}
 
 
 def load_peaks():
